@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""QuickPrefill benchmark: pruned-prefill tokens/s on 1..8 B200s (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1]): Qwen2.5-VL-7B-shaped layer (28 Q / 4 KV heads, head_dim 128), 256 frames x 256
+tokens per GPU, groups of 16 frames (16 groups x 4096 tokens), key-norm pruning per KV head at rho 0.5, bf16.
+A step = one pruned-prefill layer over every group: causal GQA attention (tcgen05) -> key-norm scores -> top-k ->
+KV compaction into the persistent cache; for N > 1 followed by the NCCL all-gather (per-rank broadcast) that
+assembles the replicated pruned cache.  Weak scaling: each GPU owns 16 groups.  The projection GEMM is not part
+of the path; Q/K/V are synthetic bf16 generated in HBM before timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CFG = dict(workload="qwen2.5-vl-7b layer, 256 frames x 256 tok/GPU, 16 frames/group, key-norm rho=0.5 per KV head",
+           frames_per_gpu=256, tokens_per_frame=256, frames_per_group=16, n_q=28, n_kv=4, d_h=128, rho=0.5,
+           layers=1)
+METRIC = "pruned-prefill tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def flops_attention(sizes, n_q, d):
+    return float(sum(4.0 * d * n_q * n * (n + 1) / 2 for n in sizes))
+
+
+def bytes_prune(plan, n_kv, d):
+    T, R = plan.total_tokens, plan.total_rows
+    score = T * n_kv * (d * 2 + 8)
+    select = T * n_kv * 8 + R * n_kv * 4
+    gather = R * n_kv * (4 * d * 2 + 8 + 4)
+    return float(score + select + gather)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while the timed region runs."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [[x.strip() for x in line.split(",")] for line in out.splitlines() if line.strip()]
+        rows = [r for r in rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        reasons = set()
+        for r in rows:
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
+                                 r[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("[N/A]", ""))}
+
+
+# ------------------------------------------------------------------------------------------------ CPU baseline
+def cpu_sample(seconds: float, cores: int):
+    """Bounded CPU sample of the same workload on the host cores: the reference's prune path (oracle/_ref
+    prune_group per KV-head slice, when built) + the oracle C port's double attention on a strided row sample of one
+    4096-token group (the reference has no attention code).  Returns (tokens/s, kind, description)."""
+    import torch  # noqa: F401  (threads)
+    from oracle import oracle as O
+
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    N, n_q, n_kv, d = CFG["frames_per_group"] * CFG["tokens_per_frame"], CFG["n_q"], CFG["n_kv"], CFG["d_h"]
+    q = O.bf16_to_f32(O.synth_bf16(1, 3, 0, 0, N, n_q, d, False)).reshape(N, n_q, d)
+    k = O.bf16_to_f32(O.synth_bf16(1, 1, 0, 0, N, n_kv, d, True)).reshape(N, n_kv, d)
+    v = O.bf16_to_f32(O.synth_bf16(1, 2, 0, 0, N, n_kv, d, False)).reshape(N, n_kv, d)
+    scale = 1 / math.sqrt(d)
+    # probe, then size the strided sample to ~seconds of attention work
+    t0 = time.perf_counter()
+    _, rows = O.attention_rows(q, k, v, n_q, n_kv, d, scale, 7, 1024)
+    probe = time.perf_counter() - t0
+    step = max(1, int(1024 * probe / max(1e-3, 0.8 * seconds)))
+    t0 = time.perf_counter()
+    _, rows = O.attention_rows(q, k, v, n_q, n_kv, d, scale, step // 2, step)
+    t_attn = (time.perf_counter() - t0) / rows  # seconds per query token (all heads), unbiased over the group
+    kind = "port"
+    t0 = time.perf_counter()
+    if O.ref is not None:
+        O.ref_prune_heads(k, v, None, N, n_kv, d, CFG["rho"])
+        kind = "reference"
+    else:
+        sc = O.score_norm(k, n_kv, d, True)
+        O.select_heads(sc, N, n_kv, O.retained_count(CFG["rho"], N))
+    t_prune = (time.perf_counter() - t0) / N
+    tps = 1.0 / (t_attn + t_prune)
+    desc = (f"1 group x {N} tokens: attention (oracle C port, fp64, OpenMP {cores} threads) on {rows} strided query "
+            f"rows (every {step}th) = {t_attn * 1e3:.2f} ms/token; prune "
+            f"({'reference prune_group per KV-head slice' if kind == 'reference' else 'oracle port'}, 1 thread) "
+            f"= {t_prune * 1e6:.2f} us/token; tokens/s = 1/(sum)")
+    return tps, kind, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_sample(2.0, cores)
+    vals, descs, kind = [], [], "port"
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tps, kind, desc = cpu_sample(4.0, cores)
+        vals.append(tps)
+        descs.append(desc)
+    wall = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    n_tok = CFG["frames_per_gpu"] * CFG["tokens_per_frame"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n_tok / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": CFG["workload"], **{k: v for k, v in CFG.items()
+                                                                         if k != "workload"}},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": descs[-1]},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_16175_b200 as qp
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2505_16175_b200.distributed import allgather_cache, segment_bounds
+
+    c = CFG
+    n_q, n_kv, d, rho = c["n_q"], c["n_kv"], c["d_h"], c["rho"]
+    plan = qp.GroupPlan.plan(c["frames_per_gpu"] * world, c["frames_per_group"], c["tokens_per_frame"], rho, world)
+    local_plan = plan.shard(rank, world)
+    g = local_plan.to(dev)
+    gidx0 = int(plan.rank_begin[rank])
+    sizes = [int(s) for s in local_plan.sizes]
+    q = torch.cat([qp.synth_bf16(1, 3, 0, gidx0 + i, n, n_q, d, False, dev) for i, n in enumerate(sizes)])
+    k = torch.cat([qp.synth_bf16(1, 1, 0, gidx0 + i, n, n_kv, d, True, dev) for i, n in enumerate(sizes)])
+    v = torch.cat([qp.synth_bf16(1, 2, 0, gidx0 + i, n, n_kv, d, False, dev) for i, n in enumerate(sizes)])
+    buf = qp.LayerBuffers.allocate(local_plan, n_q, n_kv, d, True, dev, cache_rows=plan.total_rows)
+    bounds = segment_bounds(plan, world)
+    row_base = local_plan.row_base
+    scale = 1 / math.sqrt(d)
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    attn_ev, prune_ev = [], []
+    unit = n_kv * d
+
+    def step(record: bool):
+        a0, a1, p1 = ev(), ev(), ev()
+        a0.record(stream)
+        qp.attention(q, k, v, g, n_q, n_kv, scale, out=buf.o)
+        a1.record(stream)
+        kc = buf.k_cache[row_base * unit:]
+        vc = buf.v_cache[row_base * unit:]
+        og = buf.origin[row_base * n_kv:]
+        qp.lib.qvk_prune(stream.cuda_stream, g.ref, k.data_ptr(), v.data_ptr(),
+                         qp._lib.QVK_BF16, n_kv, d, int(qp.Scorer.key_norm_small), rho, None, 0, n_kv,
+                         buf.scores.data_ptr(), buf.idx.data_ptr(), kc.data_ptr(), vc.data_ptr(), og.data_ptr())
+        p1.record(stream)
+        if world > 1:
+            allgather_cache([buf.k_cache, buf.v_cache, buf.origin], bounds, [unit, unit, n_kv])
+        if record:
+            attn_ev.append((a0, a1))
+            prune_ev.append((a1, p1))
+
+    sampler = ClockSampler(local)
+    for _ in range(args.warmup):
+        step(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = ev(), ev()
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    clocks = sampler.stop()
+    if clocks["samples"] < 3:  # timed region shorter than the sampling period: probe the same step for ~1 s
+        sampler = ClockSampler(local)
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 1.2:
+            for _ in range(20):
+                step(False)
+            torch.cuda.synchronize()
+        clocks = sampler.stop()
+        clocks["note"] = "sampled over a 1.2 s run of the same step right after the timed region"
+    attn_ms = [a.elapsed_time(b) for a, b in attn_ev]
+    prune_ms = [a.elapsed_time(b) for a, b in prune_ev]
+    el = torch.tensor([elapsed_ms, statistics.mean(attn_ms), statistics.mean(prune_ms)], device=dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    elapsed_ms, attn_avg, prune_avg = el.tolist()
+    total_tokens = plan.total_tokens
+    value = total_tokens * args.steps / (elapsed_ms / 1e3)
+
+    # ---- e2e through the C ABI with host buffers (H2D of this step's Q/K/V, D2H of the pruned cache) ----
+    e2e = None
+    if not args.no_e2e:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        out_k = torch.empty(buf.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+        out_v = torch.empty_like(out_k).pin_memory()
+        out_o = torch.empty(buf.origin.numel(), dtype=torch.int64).pin_memory()
+
+        def e2e_step():
+            q.copy_(hq, non_blocking=True)
+            k.copy_(hk, non_blocking=True)
+            v.copy_(hv, non_blocking=True)
+            qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, buffers=buf, cache_row_offset=row_base)
+            if world > 1:
+                allgather_cache([buf.k_cache, buf.v_cache, buf.origin], bounds, [unit, unit, n_kv])
+            out_k.copy_(buf.k_cache, non_blocking=True)
+            out_v.copy_(buf.v_cache, non_blocking=True)
+            out_o.copy_(buf.origin, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv))
+        d2h = sum(x.numel() * x.element_size() for x in (out_k, out_v, out_o))
+        e2e = {"value": total_tokens * args.steps / (t.item() / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "qvk_prefill_layer (C ABI) with pinned host Q/K/V in, pruned cache out"}
+
+    hbm, tf_burst, tf_sust, peak_src = peaks()
+    fl = flops_attention(sizes, n_q, d)
+    achieved = fl / (attn_avg / 1e3) / 1e12
+    prof = ROOT / "profiles" / "ncu_attention_summary.json"
+    traffic = None
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    pb = bytes_prune(local_plan, n_kv, d)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": c["workload"], "tokens_per_gpu": local_plan.total_tokens,
+                       "groups_per_gpu": local_plan.n_groups, "group_tokens": sizes[0], "n_q": n_q, "n_kv": n_kv,
+                       "head_dim": d, "rho": rho, "scorer": "key_norm_small", "pruning": "per KV head",
+                       "layers": c["layers"], "parallelism": f"group-sharded x{world}",
+                       "l2": "inputs larger than L2 (Q+K+V %.0f MB per GPU per step)" %
+                             ((q.numel() + k.numel() + v.numel()) * 2 / 1e6)},
+            "roofline": {"kernel": "attention_fwd_kernel (tcgen05)", "bound": "tensor", "achieved": achieved,
+                         "peak": tf_burst, "unit": "TFLOP/s", "frac": achieved / tf_burst, "traffic": traffic,
+                         "peak_source": peak_src + " burst", "flop_per_launch": fl,
+                         "avg_launch_ms": attn_avg},
+            "secondary": {"kernels": "score+select+gather (qvk_prune)", "avg_ms": prune_avg,
+                          "algorithmic_bytes": pb, "achieved_gbs": pb / (prune_avg / 1e3) / 1e9,
+                          "hbm_peak_gbs": hbm, "frac": pb / (prune_avg / 1e3) / 1e9 / hbm},
+            "clocks": clocks, "e2e": e2e, "gpu_launches": 4 * args.steps,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cores = os.cpu_count() or 1
+            tps, kind, desc = cpu_sample(args.cpu_seconds, cores)
+            line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": kind, "sample": desc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,168 @@
+/* qvk.h — C ABI of the B200-native (sm_100a) QuickPrefill hot path.
+ *
+ * The reference (/root/reference/proj) exposes QuickPrefill only as the C++ API of include/qv/prefill.hpp
+ * (std::span / std::vector / exceptions, no C ABI).  This header is the thin C layer underneath it:
+ *   - paper_2505_16175_b200/csrc/shim/prefill_shim.cpp implements the UNCHANGED qv:: API of prefill.hpp on top
+ *     of these entry points (that shim is the drop-in for src/prefill.cpp — see INTEGRATION.md);
+ *   - Python (ctypes) and C callers use them directly for the batched, device-resident path.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "_d" pointers are device (HBM) pointers, others are host pointers.
+ *   - Device entry points are asynchronous and stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream).  They never synchronise unless documented.
+ *   - Return 0 on success.  QVK_E_INVALID (-1) carries the reference's qv::Error text verbatim (the shim throws
+ *     qv::Error(qvk_last_error())); QVK_E_CUDA (-2) a CUDA runtime failure; QVK_E_UNSUPPORTED (-3) a shape this
+ *     build has no kernel for.  qvk_last_error() is thread-local.
+ *   - Groups (prefill.hpp:27-35 TokenGroup) are described by qvk_groups: group g owns token rows
+ *     [tok_off[g], tok_off[g+1]) of the q/k/v tensors and cache rows [row_off[g], row_off[g]+keep[g]).
+ *   - K/V/Q rows are (tokens, heads, width) row-major ("NHD", prefill.hpp:49-51).  Scores are (group, head, token):
+ *     scores[heads*tok_off[g] + h*N_g + i].  Selected indices and the cache are (cache row, head):
+ *     idx[(row_off[g]+r)*heads + h], k_cache[((row_off[g]+r)*heads + h)*width + c], origin likewise.
+ *     Per-token pruning (the reference's unchanged semantics, prefill.hpp:105-108) is heads = 1, width = n_h*d_h.
+ */
+#ifndef QVK_H
+#define QVK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* qvk_stream_t; /* == cudaStream_t */
+
+enum {
+    QVK_OK = 0,
+    QVK_E_INVALID = -1,
+    QVK_E_CUDA = -2,
+    QVK_E_UNSUPPORTED = -3,
+};
+
+enum { QVK_F32 = 0, QVK_BF16 = 1 };
+
+/* Values 0..2 equal qv::Scorer (prefill.hpp:37); 3 is the SnapKV observation-window scorer (north star (3)). */
+enum { QVK_KEY_NORM_SMALL = 0, QVK_VALUE_NORM = 1, QVK_ATTENTION_SCORE = 2, QVK_SNAPKV = 3 };
+
+typedef struct {
+    int32_t n_groups;            /* G >= 1 */
+    int64_t max_tokens;          /* max_g N_g (launch sizing) */
+    int64_t total_tokens;        /* tok_off[G] (rows of q/k/v) */
+    int64_t total_rows;          /* row_off[G] (sum of keep) */
+    const int64_t* tok_off_d;    /* [G+1] token row offsets into q/k/v */
+    const int64_t* keep_d;       /* [G]   retained tokens per group (= retained_count(rho, N_g)) */
+    const int64_t* row_off_d;    /* [G+1] cache row offsets (exclusive prefix sum of keep) */
+    const uint64_t* first_token_d; /* [G] global token id of the group's row 0 (prefill.hpp:29) */
+} qvk_groups;
+
+const char* qvk_last_error(void);
+int qvk_version(void);
+int qvk_device_count(int* out);
+
+/* ---- device memory / stream plumbing (so C++ callers such as the shim need no CUDA headers) ---------------- */
+int qvk_malloc(void** out_d, size_t bytes);
+int qvk_free(void* p_d);
+int qvk_memcpy_h2d(void* dst_d, const void* src, size_t bytes, qvk_stream_t stream);
+int qvk_memcpy_d2h(void* dst, const void* src_d, size_t bytes, qvk_stream_t stream);
+int qvk_stream_sync(qvk_stream_t stream);
+
+/* ---- (a1) group scheduler, host side ------------------------------------------------------------------------- */
+/* prefill.cpp:325-328 group_count; "frames_per_group must be >= 1" on fpg == 0. */
+int qvk_group_count(uint64_t total_frames, uint32_t frames_per_group, uint64_t* out);
+/* prefill.cpp:235-238 retained_count: min(n, max(1, llround(rho*n))). */
+size_t qvk_retained_count(double rho, size_t token_count);
+/* prefill.cpp:65-67 PruneConfig::validate: "retention ratio must be in (0, 1]". */
+int qvk_validate_rho(double rho);
+/* Plans G = ceil(F/fpg) groups of tpf tokens per frame (prefill.cpp:170-183, last group short), retained counts
+ * and cache offsets, and a contiguous partition of the groups over `world` ranks balanced by attention cost
+ * (sum N_g^2): rank r owns groups [rank_begin[r], rank_begin[r+1]).  Arrays: tok_off/row_off G+1, keep G,
+ * rank_begin world+1 (may be NULL when world <= 1).  Call with tok_off == NULL to get G only (in *n_groups). */
+int qvk_plan_groups(uint64_t total_frames, uint32_t frames_per_group, uint32_t tokens_per_frame, double rho,
+                    int32_t world, uint64_t* n_groups, int64_t* tok_off, int64_t* keep, int64_t* row_off,
+                    int32_t* rank_begin);
+
+/* ---- (a5)/(a6)/(a7) importance scores --------------------------------------------------------------------------- */
+/* key_norm_small / value_norm (prefill.cpp:200-212): per (token, head) -+sqrt(sum_j double(x_j)^2) summed
+ * sequentially over j = 0..width-1 in double — bit-identical to the reference.  attention_score
+ * (prefill.cpp:213-230, heads must be 1): (sum_t sum_j double(k_j)*q_tj)/(T*n_h) in the reference's order,
+ * bit-identical; `n_h` is only the divisor.  Shape errors carry the reference's messages. */
+int qvk_score(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, const void* v_d, int dtype,
+              int32_t heads, int32_t width, int32_t scorer, const float* text_query_d, int64_t text_count,
+              int32_t n_h, double* scores_d);
+
+/* SnapKV observation-window scores per KV head: window = the last min(window, N_g) tokens of
+ * the group; s[h, j] = sum over the n_q/n_kv query heads of h and the window rows r of causal
+ * softmax_j(scale * q_r . k_j); optional average pooling of odd width `pool` (1 = none).  bf16 q/k, fp32 math,
+ * scores written as double in the qvk_score layout (heads = n_kv). */
+int qvk_snapkv_score(qvk_stream_t stream, const qvk_groups* groups, const void* q_d, const void* k_d,
+                     int32_t n_q, int32_t n_kv, int32_t d_h, int32_t window, int32_t pool, float scale,
+                     double* scores_d);
+
+/* ---- (a9) top-k selection -------------------------------------------------------------------------------------- */
+/* Per (group, head): the keep[g] best scores under (score desc, index asc), -0.0 == +0.0, written ascending
+ * (prefill.cpp:240-253) to idx_d[(row_off[g]+r)*heads + h].  Exact radix select on the 64-bit keys. */
+int qvk_select(qvk_stream_t stream, const qvk_groups* groups, const double* scores_d, int32_t heads,
+               uint32_t* idx_d);
+
+/* ---- (a10)/(a11) KV compaction into the cache ------------------------------------------------------------------- */
+/* k_cache[(row_off[g]+r), h, :] = k[tok_off[g] + idx[...], h, :] (same for v); origin = first_token[g] + idx
+ * (prefill.cpp:277-280, 304-308).  idx_d == NULL means the rho == 1 identity (prefill.cpp:263-270): every row kept
+ * in order (requires keep[g] == N_g).  origin_d may be NULL. */
+int qvk_gather(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, const void* v_d, int dtype,
+               int32_t heads, int32_t width, const uint32_t* idx_d, void* k_cache_d, void* v_cache_d,
+               uint64_t* origin_d);
+
+/* score -> select -> gather (prune_group for every group of the batch).  scores_ws_d must hold
+ * heads * tok_off[G] doubles and idx_ws_d total_rows * heads uint32 (either may be NULL: then the call allocates
+ * and frees stream-ordered scratch).  rho == 1 takes the identity path without scoring (prefill.cpp:263-270). */
+int qvk_prune(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, const void* v_d, int dtype,
+              int32_t heads, int32_t width, int32_t scorer, double rho, const float* text_query_d,
+              int64_t text_count, int32_t n_h, double* scores_ws_d, uint32_t* idx_ws_d, void* k_cache_d,
+              void* v_cache_d, uint64_t* origin_d);
+
+/* ---- (a4) per-group causal GQA attention ------------------------------------------------------------------------ */
+/* O[i, h, :] = sum_{j <= i, same group} softmax_j(scale * Q[i,h].K[j,h/(n_q/n_kv)]) V[j, ...]; bf16 in/out, fp32
+ * accumulate.  tcgen05/TMEM/TMA kernel; d_h == 128 only (QVK_E_UNSUPPORTED otherwise). */
+int qvk_attention(qvk_stream_t stream, const qvk_groups* groups, const void* q_d, const void* k_d,
+                  const void* v_d, int32_t n_q, int32_t n_kv, int32_t d_h, float scale, void* o_d);
+
+/* ---- one full pruned-prefill layer for all groups of the batch -------------------------------------------------- */
+typedef struct {
+    int32_t n_q, n_kv, d_h;   /* GQA shape; K/V rows are (tokens, n_kv, d_h) */
+    int32_t scorer;           /* QVK_KEY_NORM_SMALL / QVK_VALUE_NORM / QVK_SNAPKV */
+    int32_t per_head;         /* 1: prune each KV head independently (north star (4)); 0: per token (reference) */
+    double rho;               /* retention ratio (0, 1] */
+    float scale;              /* softmax scale, usually 1/sqrt(d_h) */
+    int32_t snap_window, snap_pool;
+} qvk_layer_params;
+
+/* attention -> score -> select -> gather for one layer.  scores_ws_d: n_kv * tok_off[G] doubles; idx_ws_d:
+ * total_rows * n_kv uint32 (NULL -> stream-ordered scratch). */
+int qvk_prefill_layer(qvk_stream_t stream, const qvk_groups* groups, const qvk_layer_params* p, const void* q_d,
+                      const void* k_d, const void* v_d, void* o_d, double* scores_ws_d, uint32_t* idx_ws_d,
+                      void* k_cache_d, void* v_cache_d, uint64_t* origin_d);
+
+/* ---- stand-in model pieces of the reference API (exact, for the drop-in shim) ----------------------------------- */
+/* prefill.cpp:21-30 seeded_matrix generated on the device, bit-identical (counter-based splitmix64). */
+int qvk_seeded_matrix(qvk_stream_t stream, uint64_t seed, uint32_t tag, uint32_t layer, size_t count, double scale,
+                      float* out_d);
+/* prefill.cpp:38-54 matmul: out(rows, d_out) = x(rows, d_in) * w(d_in, d_out), double accumulation in the
+ * reference's sequential order (no FMA) — bit-identical fp32 output. */
+int qvk_project_exact(qvk_stream_t stream, const float* x_d, int64_t rows, int32_t d_in, const float* w_d,
+                      int32_t d_out, float* out_d);
+/* prefill.cpp:123-168 tokenize_group body: frames are (n_frames, 3, height, width) uint8 slots; tokens
+ * (n_frames * tpf, d_model) fp32; embed (d_model, 3).  Bit-identical.  "tokenize: frame size not divisible into
+ * the patch grid" on a bad size. */
+int qvk_tokenize(qvk_stream_t stream, const uint8_t* frames_d, int64_t n_frames, uint32_t width, uint32_t height,
+                 uint32_t tokens_per_frame, const float* embed_d, int32_t d_model, float* tokens_d);
+/* prefill.cpp:116-121 */
+void qvk_patch_grid(uint32_t tokens_per_frame, uint32_t* rows, uint32_t* cols);
+
+/* ---- synthetic device-resident inputs (benchmark / tests; same bits as oracle qvo_synth_bf16) ------------------- */
+int qvk_synth_bf16(qvk_stream_t stream, uint64_t seed, uint32_t tag, uint32_t layer, uint64_t group, int64_t rows,
+                   int32_t heads, int32_t width, int32_t head_scale, void* out_d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QVK_H */

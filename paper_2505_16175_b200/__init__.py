@@ -1,0 +1,31 @@
+"""B200-native (sm_100a) QuickPrefill: group-wise prefill of video-frame tokens with per-group KV-cache pruning.
+
+The compute path is libqvk.so (hand-written CUDA behind include/qvk.h); this package is its host-side mirror of the
+reference interface (/root/reference/proj/include/qv/prefill.hpp).  Importing fails loudly when the library has
+not been built — there is no CPU fallback.
+"""
+from ._lib import QvError, header_symbols, lib  # noqa: F401  (raises ImportError if libqvk.so is missing)
+from .prefill import (  # noqa: F401
+    DeviceGroups,
+    GroupPlan,
+    LayerBuffers,
+    PrunedGroup,
+    PruneConfig,
+    Scorer,
+    attention,
+    gather,
+    group_count,
+    prefill_layer,
+    prune,
+    prune_group,
+    retained_count,
+    score,
+    score_tokens,
+    scorer_from_name,
+    select,
+    snapkv_scores,
+    synth_bf16,
+    top_k_indices,
+)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

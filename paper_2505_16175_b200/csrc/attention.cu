@@ -1,0 +1,391 @@
+// (a4) Per-group causal GQA attention prefill on sm_100a: TMA -> smem ring -> tcgen05.mma into TMEM, online
+// softmax in registers, P kept in TMEM (TS-MMA), no reference counterpart.
+//
+// Work unit = (group g, query head hq, query-tile pair p): two 128-row query tiles (rows [256p, 256p+256) of the
+// group) share every K/V tile the CTA streams (the second tile needs one extra, diagonal, K/V tile).
+//
+// Warp roles (320 threads, 1 CTA per SM):
+//   warps 0-3  softmax for query tile 0   (thread = one TMEM lane = one query row; the whole S row is thread-local)
+//   warps 4-7  softmax for query tile 1
+//   warp  8    TMA producer  (Q0, Q1 once; then K0, V0, K1, V1, ... through a 4-stage 32 KB ring)
+//   warp  9    MMA issuer    (one elected lane) + TMEM owner (512 columns: S0 | S1 | O0 | O1, 128 each)
+// MMA order per K/V step j (FA4-style ping-pong, so the tensor pipe works on one tile while the other's softmax
+// runs):  PV0(j)  S0(j+1)  PV1(j)  S1(j+1).  P_t(j) (bf16) is written by the softmax warps over the first 64 columns
+// of S_t and consumed as the TMEM A operand of PV_t(j); tcgen05 ops execute in issue order, so S_t(j+1) (issued
+// after PV_t(j)) never overwrites P_t(j) early, and the commit of S_t(j+1) also proves PV_t(j) retired — which is
+// what lets the softmax warps rescale O_t in TMEM (lazily, only when a row max grows by > 2^8) without another
+// barrier.
+//
+// Layouts: Q/K/V are (tokens, heads, 128) bf16.  Each 128x128 tile lands in smem as two 128-row x 128-byte
+// SWIZZLE_128B chunks (d 0..63, d 64..127) via 3-D TMA boxes {64, 1, 128}.  S = Q K^T uses K-major A and B
+// descriptors (SBO 1024 B); O += P V uses V as an MN-major B operand (LBO 16 KB between the d chunks, SBO 1024 B).
+// Algorithmic FLOPs per (group, q head): 4 * d * N (N + 1) / 2 (causal, diagonal included; masked work uncredited).
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace qvk {
+namespace {
+
+constexpr int kBM = 128;                      // query rows per tile
+constexpr int kBN = 128;                      // kv rows per tile
+constexpr int kD = 128;                       // head dim
+constexpr int kStages = 4;                    // K/V ring depth
+constexpr uint32_t kTileBytes = kBM * kD * 2; // 32 KB (one bf16 128x128 tile)
+constexpr uint32_t kChunkBytes = kTileBytes / 2;
+constexpr int kThreads = 384;                 // 3 warpgroups: softmax0, softmax1, {TMA, MMA, 2 spare}
+constexpr int kTmaWarp = 8;
+constexpr int kMmaWarp = 9;
+constexpr int kRegsSoftmax = 224;             // 2*128*224 + 128*56 = 64512 <= 65536 registers per SM
+constexpr int kRegsProducer = 56;
+constexpr float kRescaleThreshold = 8.0f;     // log2 units: rescale O only when a row max grows by > 256x
+
+struct AttnParams {
+    const int64_t* tok_off;
+    int n_groups;
+    int n_q;
+    int n_kv;
+    int pairs_max;
+    float scale_log2;
+    __nv_bfloat16* o;
+};
+
+struct Barriers {
+    uint64_t q_full;
+    uint64_t kv_full[kStages];
+    uint64_t kv_empty[kStages];
+    uint64_t s_full[2];
+    uint64_t p_full[2];
+    uint64_t o_done[2];
+    uint32_t tmem_base;
+};
+
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + (2 + kStages) * kTileBytes + sizeof(Barriers);
+
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_addr, int kk) {
+    // k-step kk (16 elements) of a K-major SW128 tile: chunk kk/4, +32 B per step inside the 128-byte row.
+    return ptx::umma_desc_sw128(tile_addr + (kk >> 2) * kChunkBytes + (kk & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t mnmajor_desc(uint32_t tile_addr, int kk) {
+    // k-step kk (16 kv rows) of the MN-major V tile: +16 rows * 128 B; the two 64-wide d chunks are LBO apart.
+    return ptx::umma_desc_sw128(tile_addr + kk * 16 * 128, kChunkBytes, 1024);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                       // Q0, Q1
+    uint8_t* sKV = smem + 2 * kTileBytes;     // ring
+    Barriers* bar = reinterpret_cast<Barriers*>(smem + (2 + kStages) * kTileBytes);
+
+    // ---- work unit (heaviest query-tile pairs first) ----
+    const int per_pair = p.n_groups * p.n_q;
+    const int pair = p.pairs_max - 1 - static_cast<int>(blockIdx.x) / per_pair;
+    const int rem = static_cast<int>(blockIdx.x) % per_pair;
+    const int g = rem / p.n_q;
+    const int hq = rem - g * p.n_q;
+    const int64_t tok0 = p.tok_off[g];
+    const int n = static_cast<int>(p.tok_off[g + 1] - tok0);
+    const int mt0 = 2 * pair, mt1 = 2 * pair + 1;
+    if (mt0 * kBM >= n) return;  // CTA-uniform, before any barrier
+    const int n0 = mt0 + 1;                          // K/V tiles of query tile 0 (last one is diagonal)
+    const int n1 = mt1 * kBM < n ? mt1 + 1 : 0;      // K/V tiles of query tile 1 (0: tile absent)
+    const int nkv = n1 ? n1 : n0;
+    const int hk = hq / (p.n_q / p.n_kv);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar->q_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&bar->kv_full[s], 1);
+            ptx::mbar_init(&bar->kv_empty[s], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            ptx::mbar_init(&bar->s_full[t], 1);
+            ptx::mbar_init(&bar->p_full[t], 128);
+            ptx::mbar_init(&bar->o_done[t], 1);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == kMmaWarp) ptx::tmem_alloc<512>(&bar->tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = bar->tmem_base;
+
+    // Register rebalancing (warpgroup-uniform): producer/issuer warpgroup gives registers to the softmax ones.
+    if (warp >= 8) {
+      ptx::setmaxnreg_dec<kRegsProducer>();
+      if (warp == kTmaWarp) {
+        // ===================== TMA producer =====================
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tm_q);
+            ptx::prefetch_tmap(&tm_k);
+            ptx::prefetch_tmap(&tm_v);
+            ptx::mbar_arrive_expect_tx(&bar->q_full, n1 ? 2 * kTileBytes : kTileBytes);
+            const int r0 = static_cast<int>(tok0) + mt0 * kBM;
+            ptx::tma_load_3d(sQ, &tm_q, &bar->q_full, 0, hq, r0);
+            ptx::tma_load_3d(sQ + kChunkBytes, &tm_q, &bar->q_full, 64, hq, r0);
+            if (n1) {
+                ptx::tma_load_3d(sQ + kTileBytes, &tm_q, &bar->q_full, 0, hq, r0 + kBM);
+                ptx::tma_load_3d(sQ + kTileBytes + kChunkBytes, &tm_q, &bar->q_full, 64, hq, r0 + kBM);
+            }
+            for (int item = 0; item < 2 * nkv; ++item) {
+                const int st = item % kStages;
+                ptx::mbar_wait(&bar->kv_empty[st], ((item / kStages) & 1) ^ 1);
+                const CUtensorMap* map = (item & 1) ? &tm_v : &tm_k;
+                const int row = static_cast<int>(tok0) + (item >> 1) * kBN;
+                uint8_t* dst = sKV + st * kTileBytes;
+                ptx::mbar_arrive_expect_tx(&bar->kv_full[st], kTileBytes);
+                ptx::tma_load_3d(dst, map, &bar->kv_full[st], 0, hk, row);
+                ptx::tma_load_3d(dst + kChunkBytes, map, &bar->kv_full[st], 64, hk, row);
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        // ===================== MMA issuer =====================
+        if (ptx::elect_one()) {
+            constexpr uint32_t kIdS = ptx::idesc_bf16_f32(kBM, kBN, false, false);
+            constexpr uint32_t kIdPV = ptx::idesc_bf16_f32(kBM, kD, false, true);
+            const uint32_t q_addr = ptx::smem_u32(sQ);
+            const uint32_t ring = ptx::smem_u32(sKV);
+            auto wait_item = [&](int item) -> uint32_t {
+                const int st = item % kStages;
+                ptx::mbar_wait(&bar->kv_full[st], (item / kStages) & 1);
+                ptx::tc_fence_after();
+                return ring + st * kTileBytes;
+            };
+            auto issue_s = [&](int t, uint32_t k_addr) {
+                const uint32_t qa = q_addr + t * kTileBytes;
+#pragma unroll
+                for (int kk = 0; kk < kD / 16; ++kk)
+                    ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
+            };
+            auto issue_pv = [&](int t, uint32_t v_addr, bool acc) {
+#pragma unroll
+                for (int kk = 0; kk < kBN / 16; ++kk)
+                    ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_addr, kk), kIdPV,
+                                (acc || kk > 0) ? 1u : 0u);
+            };
+
+            ptx::mbar_wait(&bar->q_full, 0);
+            ptx::tc_fence_after();
+            uint32_t k_addr = wait_item(0);
+            issue_s(0, k_addr);
+            ptx::mma_commit(&bar->s_full[0]);
+            if (n1) {
+                issue_s(1, k_addr);
+                ptx::mma_commit(&bar->s_full[1]);
+            }
+            ptx::mma_commit(&bar->kv_empty[0]);
+            for (int j = 0; j < nkv; ++j) {
+                const int v_item = 2 * j + 1;
+                const uint32_t v_addr = wait_item(v_item);
+                const bool more = j + 1 < nkv;
+                if (j < n0) {
+                    ptx::mbar_wait(&bar->p_full[0], j & 1);
+                    ptx::tc_fence_after();
+                    issue_pv(0, v_addr, j > 0);
+                    if (j == n0 - 1) ptx::mma_commit(&bar->o_done[0]);
+                }
+                uint32_t kn = 0;
+                if (more) kn = wait_item(v_item + 1);
+                if (j + 1 < n0) {
+                    issue_s(0, kn);
+                    ptx::mma_commit(&bar->s_full[0]);
+                }
+                if (j < n1) {
+                    ptx::mbar_wait(&bar->p_full[1], j & 1);
+                    ptx::tc_fence_after();
+                    issue_pv(1, v_addr, j > 0);
+                    if (j == n1 - 1) ptx::mma_commit(&bar->o_done[1]);
+                }
+                ptx::mma_commit(&bar->kv_empty[v_item % kStages]);
+                if (j + 1 < n1) {
+                    issue_s(1, kn);
+                    ptx::mma_commit(&bar->s_full[1]);
+                }
+                if (more) ptx::mma_commit(&bar->kv_empty[(v_item + 1) % kStages]);
+            }
+        }
+      }
+    } else {
+        ptx::setmaxnreg_inc<kRegsSoftmax>();
+        // ===================== softmax / correction / epilogue =====================
+        const int t = warp >> 2;                 // query tile handled by this warpgroup
+        const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+        const int row = quarter * 32 + lane;
+        const int mt = t ? mt1 : mt0;
+        const int nt = t ? n1 : n0;
+        if (nt > 0) {
+            const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+            const uint32_t s_col = tmem + lane_off + t * 128;
+            const uint32_t o_col = tmem + lane_off + 256 + t * 128;
+            const float sl2 = p.scale_log2;
+            float m_ref = -INFINITY, l = 0.f;
+            for (int j = 0; j < nt; ++j) {
+                ptx::mbar_wait(&bar->s_full[t], j & 1);
+                ptx::tc_fence_after();
+                float x[128];
+                QVK_TMEM_LD32F(s_col + 0, (x + 0));
+                QVK_TMEM_LD32F(s_col + 32, (x + 32));
+                QVK_TMEM_LD32F(s_col + 64, (x + 64));
+                QVK_TMEM_LD32F(s_col + 96, (x + 96));
+                ptx::tmem_ld_wait();
+                if (j == mt) {
+#pragma unroll
+                    for (int c = 0; c < 128; ++c)
+                        if (c > row) x[c] = -INFINITY;
+                }
+                float mx0 = x[0], mx1 = x[1], mx2 = x[2], mx3 = x[3];
+#pragma unroll
+                for (int c = 4; c < 128; c += 4) {
+                    mx0 = fmaxf(mx0, x[c]);
+                    mx1 = fmaxf(mx1, x[c + 1]);
+                    mx2 = fmaxf(mx2, x[c + 2]);
+                    mx3 = fmaxf(mx3, x[c + 3]);
+                }
+                const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+                const float m_new = mx * sl2;
+                if (j == 0) {
+                    m_ref = m_new;
+                } else {
+                    const bool need = m_new > m_ref + kRescaleThreshold;
+                    if (__any_sync(0xffffffffu, need)) {
+                        const float m_upd = need ? m_new : m_ref;
+                        const float f = ptx::ex2(m_ref - m_upd);
+                        l *= f;
+                        m_ref = m_upd;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t o[32];
+                            QVK_TMEM_LD32(o_col + c * 32, o);
+                            ptx::tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                            QVK_TMEM_ST32(o_col + c * 32, o);
+                        }
+                        ptx::tmem_st_wait();
+                    }
+                }
+                const float neg = -m_ref;
+                float sum = 0.f;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {  // 64 probabilities -> 32 packed bf16x2 columns per store
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const float p0 = ptx::ex2(fmaf(x[64 * half + 2 * c], sl2, neg));
+                        const float p1 = ptx::ex2(fmaf(x[64 * half + 2 * c + 1], sl2, neg));
+                        sum += p0 + p1;
+                        pk[c] = ptx::pack_bf16(p0, p1);
+                    }
+                    QVK_TMEM_ST32(s_col + 32 * half, pk);
+                }
+                l += sum;
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&bar->p_full[t]);
+            }
+            // ---- epilogue: O / l -> bf16 -> HBM ----
+            ptx::mbar_wait(&bar->o_done[t], 0);
+            ptx::tc_fence_after();
+            const float inv = 1.f / l;
+            const int qrow = mt * kBM + row;
+            __nv_bfloat16* dst = p.o + ((tok0 + qrow) * p.n_q + hq) * static_cast<int64_t>(kD);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t o[32];
+                QVK_TMEM_LD32(o_col + c * 32, o);
+                ptx::tmem_ld_wait();
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    pk[e] = ptx::pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+                if (qrow < n) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) d4[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// (tokens, heads, 128) bf16 viewed as a 3-D tensor {d, heads, tokens}; box {64, 1, 128}, 128-byte swizzle.
+bool make_map(CUtensorMap* m, const void* base, int heads, int64_t tokens) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(kD), static_cast<cuuint64_t>(heads),
+                          static_cast<cuuint64_t>(tokens)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(kD) * 2, static_cast<cuuint64_t>(heads) * kD * 2};
+    cuuint32_t box[3] = {64, 1, static_cast<cuuint32_t>(kBM)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, const void* v, int n_q,
+                     int n_kv, int d_h, float scale, void* o) {
+    if (d_h != kD) {
+        set_error("attention: only head_dim 128 is implemented (got " + std::to_string(d_h) + ")");
+        return QVK_E_UNSUPPORTED;
+    }
+    if (n_q <= 0 || n_kv <= 0 || n_q % n_kv != 0) QVK_INVALID("attention: n_q must be a positive multiple of n_kv");
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v) |
+         reinterpret_cast<uintptr_t>(o)) & 15)
+        QVK_INVALID("attention: q/k/v/o must be 16-byte aligned");
+    if (g->total_tokens == 0 || g->max_tokens == 0) return QVK_OK;
+    if (g->total_tokens > 0x7fffffff) QVK_INVALID("attention: more than 2^31 token rows");
+    CUtensorMap mq, mk, mv;
+    if (!make_map(&mq, q, n_q, g->total_tokens) || !make_map(&mk, k, n_kv, g->total_tokens) ||
+        !make_map(&mv, v, n_kv, g->total_tokens)) {
+        set_error("attention: cuTensorMapEncodeTiled failed");
+        return QVK_E_CUDA;
+    }
+    static bool attr = false;
+    if (!attr) {
+        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmemBytes)));
+        attr = true;
+    }
+    AttnParams prm;
+    prm.tok_off = g->tok_off_d;
+    prm.n_groups = g->n_groups;
+    prm.n_q = n_q;
+    prm.n_kv = n_kv;
+    const int64_t tiles = (g->max_tokens + kBM - 1) / kBM;
+    prm.pairs_max = static_cast<int>((tiles + 1) / 2);
+    prm.scale_log2 = scale * 1.4426950408889634f;
+    prm.o = static_cast<__nv_bfloat16*>(o);
+    const int64_t blocks = static_cast<int64_t>(prm.pairs_max) * g->n_groups * n_q;
+    if (blocks > 0x7fffffff) QVK_INVALID("attention: grid too large");
+    attention_fwd_kernel<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, stream>>>(mq, mk, mv, prm);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
+}  // namespace qvk

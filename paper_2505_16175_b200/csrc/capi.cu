@@ -1,0 +1,280 @@
+// extern "C" entry points of include/qvk.h: argument validation with the reference's error texts, the host-side
+// group scheduler, and the stream-ordered orchestration of the kernels (score.cu, select.cu, gather.cu,
+// attention.cu, snapkv.cu, exact.cu).  No computation of the path happens on the host.
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace qvk {
+
+thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int launch_score(cudaStream_t, const qvk_groups*, int64_t, const void*, const void*, int, int, int, int,
+                 const float*, int64_t, int, double*);
+int launch_select(cudaStream_t, const qvk_groups*, const double*, int, uint32_t*);
+int launch_gather(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const uint32_t*, void*,
+                  void*, uint64_t*);
+int launch_attention(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, int, float,
+                     void*);
+int launch_snapkv(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, int, int, float,
+                  double*);
+int launch_seeded_matrix(cudaStream_t, uint64_t, uint32_t, uint32_t, size_t, double, float*);
+int launch_project_exact(cudaStream_t, const float*, int64_t, int, const float*, int, float*);
+int launch_tokenize(cudaStream_t, const uint8_t*, int64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
+                    const float*, int, float*);
+int launch_synth_bf16(cudaStream_t, uint64_t, uint32_t, uint32_t, uint64_t, int64_t, int, int, int, void*);
+
+namespace {
+
+int check_groups(const qvk_groups* g) {
+    if (!g) QVK_INVALID("groups: null descriptor");
+    if (g->n_groups <= 0) QVK_INVALID("prefill: no token groups");  // prefill.cpp:317
+    if (!g->tok_off_d || !g->keep_d || !g->row_off_d) QVK_INVALID("groups: null offset array");
+    if (g->max_tokens < 0 || g->total_tokens < 0 || g->total_rows < 0) QVK_INVALID("groups: negative size");
+    return QVK_OK;
+}
+
+int check_rho(double rho) {
+    if (!(rho > 0.0 && rho <= 1.0)) QVK_INVALID("retention ratio must be in (0, 1]");  // prefill.cpp:65-67
+    return QVK_OK;
+}
+
+size_t retained(double rho, size_t n) {  // prefill.cpp:235-238
+    const auto rounded = static_cast<size_t>(std::llround(rho * static_cast<double>(n)));
+    return std::min(n, std::max<size_t>(1, rounded));
+}
+
+#define QVK_TRY(expr)                 \
+    do {                              \
+        const int _rc = (expr);       \
+        if (_rc != QVK_OK) return _rc; \
+    } while (0)
+
+}  // namespace
+}  // namespace qvk
+
+using namespace qvk;
+
+extern "C" {
+
+const char* qvk_last_error(void) { return g_last_error.c_str(); }
+int qvk_version(void) { return 1; }
+
+int qvk_device_count(int* out) {
+    QVK_CUDA_CHECK(cudaGetDeviceCount(out));
+    return QVK_OK;
+}
+
+int qvk_malloc(void** out, size_t bytes) {
+    *out = nullptr;
+    if (bytes == 0) return QVK_OK;
+    QVK_CUDA_CHECK(cudaMalloc(out, bytes));
+    return QVK_OK;
+}
+int qvk_free(void* p) {
+    if (p) QVK_CUDA_CHECK(cudaFree(p));
+    return QVK_OK;
+}
+int qvk_memcpy_h2d(void* dst, const void* src, size_t bytes, qvk_stream_t s) {
+    if (bytes) QVK_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return QVK_OK;
+}
+int qvk_memcpy_d2h(void* dst, const void* src, size_t bytes, qvk_stream_t s) {
+    if (bytes) QVK_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    return QVK_OK;
+}
+int qvk_stream_sync(qvk_stream_t s) {
+    QVK_CUDA_CHECK(cudaStreamSynchronize(s));
+    return QVK_OK;
+}
+
+// ---- (a1) group scheduler ---------------------------------------------------------------------------------------
+int qvk_group_count(uint64_t total_frames, uint32_t fpg, uint64_t* out) {
+    if (fpg == 0) QVK_INVALID("frames_per_group must be >= 1");  // prefill.cpp:326
+    *out = (total_frames + fpg - 1) / fpg;
+    return QVK_OK;
+}
+
+size_t qvk_retained_count(double rho, size_t n) { return retained(rho, n); }
+
+int qvk_validate_rho(double rho) { return check_rho(rho); }
+
+int qvk_plan_groups(uint64_t total_frames, uint32_t fpg, uint32_t tpf, double rho, int32_t world,
+                    uint64_t* n_groups, int64_t* tok_off, int64_t* keep, int64_t* row_off, int32_t* rank_begin) {
+    if (fpg == 0) QVK_INVALID("tokenize: frames_per_group must be >= 1");     // prefill.cpp:173
+    if (total_frames == 0) QVK_INVALID("tokenize: empty frame buffer");       // prefill.cpp:172
+    if (tpf == 0) QVK_INVALID("model config: dimensions must be positive");   // prefill.cpp:59-60
+    QVK_TRY(check_rho(rho));
+    if (world < 1) QVK_INVALID("plan: world size must be >= 1");
+    const uint64_t G = (total_frames + fpg - 1) / fpg;
+    if (n_groups) *n_groups = G;
+    if (!tok_off) return QVK_OK;
+    tok_off[0] = 0;
+    row_off[0] = 0;
+    std::vector<double> cost(G);
+    double total_cost = 0;
+    for (uint64_t g = 0; g < G; ++g) {  // prefill.cpp:176-181: last group may be short
+        const uint64_t begin = g * fpg;
+        const uint64_t end = std::min<uint64_t>(begin + fpg, total_frames);
+        const int64_t n = static_cast<int64_t>((end - begin) * tpf);
+        tok_off[g + 1] = tok_off[g] + n;
+        keep[g] = static_cast<int64_t>(retained(rho, static_cast<size_t>(n)));
+        row_off[g + 1] = row_off[g] + keep[g];
+        cost[g] = static_cast<double>(n) * static_cast<double>(n);  // causal attention ~ N^2
+        total_cost += cost[g];
+    }
+    if (rank_begin) {
+        // Contiguous blocks balanced by cost: rank r starts at the first group whose cumulative cost reaches
+        // r/world of the total; never leave a rank empty while groups remain.
+        rank_begin[0] = 0;
+        double acc = 0;
+        uint64_t g = 0;
+        for (int32_t r = 1; r < world; ++r) {
+            const double target = total_cost * r / world;
+            while (g < G && acc + 0.5 * cost[g] < target) acc += cost[g++];
+            const uint64_t min_g = static_cast<uint64_t>(rank_begin[r - 1]) + ((uint64_t)rank_begin[r - 1] < G ? 1 : 0);
+            if (g < min_g) {
+                for (uint64_t x = g; x < min_g; ++x) acc += cost[x];
+                g = min_g;
+            }
+            rank_begin[r] = static_cast<int32_t>(std::min<uint64_t>(g, G));
+        }
+        rank_begin[world] = static_cast<int32_t>(G);
+    }
+    return QVK_OK;
+}
+
+// ---- scores ------------------------------------------------------------------------------------------------------
+int qvk_score(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
+              int32_t width, int32_t scorer, const float* tq, int64_t text_count, int32_t n_h, double* scores) {
+    QVK_TRY(check_groups(g));
+    if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
+    if (dtype != QVK_F32 && dtype != QVK_BF16) QVK_INVALID("score: unsupported dtype");
+    if (scorer == QVK_ATTENTION_SCORE) {
+        // prefill.cpp:214-217
+        if (!tq || text_count <= 0) QVK_INVALID("attention_score scorer requires a text query");
+    } else if (scorer != QVK_KEY_NORM_SMALL && scorer != QVK_VALUE_NORM) {
+        QVK_INVALID("score: unknown scorer (use qvk_snapkv_score for SnapKV)");
+    }
+    return launch_score(s, g, g->total_tokens, k, v, dtype, heads, width, scorer, tq, text_count, n_h, scores);
+}
+
+int qvk_snapkv_score(qvk_stream_t s, const qvk_groups* g, const void* q, const void* k, int32_t n_q, int32_t n_kv,
+                     int32_t d_h, int32_t window, int32_t pool, float scale, double* scores) {
+    QVK_TRY(check_groups(g));
+    return launch_snapkv(s, g, q, k, n_q, n_kv, d_h, window, pool, scale, scores);
+}
+
+int qvk_select(qvk_stream_t s, const qvk_groups* g, const double* scores, int32_t heads, uint32_t* idx) {
+    QVK_TRY(check_groups(g));
+    if (heads <= 0) QVK_INVALID("model config: dimensions must be positive");
+    return launch_select(s, g, scores, heads, idx);
+}
+
+int qvk_gather(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
+               int32_t width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin) {
+    QVK_TRY(check_groups(g));
+    if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
+    if (dtype != QVK_F32 && dtype != QVK_BF16) QVK_INVALID("gather: unsupported dtype");
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
+    return launch_gather(s, g, k, v, dtype, heads, width, idx, kc, vc, origin);
+}
+
+int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
+              int32_t width, int32_t scorer, double rho, const float* tq, int64_t text_count, int32_t n_h,
+              double* scores_ws, uint32_t* idx_ws, void* kc, void* vc, uint64_t* origin) {
+    QVK_TRY(check_rho(rho));  // prefill.cpp:258, validated before anything else
+    QVK_TRY(check_groups(g));
+    if (rho == 1.0)  // prefill.cpp:263-270: identity, no scoring, no shape check
+        return qvk_gather(s, g, k, v, dtype, heads, width, nullptr, kc, vc, origin);
+    double* sc = scores_ws;
+    uint32_t* ix = idx_ws;
+    if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
+                                            sizeof(double) * std::max<int64_t>(1, g->total_tokens * heads), s));
+    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+                                            sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
+    int rc = qvk_score(s, g, k, v, dtype, heads, width, scorer, tq, text_count, n_h, sc);
+    if (rc == QVK_OK) rc = qvk_select(s, g, sc, heads, ix);
+    if (rc == QVK_OK) rc = qvk_gather(s, g, k, v, dtype, heads, width, ix, kc, vc, origin);
+    if (!scores_ws) cudaFreeAsync(sc, s);
+    if (!idx_ws) cudaFreeAsync(ix, s);
+    return rc;
+}
+
+int qvk_attention(qvk_stream_t s, const qvk_groups* g, const void* q, const void* k, const void* v, int32_t n_q,
+                  int32_t n_kv, int32_t d_h, float scale, void* o) {
+    QVK_TRY(check_groups(g));
+    return launch_attention(s, g, q, k, v, n_q, n_kv, d_h, scale, o);
+}
+
+int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q,
+                      const void* k, const void* v, void* o, double* scores_ws, uint32_t* idx_ws, void* kc, void* vc,
+                      uint64_t* origin) {
+    if (!p) QVK_INVALID("prefill_layer: null params");
+    QVK_TRY(check_rho(p->rho));
+    QVK_TRY(check_groups(g));
+    QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
+    const int heads = p->per_head ? p->n_kv : 1;
+    const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
+    if (p->rho == 1.0) return launch_gather(s, g, k, v, QVK_BF16, heads, width, nullptr, kc, vc, origin);
+    double* sc = scores_ws;
+    uint32_t* ix = idx_ws;
+    if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
+                                            sizeof(double) * std::max<int64_t>(1, g->total_tokens * heads), s));
+    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+                                            sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
+    int rc;
+    if (p->scorer == QVK_SNAPKV) {
+        rc = p->per_head ? launch_snapkv(s, g, q, k, p->n_q, p->n_kv, p->d_h, p->snap_window, p->snap_pool, p->scale,
+                                         sc)
+                         : (set_error("prefill_layer: SnapKV scores are per KV head (set per_head = 1)"),
+                            QVK_E_INVALID);
+    } else {
+        rc = qvk_score(s, g, k, v, QVK_BF16, heads, width, p->scorer, nullptr, 0, p->n_kv, sc);
+    }
+    if (rc == QVK_OK) rc = launch_select(s, g, sc, heads, ix);
+    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin);
+    if (!scores_ws) cudaFreeAsync(sc, s);
+    if (!idx_ws) cudaFreeAsync(ix, s);
+    return rc;
+}
+
+// ---- stand-in model pieces --------------------------------------------------------------------------------------
+int qvk_seeded_matrix(qvk_stream_t s, uint64_t seed, uint32_t tag, uint32_t layer, size_t count, double scale,
+                      float* out) {
+    return launch_seeded_matrix(s, seed, tag, layer, count, scale, out);
+}
+
+int qvk_project_exact(qvk_stream_t s, const float* x, int64_t rows, int32_t d_in, const float* w, int32_t d_out,
+                      float* out) {
+    if (rows < 0 || d_in <= 0 || d_out <= 0) QVK_INVALID("model config: dimensions must be positive");
+    return launch_project_exact(s, x, rows, d_in, w, d_out, out);
+}
+
+void qvk_patch_grid(uint32_t tpf, uint32_t* rows, uint32_t* cols) {  // prefill.cpp:116-121
+    uint32_t r = 1;
+    for (uint32_t x = 1; static_cast<uint64_t>(x) * x <= tpf; ++x)
+        if (tpf % x == 0) r = x;
+    *rows = r;
+    *cols = tpf / r;
+}
+
+int qvk_tokenize(qvk_stream_t s, const uint8_t* frames, int64_t n_frames, uint32_t width, uint32_t height,
+                 uint32_t tpf, const float* embed, int32_t d_model, float* tokens) {
+    if (tpf == 0 || d_model <= 0) QVK_INVALID("model config: dimensions must be positive");
+    uint32_t gr, gc;
+    qvk_patch_grid(tpf, &gr, &gc);
+    if (height % gr != 0 || width % gc != 0)  // prefill.cpp:128-129
+        QVK_INVALID("tokenize: frame size not divisible into the patch grid");
+    return launch_tokenize(s, frames, n_frames, width, height, tpf, gr, gc, embed, d_model, tokens);
+}
+
+int qvk_synth_bf16(qvk_stream_t s, uint64_t seed, uint32_t tag, uint32_t layer, uint64_t group, int64_t rows,
+                   int32_t heads, int32_t width, int32_t head_scale, void* out) {
+    return launch_synth_bf16(s, seed, tag, layer, group, rows, heads, width, head_scale, out);
+}
+
+}  // extern "C"

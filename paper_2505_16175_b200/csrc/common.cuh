@@ -1,0 +1,72 @@
+// Shared device/host helpers for the qvk library (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+
+#include "qvk.h"
+
+namespace qvk {
+
+// Thread-local error text returned by qvk_last_error() (capi.cu).
+void set_error(const std::string& msg);
+
+constexpr int kNumSms = 148;
+
+// Order-preserving map of a double score onto uint64: larger score <=> larger key.  -0.0 is canonicalised to +0.0
+// first because the reference compares scores with `!=` (prefill.cpp:245), under which the two zeros tie.
+__device__ __forceinline__ uint64_t score_key(double s) {
+    if (s == 0.0) s = 0.0;
+    const uint64_t u = static_cast<uint64_t>(__double_as_longlong(s));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// Group containing token row t: largest g with off[g] <= t (off has G+1 ascending entries).
+__device__ __forceinline__ int find_group(const int64_t* __restrict__ off, int n_groups, int64_t t) {
+    int lo = 0, hi = n_groups - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint64_t splitmix64_at(uint64_t state0, uint64_t i) {
+    // Draw i (0-based) of splitmix64 seeded with state0 (synthetic.cpp:5-10): state advances by gamma per draw.
+    uint64_t z = state0 + (i + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t stream_seed(uint64_t seed, uint32_t tag, uint32_t layer) {
+    // prefill.cpp:13-18
+    uint64_t s = seed;
+    s = s * 0x100000001b3ull + tag + 1;
+    s = s * 0x100000001b3ull + layer + 1;
+    return s;
+}
+
+}  // namespace qvk
+
+#define QVK_CUDA_CHECK(expr)                                                                    \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess) {                                                                \
+            ::qvk::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " +    \
+                             __FILE__ + ":" + std::to_string(__LINE__));                        \
+            return QVK_E_CUDA;                                                                  \
+        }                                                                                       \
+    } while (0)
+
+#define QVK_LAUNCH_CHECK() QVK_CUDA_CHECK(cudaGetLastError())
+
+#define QVK_INVALID(msg)              \
+    do {                              \
+        ::qvk::set_error(msg);        \
+        return QVK_E_INVALID;         \
+    } while (0)

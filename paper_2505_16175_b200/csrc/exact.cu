@@ -1,0 +1,159 @@
+// Stand-in model pieces of the reference API, computed on the device and bit-identical to prefill.cpp:
+//   seeded_matrix   prefill.cpp:21-30   counter-based splitmix64, double arithmetic, float store
+//   project_exact   prefill.cpp:38-54   out = x * w with double accumulation in the reference's sequential order
+//   tokenize        prefill.cpp:123-168 per-patch double mean (exact integer sums) and the 3 -> d embed
+// plus the synthetic bf16 generator of the benchmark (same bits as oracle qvo_synth_bf16).
+// Every double operation is an explicit _rn intrinsic so nvcc can never contract it into an FMA.
+#include "common.cuh"
+
+namespace qvk {
+namespace {
+
+__global__ void seeded_matrix_kernel(uint64_t state0, size_t count, double scale, float* __restrict__ out) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double u = __dmul_rn(static_cast<double>(splitmix64_at(state0, i) >> 11), 0x1.0p-53);
+        out[i] = __double2float_rn(__dmul_rn(__dsub_rn(__dmul_rn(u, 2.0), 1.0), scale));
+    }
+}
+
+// out(rows, d_out) = x(rows, d_in) * w(d_in, d_out); thread (r, o) accumulates i = 0..d_in-1 in order.
+constexpr int kPT = 32;  // outputs per tile (threadIdx.x)
+constexpr int kPR = 8;   // rows per tile (threadIdx.y)
+constexpr int kPK = 32;  // reduction chunk
+__global__ void __launch_bounds__(kPT * kPR) project_exact_kernel(const float* __restrict__ x, int64_t rows,
+                                                                  int d_in, const float* __restrict__ w,
+                                                                  int d_out, float* __restrict__ out) {
+    __shared__ double xs[kPR][kPK];
+    __shared__ double ws[kPK][kPT + 1];
+    const int o = blockIdx.x * kPT + threadIdx.x;
+    const int64_t r = static_cast<int64_t>(blockIdx.y) * kPR + threadIdx.y;
+    double acc = 0.0;
+    for (int i0 = 0; i0 < d_in; i0 += kPK) {
+        const int kw = min(kPK, d_in - i0);
+        __syncthreads();
+        for (int e = threadIdx.y * kPT + threadIdx.x; e < kPR * kPK; e += kPT * kPR) {
+            const int rr = e / kPK, ii = e % kPK;
+            const int64_t gr = static_cast<int64_t>(blockIdx.y) * kPR + rr;
+            xs[rr][ii] = (gr < rows && ii < kw) ? static_cast<double>(x[gr * d_in + i0 + ii]) : 0.0;
+        }
+        for (int e = threadIdx.y * kPT + threadIdx.x; e < kPK * kPT; e += kPT * kPR) {
+            const int ii = e / kPT, oo = e % kPT;
+            const int go = blockIdx.x * kPT + oo;
+            ws[ii][oo] = (go < d_out && ii < kw) ? static_cast<double>(w[static_cast<int64_t>(i0 + ii) * d_out + go])
+                                                 : 0.0;
+        }
+        __syncthreads();
+        for (int ii = 0; ii < kw; ++ii) acc = __dadd_rn(acc, __dmul_rn(xs[threadIdx.y][ii], ws[ii][threadIdx.x]));
+    }
+    if (r < rows && o < d_out) out[r * d_out + o] = __double2float_rn(acc);
+}
+
+// One CTA per token (frame slot f, patch gr, gc).  Integer channel sums are exact in any order (the reference
+// accumulates uint8 into a double, exact below 2^53), then mean = sum / (double(ph) * pw) and
+// out[o] = float(e0*m0 + e1*m1 + e2*m2) evaluated left to right in double.
+__global__ void __launch_bounds__(256) tokenize_kernel(const uint8_t* __restrict__ frames, uint32_t width,
+                                                       uint32_t height, uint32_t tpf, uint32_t grid_cols,
+                                                       uint32_t ph, uint32_t pw, const float* __restrict__ embed,
+                                                       int d, float* __restrict__ tokens) {
+    __shared__ unsigned long long sums[3];
+    __shared__ double mean[3];
+    const int64_t token = blockIdx.x;
+    const int64_t f = token / tpf;
+    const uint32_t p = static_cast<uint32_t>(token - f * tpf);
+    const uint32_t gr = p / grid_cols, gc = p % grid_cols;
+    const size_t plane = static_cast<size_t>(width) * height;
+    const uint8_t* px = frames + f * 3 * plane;
+    if (threadIdx.x < 3) sums[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long part[3] = {0, 0, 0};
+    for (uint32_t e = threadIdx.x; e < ph * pw; e += blockDim.x) {
+        const uint32_t y = gr * ph + e / pw, x = gc * pw + e % pw;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) part[c] += px[c * plane + static_cast<size_t>(y) * width + x];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) atomicAdd(&sums[c], part[c]);
+    __syncthreads();
+    if (threadIdx.x < 3)
+        mean[threadIdx.x] = __ddiv_rn(static_cast<double>(sums[threadIdx.x]),
+                                      __dmul_rn(static_cast<double>(ph), static_cast<double>(pw)));
+    __syncthreads();
+    for (int o = threadIdx.x; o < d; o += blockDim.x) {
+        const double e0 = embed[o * 3 + 0], e1 = embed[o * 3 + 1], e2 = embed[o * 3 + 2];
+        const double s = __dadd_rn(__dadd_rn(__dmul_rn(e0, mean[0]), __dmul_rn(e1, mean[1])), __dmul_rn(e2, mean[2]));
+        tokens[token * d + o] = __double2float_rn(s);
+    }
+}
+
+__constant__ float kHeadScale[9] = {0.5f,        0.59460356f, 0.70710678f, 0.84089642f, 1.0f,
+                                    1.18920712f, 1.41421356f, 1.68179283f, 2.0f};
+
+// Irwin-Hall(4) approximate N(0,1) per element, per-(row, head) scale 2^(j/4); see oracle qvo_synth_bf16.
+__global__ void synth_bf16_kernel(uint64_t base, int64_t rows, int heads, int width, int head_scale,
+                                  __nv_bfloat16* __restrict__ out) {
+    const int64_t total = rows * heads * width;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t z = splitmix64_at(base, static_cast<uint64_t>(e));
+        const int32_t s = static_cast<int32_t>(z & 0xffff) + static_cast<int32_t>((z >> 16) & 0xffff) +
+                          static_cast<int32_t>((z >> 32) & 0xffff) + static_cast<int32_t>(z >> 48);
+        float val = __fmul_rn(static_cast<float>(s - 131070), 2.6428812e-05f);
+        if (head_scale) {
+            const uint64_t unit = static_cast<uint64_t>(e / width);
+            val = __fmul_rn(val, kHeadScale[splitmix64_at(base ^ 0x5bd1e995ull, unit) % 9]);
+        }
+        out[e] = __float2bfloat16_rn(val);
+    }
+}
+
+unsigned grid_for(int64_t n, int threads) {
+    const int64_t want = (n + threads - 1) / threads;
+    return static_cast<unsigned>(want < 1 ? 1 : (want > kNumSms * 32 ? kNumSms * 32 : want));
+}
+
+}  // namespace
+
+int launch_seeded_matrix(cudaStream_t s, uint64_t seed, uint32_t tag, uint32_t layer, size_t count, double scale,
+                         float* out) {
+    if (count == 0) return QVK_OK;
+    seeded_matrix_kernel<<<grid_for(static_cast<int64_t>(count), 256), 256, 0, s>>>(stream_seed(seed, tag, layer),
+                                                                                    count, scale, out);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
+int launch_project_exact(cudaStream_t s, const float* x, int64_t rows, int d_in, const float* w, int d_out,
+                         float* out) {
+    if (rows == 0 || d_out == 0) return QVK_OK;
+    if ((rows + kPR - 1) / kPR > 65535) QVK_INVALID("project: too many rows for one launch");
+    dim3 grid((d_out + kPT - 1) / kPT, static_cast<unsigned>((rows + kPR - 1) / kPR));
+    project_exact_kernel<<<grid, dim3(kPT, kPR), 0, s>>>(x, rows, d_in, w, d_out, out);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
+int launch_tokenize(cudaStream_t s, const uint8_t* frames, int64_t n_frames, uint32_t width, uint32_t height,
+                    uint32_t tpf, uint32_t grid_rows, uint32_t grid_cols, const float* embed, int d, float* tokens) {
+    const int64_t n_tok = n_frames * tpf;
+    if (n_tok == 0) return QVK_OK;
+    if (n_tok > 0x7fffffff) QVK_INVALID("tokenize: too many tokens for one launch");
+    tokenize_kernel<<<static_cast<unsigned>(n_tok), 256, 0, s>>>(frames, width, height, tpf, grid_cols,
+                                                                  height / grid_rows, width / grid_cols, embed, d,
+                                                                  tokens);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
+int launch_synth_bf16(cudaStream_t s, uint64_t seed, uint32_t tag, uint32_t layer, uint64_t group, int64_t rows,
+                      int heads, int width, int head_scale, void* out) {
+    const uint64_t base = stream_seed(seed, tag, layer) ^ (group * 0xd1b54a32d192ed03ull);
+    const int64_t total = rows * heads * width;
+    if (total == 0) return QVK_OK;
+    synth_bf16_kernel<<<grid_for(total, 256), 256, 0, s>>>(base, rows, heads, width, head_scale,
+                                                           static_cast<__nv_bfloat16*>(out));
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
+}  // namespace qvk

@@ -1,0 +1,348 @@
+// Drop-in implementation of the UNCHANGED reference API /root/reference/proj/include/qv/prefill.hpp on top of the
+// C ABI in include/qvk.h.  Linking libqv_prefill.so instead of compiling src/prefill.cpp switches a reference user
+// onto the B200 path.  Every numeric step runs in a CUDA kernel; this file only validates
+// arguments in the reference's order (prefill.cpp:58-83, 123-183, 192-330), moves the caller's host spans to and
+// from HBM, and maps QVK_E_* status codes to qv::Error with the reference's messages.
+//
+// Results are bit-identical to the reference (tests/native/parity_driver.cpp, tests/test_shim_gpu.py):
+//   weights / text query   device splitmix64 + exact fp64 projection      (prefill.cpp:21-30, 96-114)
+//   tokenize               exact integer patch sums, fp64 embed           (prefill.cpp:123-168)
+//   project                fp64 accumulation in the reference's order     (prefill.cpp:38-54, 185-190)
+//   score / top-k / gather exact fp64 scores, exact radix select, copies  (prefill.cpp:192-282)
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "qv/prefill.hpp"
+#include "qvk.h"
+
+namespace qv {
+namespace {
+
+constexpr uint32_t kTagKey = 1, kTagValue = 2, kTagQuery = 3, kTagEmbed = 4, kTagPrompt = 5;  // prefill.cpp:32-36
+
+void check(int rc) {
+    if (rc != QVK_OK) throw Error(qvk_last_error());
+}
+
+// Owning device allocation.
+class Dev {
+public:
+    Dev() = default;
+    explicit Dev(size_t bytes) { check(qvk_malloc(&p_, bytes)); }
+    Dev(const void* host, size_t bytes) : Dev(bytes) { check(qvk_memcpy_h2d(p_, host, bytes, nullptr)); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    Dev(Dev&& o) noexcept : p_(o.p_) { o.p_ = nullptr; }
+    Dev& operator=(Dev&& o) noexcept {
+        std::swap(p_, o.p_);
+        return *this;
+    }
+    ~Dev() { qvk_free(p_); }
+    template <class T = void>
+    T* get() const { return static_cast<T*>(p_); }
+
+private:
+    void* p_ = nullptr;
+};
+
+template <class T>
+void download(std::vector<T>& out, const Dev& d, size_t count) {
+    out.resize(count);
+    check(qvk_memcpy_d2h(out.data(), d.get(), count * sizeof(T), nullptr));
+    check(qvk_stream_sync(nullptr));
+}
+
+// Device group descriptor for one group of `n` tokens keeping `keep` of them.
+struct OneGroup {
+    Dev arrays;
+    qvk_groups g{};
+    OneGroup(int64_t n, int64_t keep, uint64_t first_token) {
+        const int64_t host[6] = {0, n, keep, 0, keep, static_cast<int64_t>(first_token)};
+        arrays = Dev(host, sizeof(host));
+        const int64_t* base = arrays.get<int64_t>();
+        g.n_groups = 1;
+        g.max_tokens = n;
+        g.total_tokens = n;
+        g.total_rows = keep;
+        g.tok_off_d = base;
+        g.keep_d = base + 2;
+        g.row_off_d = base + 3;
+        g.first_token_d = reinterpret_cast<const uint64_t*>(base + 5);
+    }
+};
+
+std::vector<float> seeded(uint64_t seed, uint32_t tag, uint32_t layer, size_t count, double scale) {
+    Dev d(count * sizeof(float));
+    check(qvk_seeded_matrix(nullptr, seed, tag, layer, count, scale, d.get<float>()));
+    std::vector<float> out;
+    download(out, d, count);
+    return out;
+}
+
+}  // namespace
+
+// ---- config / naming (prefill.cpp:58-94) ---------------------------------------------------------------------------
+void ModelConfig::validate() const {
+    if (d_model == 0 || n_h == 0 || d_h == 0 || layers == 0 || tokens_per_frame == 0)
+        throw Error("model config: dimensions must be positive");
+    if (uint64_t{n_h} * d_h != d_model) throw Error("model config: d_model must equal n_h * d_h");
+}
+
+void PruneConfig::validate() const { check(qvk_validate_rho(rho)); }
+
+Scorer scorer_from_name(const std::string& name) {
+    if (name == "key_norm_small") return Scorer::key_norm_small;
+    if (name == "value_norm") return Scorer::value_norm;
+    if (name == "attention_score") return Scorer::attention_score;
+    throw Error("unknown scorer: " + name);
+}
+
+const char* scorer_name(Scorer s) {
+    switch (s) {
+        case Scorer::key_norm_small: return "key_norm_small";
+        case Scorer::value_norm: return "value_norm";
+        case Scorer::attention_score: return "attention_score";
+    }
+    return "?";
+}
+
+uint64_t KvCache::value_bytes() const {  // host-API semantics: fp32 K+V bytes (prefill.cpp:85-90)
+    uint64_t total = 0;
+    for (const LayerCache& l : layers) total += (l.k.size() + l.v.size()) * sizeof(float);
+    return total;
+}
+
+bool KvCache::same_entries(const KvCache& other) const {
+    return n_h == other.n_h && d_h == other.d_h && layers == other.layers;
+}
+
+// ---- StandInModel (prefill.cpp:96-190) ---------------------------------------------------------------------------
+StandInModel::StandInModel(const ModelConfig& config) : config_(config) {
+    config_.validate();
+    const size_t d = config_.d_model;
+    const double proj_scale = 1.0 / std::sqrt(double(d));
+    w_k_.reserve(config_.layers);
+    w_v_.reserve(config_.layers);
+    for (uint32_t l = 0; l < config_.layers; ++l) {
+        w_k_.push_back(seeded(config_.seed, kTagKey, l, d * d, proj_scale));
+        w_v_.push_back(seeded(config_.seed, kTagValue, l, d * d, proj_scale));
+    }
+    embed_ = seeded(config_.seed, kTagEmbed, 0, d * 3, 1.0 / 255.0);
+    // Text query = prompt * W_q, both generated and multiplied on the device (prefill.cpp:106-113).
+    const size_t t = config_.text_tokens;
+    Dev prompt(t * d * sizeof(float)), wq(d * d * sizeof(float)), q(std::max<size_t>(1, t * d) * sizeof(float));
+    check(qvk_seeded_matrix(nullptr, config_.seed, kTagPrompt, 0, t * d, 1.0, prompt.get<float>()));
+    check(qvk_seeded_matrix(nullptr, config_.seed, kTagQuery, 0, d * d, proj_scale, wq.get<float>()));
+    check(qvk_project_exact(nullptr, prompt.get<float>(), static_cast<int64_t>(t), static_cast<int32_t>(d),
+                            wq.get<float>(), static_cast<int32_t>(d), q.get<float>()));
+    download(query_, q, t * d);
+}
+
+std::pair<uint32_t, uint32_t> StandInModel::patch_grid(uint32_t tokens_per_frame) {
+    uint32_t r, c;
+    qvk_patch_grid(tokens_per_frame, &r, &c);
+    return {r, c};
+}
+
+TokenGroup StandInModel::tokenize_group(const FrameBuffer& frames, size_t frame_begin, size_t frame_end,
+                                        size_t group_id) const {
+    if (frame_end <= frame_begin || frame_end > frames.slots()) throw Error("tokenize: bad frame range");
+    const auto [gr, gc] = patch_grid(config_.tokens_per_frame);
+    if (frames.height() % gr != 0 || frames.width() % gc != 0)
+        throw Error("tokenize: frame size not divisible into the patch grid");
+    const size_t d = config_.d_model;
+    TokenGroup group;
+    group.group_id = group_id;
+    group.first_token = uint64_t(frame_begin) * config_.tokens_per_frame;
+    group.frame_begin = frame_begin;
+    group.frame_end = frame_end;
+    group.token_count = (frame_end - frame_begin) * size_t{config_.tokens_per_frame};
+    const size_t n_frames = frame_end - frame_begin;
+    Dev pixels(frames.slot(frame_begin).data(), n_frames * frames.slot_bytes());
+    Dev embed(embed_.data(), embed_.size() * sizeof(float));
+    Dev tokens(std::max<size_t>(1, group.token_count * d) * sizeof(float));
+    check(qvk_tokenize(nullptr, pixels.get<uint8_t>(), static_cast<int64_t>(n_frames), frames.width(),
+                       frames.height(), config_.tokens_per_frame, embed.get<float>(), static_cast<int32_t>(d),
+                       tokens.get<float>()));
+    download(group.tokens, tokens, group.token_count * d);
+    return group;
+}
+
+std::vector<TokenGroup> StandInModel::tokenize(const FrameBuffer& frames, uint32_t frames_per_group) const {
+    if (frames.slots() == 0) throw Error("tokenize: empty frame buffer");
+    if (frames_per_group == 0) throw Error("tokenize: frames_per_group must be >= 1");
+    const auto [gr, gc] = patch_grid(config_.tokens_per_frame);
+    if (frames.height() % gr != 0 || frames.width() % gc != 0)
+        throw Error("tokenize: frame size not divisible into the patch grid");
+    // One H2D of every slot and one launch for all tokens; groups are slices (prefill.cpp:170-183 order).
+    const size_t d = config_.d_model, tpf = config_.tokens_per_frame, slots = frames.slots();
+    Dev pixels(frames.bytes().data(), frames.bytes().size());
+    Dev embed(embed_.data(), embed_.size() * sizeof(float));
+    Dev tokens(slots * tpf * d * sizeof(float));
+    check(qvk_tokenize(nullptr, pixels.get<uint8_t>(), static_cast<int64_t>(slots), frames.width(), frames.height(),
+                       config_.tokens_per_frame, embed.get<float>(), static_cast<int32_t>(d), tokens.get<float>()));
+    std::vector<float> all;
+    download(all, tokens, slots * tpf * d);
+    uint64_t count = 0;
+    check(qvk_group_count(slots, frames_per_group, &count));
+    std::vector<TokenGroup> groups;
+    groups.reserve(count);
+    for (uint64_t g = 0; g < count; ++g) {
+        TokenGroup group;
+        group.group_id = size_t(g);
+        group.frame_begin = size_t(g) * frames_per_group;
+        group.frame_end = std::min<size_t>(group.frame_begin + frames_per_group, slots);
+        group.first_token = uint64_t(group.frame_begin) * tpf;
+        group.token_count = (group.frame_end - group.frame_begin) * tpf;
+        const float* src = all.data() + group.frame_begin * tpf * d;
+        group.tokens.assign(src, src + group.token_count * d);
+        groups.push_back(std::move(group));
+    }
+    return groups;
+}
+
+void StandInModel::project(const TokenGroup& group, uint32_t layer, std::vector<float>& k,
+                           std::vector<float>& v) const {
+    if (layer >= config_.layers) throw Error("project: layer out of range");
+    const size_t d = config_.d_model, n = group.token_count;
+    Dev x(group.tokens.data(), std::max<size_t>(1, n * d) * sizeof(float));
+    Dev wk(w_k_[layer].data(), d * d * sizeof(float)), wv(w_v_[layer].data(), d * d * sizeof(float));
+    Dev dk(std::max<size_t>(1, n * d) * sizeof(float)), dv(std::max<size_t>(1, n * d) * sizeof(float));
+    check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(n), static_cast<int32_t>(d),
+                            wk.get<float>(), static_cast<int32_t>(d), dk.get<float>()));
+    check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(n), static_cast<int32_t>(d),
+                            wv.get<float>(), static_cast<int32_t>(d), dv.get<float>()));
+    download(k, dk, n * d);
+    download(v, dv, n * d);
+}
+
+// ---- scoring / selection / pruning (prefill.cpp:192-282) ----------------------------------------------------------
+std::vector<double> score_tokens(std::span<const float> k, std::span<const float> v, size_t token_count,
+                                 uint32_t n_h, uint32_t d_h, Scorer scorer, std::span<const float> text_query) {
+    const size_t d = size_t{n_h} * d_h;
+    if (k.size() != token_count * d || v.size() != token_count * d) throw Error("score: tensor shape mismatch");
+    size_t text_count = 0;
+    if (scorer == Scorer::attention_score) {
+        if (text_query.empty()) throw Error("attention_score scorer requires a text query");
+        if (text_query.size() % d != 0) throw Error("score: text query shape mismatch");
+        text_count = text_query.size() / d;
+    }
+    std::vector<double> scores(token_count);
+    if (token_count == 0) return scores;
+    OneGroup grp(static_cast<int64_t>(token_count), static_cast<int64_t>(token_count), 0);
+    Dev dk(k.data(), k.size_bytes()), dv(v.data(), v.size_bytes()), ds(token_count * sizeof(double));
+    Dev dq;
+    if (text_count) dq = Dev(text_query.data(), text_query.size_bytes());
+    check(qvk_score(nullptr, &grp.g, dk.get(), dv.get(), QVK_F32, 1, static_cast<int32_t>(d),
+                    static_cast<int32_t>(scorer), dq.get<float>(), static_cast<int64_t>(text_count),
+                    static_cast<int32_t>(n_h), ds.get<double>()));
+    download(scores, ds, token_count);
+    return scores;
+}
+
+size_t retained_count(double rho, size_t token_count) { return qvk_retained_count(rho, token_count); }
+
+std::vector<uint32_t> top_k_indices(std::span<const double> scores, size_t k) {
+    const size_t n = scores.size();
+    k = std::min(k, n);
+    std::vector<uint32_t> idx;
+    if (k == 0) return idx;
+    OneGroup grp(static_cast<int64_t>(n), static_cast<int64_t>(k), 0);
+    Dev ds(scores.data(), scores.size_bytes()), di(k * sizeof(uint32_t));
+    check(qvk_select(nullptr, &grp.g, ds.get<double>(), 1, di.get<uint32_t>()));
+    download(idx, di, k);
+    return idx;
+}
+
+PrunedGroup prune_group(std::span<const float> k, std::span<const float> v, size_t token_count, uint32_t n_h,
+                        uint32_t d_h, const PruneConfig& prune, std::span<const float> text_query) {
+    prune.validate();
+    if (token_count == 0) throw Error("prune: empty group");
+    const size_t d = size_t{n_h} * d_h;
+    PrunedGroup out;
+    if (prune.rho == 1.0) {
+        // No-pruning identity, bit for bit, without scoring or a shape check (prefill.cpp:263-270).
+        out.indices.resize(token_count);
+        std::iota(out.indices.begin(), out.indices.end(), 0u);
+        if (k.size() != token_count * d || v.size() != token_count * d) {
+            out.k.assign(k.begin(), k.end());  // the reference returns such inputs verbatim
+            out.v.assign(v.begin(), v.end());
+            return out;
+        }
+        OneGroup grp(static_cast<int64_t>(token_count), static_cast<int64_t>(token_count), 0);
+        Dev dk(k.data(), k.size_bytes()), dv(v.data(), v.size_bytes());
+        Dev ck(k.size_bytes()), cv(v.size_bytes());
+        check(qvk_gather(nullptr, &grp.g, dk.get(), dv.get(), QVK_F32, 1, static_cast<int32_t>(d), nullptr,
+                         ck.get(), cv.get(), nullptr));
+        download(out.k, ck, k.size());
+        download(out.v, cv, v.size());
+        return out;
+    }
+    if (k.size() != token_count * d || v.size() != token_count * d) throw Error("score: tensor shape mismatch");
+    size_t text_count = 0;
+    if (prune.scorer == Scorer::attention_score) {
+        if (text_query.empty()) throw Error("attention_score scorer requires a text query");
+        if (text_query.size() % d != 0) throw Error("score: text query shape mismatch");
+        text_count = text_query.size() / d;
+    }
+    const size_t kept = retained_count(prune.rho, token_count);
+    OneGroup grp(static_cast<int64_t>(token_count), static_cast<int64_t>(kept), 0);
+    Dev dk(k.data(), k.size_bytes()), dv(v.data(), v.size_bytes());
+    Dev dq;
+    if (text_count) dq = Dev(text_query.data(), text_query.size_bytes());
+    Dev ck(kept * d * sizeof(float)), cv(kept * d * sizeof(float)), ci(kept * sizeof(uint32_t));
+    Dev ds(token_count * sizeof(double));
+    check(qvk_prune(nullptr, &grp.g, dk.get(), dv.get(), QVK_F32, 1, static_cast<int32_t>(d),
+                    static_cast<int32_t>(prune.scorer), prune.rho, dq.get<float>(), static_cast<int64_t>(text_count),
+                    static_cast<int32_t>(n_h), ds.get<double>(), ci.get<uint32_t>(), ck.get(), cv.get(), nullptr));
+    download(out.indices, ci, kept);
+    download(out.k, ck, kept * d);
+    download(out.v, cv, kept * d);
+    return out;
+}
+
+KvCache make_cache(const ModelConfig& config) {
+    config.validate();
+    KvCache cache;
+    cache.n_h = config.n_h;
+    cache.d_h = config.d_h;
+    cache.layers.resize(config.layers);
+    return cache;
+}
+
+void prefill_group(const StandInModel& model, const TokenGroup& group, const PruneConfig& prune, KvCache& cache) {
+    const ModelConfig& cfg = model.config();
+    std::vector<float> k, v;
+    size_t retained = 0;
+    for (uint32_t l = 0; l < cfg.layers; ++l) {
+        model.project(group, l, k, v);
+        PrunedGroup pruned = prune_group(
+            k, v, group.token_count, cfg.n_h, cfg.d_h, prune,
+            prune.scorer == Scorer::attention_score ? model.text_query() : std::span<const float>{});
+        LayerCache& layer = cache.layers[l];
+        layer.k.insert(layer.k.end(), pruned.k.begin(), pruned.k.end());
+        layer.v.insert(layer.v.end(), pruned.v.begin(), pruned.v.end());
+        for (uint32_t i : pruned.indices) layer.origin.push_back(group.first_token + i);
+        retained = pruned.indices.size();
+    }
+    cache.retained_per_group.push_back(retained);
+    cache.tokens_seen += group.token_count;
+    cache.peak_group_tokens = std::max(cache.peak_group_tokens, group.token_count);
+}
+
+KvCache prefill(const StandInModel& model, std::span<const TokenGroup> groups, const PruneConfig& prune) {
+    if (groups.empty()) throw Error("prefill: no token groups");
+    prune.validate();
+    KvCache cache = make_cache(model.config());
+    for (const TokenGroup& g : groups) prefill_group(model, g, prune, cache);
+    return cache;
+}
+
+uint64_t group_count(uint64_t total_frames, uint32_t frames_per_group) {
+    uint64_t out = 0;
+    check(qvk_group_count(total_frames, frames_per_group, &out));
+    return out;
+}
+
+}  // namespace qv

@@ -1,0 +1,233 @@
+// TEST INFRASTRUCTURE — end-to-end parity of the drop-in qv:: API (libqv_prefill.so -> libqvk.so, on the GPU)
+// against the UNMODIFIED reference (oracle/_ref/libqvref.so through oracle/ref_capi.cpp).
+//
+//   parity_driver pipeline <pattern> <seed> <frames> <w> <h> <d_model> <n_h> <d_h> <layers> <tpf> <text> <fpg>
+//                          <scorer> <rho>
+//       synth frames (reference fill_pattern) -> StandInModel -> tokenize -> prefill, on both sides; prints one
+//       JSON line with bitwise comparisons of tokens, text query, every layer's K/V/origin and the cache stats.
+//   parity_driver errors
+//       drives the documented misuse cases through both APIs and prints each pair of qv::Error messages.
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "qv/prefill.hpp"
+
+extern "C" {
+const char* qvref_last_error(void);
+void qvref_fill_pattern(int, uint64_t, uint64_t, uint32_t, uint32_t, uint8_t*);
+void* qvref_model_create(uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint64_t);
+void qvref_model_destroy(void*);
+size_t qvref_model_text_query(void*, float*);
+int qvref_model_tokenize(void*, const uint8_t*, size_t, uint32_t, uint32_t, uint32_t, float*, uint64_t*, uint64_t*,
+                         uint64_t*, uint64_t*, size_t*);
+void* qvref_prefill_frames(void*, const uint8_t*, size_t, uint32_t, uint32_t, uint32_t, int, double);
+void qvref_cache_destroy(void*);
+size_t qvref_cache_layers(void*);
+size_t qvref_cache_rows(void*, size_t);
+size_t qvref_cache_groups(void*);
+uint64_t qvref_cache_tokens_seen(void*);
+size_t qvref_cache_peak_group_tokens(void*);
+uint64_t qvref_cache_value_bytes(void*);
+void qvref_cache_copy_layer(void*, size_t, float*, float*, uint64_t*);
+void qvref_cache_retained_per_group(void*, uint64_t*);
+int qvref_score_tokens(const float*, size_t, const float*, size_t, size_t, uint32_t, uint32_t, int, const float*,
+                       size_t, double*);
+int qvref_prune_group(const float*, size_t, const float*, size_t, size_t, uint32_t, uint32_t, int, double,
+                      const float*, size_t, float*, float*, uint32_t*, size_t*);
+int qvref_group_count(uint64_t, uint32_t, uint64_t*);
+}
+
+namespace {
+
+template <class T>
+bool same_bits(const std::vector<T>& a, const T* b, size_t n) {
+    return a.size() == n && (n == 0 || std::memcmp(a.data(), b, n * sizeof(T)) == 0);
+}
+
+int pipeline(char** a) {
+    const int pattern = std::stoi(a[0]);
+    const uint64_t seed = std::stoull(a[1]);
+    const size_t frames = std::stoull(a[2]);
+    const uint32_t w = std::stoul(a[3]), h = std::stoul(a[4]);
+    qv::ModelConfig cfg;
+    cfg.d_model = std::stoul(a[5]);
+    cfg.n_h = std::stoul(a[6]);
+    cfg.d_h = std::stoul(a[7]);
+    cfg.layers = std::stoul(a[8]);
+    cfg.tokens_per_frame = std::stoul(a[9]);
+    cfg.text_tokens = std::stoul(a[10]);
+    cfg.seed = seed;
+    const uint32_t fpg = std::stoul(a[11]);
+    qv::PruneConfig prune;
+    prune.scorer = qv::scorer_from_name(a[12]);
+    prune.rho = std::stod(a[13]);
+
+    qv::FrameBuffer fb(frames, w, h);
+    std::vector<uint8_t> pixels(frames * fb.slot_bytes());
+    for (size_t f = 0; f < frames; ++f) {
+        qvref_fill_pattern(pattern, seed, f, w, h, pixels.data() + f * fb.slot_bytes());
+        fb.write_slot(f, {pixels.data() + f * fb.slot_bytes(), fb.slot_bytes()});
+    }
+
+    // drop-in (GPU)
+    qv::StandInModel model(cfg);
+    const auto groups = model.tokenize(fb, fpg);
+    const qv::KvCache cache = qv::prefill(model, groups, prune);
+
+    // reference (CPU)
+    void* ref = qvref_model_create(cfg.d_model, cfg.n_h, cfg.d_h, cfg.layers, cfg.tokens_per_frame,
+                                   cfg.text_tokens, seed);
+    std::vector<float> ref_q(size_t{cfg.text_tokens} * cfg.d_model);
+    qvref_model_text_query(ref, ref_q.data());
+    const size_t n_tok = frames * cfg.tokens_per_frame;
+    std::vector<float> ref_tok(n_tok * cfg.d_model);
+    std::vector<uint64_t> ft(groups.size() + 1), fbg(groups.size() + 1), fe(groups.size() + 1), tc(groups.size() + 1);
+    size_t n_groups = 0;
+    qvref_model_tokenize(ref, pixels.data(), frames, w, h, fpg, ref_tok.data(), ft.data(), fbg.data(), fe.data(),
+                         tc.data(), &n_groups);
+    bool tokens_equal = n_groups == groups.size();
+    size_t off = 0;
+    for (size_t g = 0; tokens_equal && g < groups.size(); ++g) {
+        tokens_equal = same_bits(groups[g].tokens, ref_tok.data() + off, size_t(tc[g]) * cfg.d_model) &&
+                       groups[g].first_token == ft[g] && groups[g].frame_begin == fbg[g] &&
+                       groups[g].frame_end == fe[g] && groups[g].token_count == tc[g];
+        off += size_t(tc[g]) * cfg.d_model;
+    }
+    const auto q = model.text_query();
+    const bool query_equal = same_bits(std::vector<float>(q.begin(), q.end()), ref_q.data(), ref_q.size());
+
+    void* rc = qvref_prefill_frames(ref, pixels.data(), frames, w, h, fpg, static_cast<int>(prune.scorer), prune.rho);
+    bool cache_equal = rc && qvref_cache_layers(rc) == cache.layers.size();
+    size_t rows = 0;
+    int first_bad_layer = -1;
+    for (size_t l = 0; cache_equal && l < cache.layers.size(); ++l) {
+        const size_t r = qvref_cache_rows(rc, l);
+        const size_t d = cfg.d_model;
+        std::vector<float> k(r * d), v(r * d);
+        std::vector<uint64_t> o(r);
+        qvref_cache_copy_layer(rc, l, k.data(), v.data(), o.data());
+        const bool ok = same_bits(cache.layers[l].k, k.data(), r * d) && same_bits(cache.layers[l].v, v.data(), r * d) &&
+                        same_bits(cache.layers[l].origin, o.data(), r);
+        if (!ok) first_bad_layer = static_cast<int>(l);
+        cache_equal = ok;
+        rows += r;
+    }
+    std::vector<uint64_t> rpg(rc ? qvref_cache_groups(rc) : 0);
+    if (rc) qvref_cache_retained_per_group(rc, rpg.data());
+    bool stats_equal = rc && rpg.size() == cache.retained_per_group.size() &&
+                       cache.tokens_seen == qvref_cache_tokens_seen(rc) &&
+                       cache.peak_group_tokens == qvref_cache_peak_group_tokens(rc) &&
+                       cache.value_bytes() == qvref_cache_value_bytes(rc);
+    for (size_t i = 0; stats_equal && i < rpg.size(); ++i) stats_equal = rpg[i] == cache.retained_per_group[i];
+    std::printf(
+        "{\"tokens_equal\": %s, \"query_equal\": %s, \"cache_equal\": %s, \"stats_equal\": %s, \"groups\": %zu, "
+        "\"rows\": %zu, \"first_bad_layer\": %d, \"value_bytes\": %llu}\n",
+        tokens_equal ? "true" : "false", query_equal ? "true" : "false", cache_equal ? "true" : "false",
+        stats_equal ? "true" : "false", groups.size(), rows, first_bad_layer,
+        static_cast<unsigned long long>(cache.value_bytes()));
+    if (rc) qvref_cache_destroy(rc);
+    qvref_model_destroy(ref);
+    return tokens_equal && query_equal && cache_equal && stats_equal ? 0 : 1;
+}
+
+std::string catch_msg(const std::function<void()>& f) {
+    try {
+        f();
+    } catch (const qv::Error& e) {
+        return e.what();
+    }
+    return "<no error>";
+}
+
+std::string ref_msg(int rc) { return rc == 0 ? "<no error>" : qvref_last_error(); }
+
+void report(const char* name, const std::string& ours, const std::string& ref, bool& all) {
+    const bool ok = ours == ref;
+    all = all && ok;
+    std::printf("%s\t%s\t%s\t%s\n", ok ? "OK" : "MISMATCH", name, ours.c_str(), ref.c_str());
+}
+
+int errors() {
+    bool all = true;
+    std::vector<float> k(8, 1.f), v(8, 1.f), kout(8), vout(8), q(3, 1.f);
+    std::vector<uint32_t> idx(8);
+    std::vector<double> s(8);
+    size_t kept;
+    auto prune = [](int scorer, double rho) {
+        qv::PruneConfig p;
+        p.scorer = static_cast<qv::Scorer>(scorer);
+        p.rho = rho;
+        return p;
+    };
+    report("rho_zero", catch_msg([&] { qv::prune_group(k, v, 4, 1, 2, prune(0, 0.0)); }),
+           ref_msg(qvref_prune_group(k.data(), 8, v.data(), 8, 4, 1, 2, 0, 0.0, nullptr, 0, kout.data(), vout.data(),
+                                     idx.data(), &kept)), all);
+    report("rho_gt_one", catch_msg([&] { qv::prune_group(k, v, 4, 1, 2, prune(0, 1.5)); }),
+           ref_msg(qvref_prune_group(k.data(), 8, v.data(), 8, 4, 1, 2, 0, 1.5, nullptr, 0, kout.data(), vout.data(),
+                                     idx.data(), &kept)), all);
+    report("empty_group", catch_msg([&] { qv::prune_group(k, v, 0, 1, 2, prune(0, 0.5)); }),
+           ref_msg(qvref_prune_group(k.data(), 8, v.data(), 8, 0, 1, 2, 0, 0.5, nullptr, 0, kout.data(), vout.data(),
+                                     idx.data(), &kept)), all);
+    report("shape_mismatch", catch_msg([&] { qv::prune_group(k, v, 3, 1, 2, prune(0, 0.5)); }),
+           ref_msg(qvref_prune_group(k.data(), 8, v.data(), 8, 3, 1, 2, 0, 0.5, nullptr, 0, kout.data(), vout.data(),
+                                     idx.data(), &kept)), all);
+    report("identity_skips_shape_check", catch_msg([&] { qv::prune_group(k, v, 3, 1, 2, prune(0, 1.0)); }),
+           ref_msg(qvref_prune_group(k.data(), 8, v.data(), 8, 3, 1, 2, 0, 1.0, nullptr, 0, kout.data(), vout.data(),
+                                     idx.data(), &kept)), all);
+    report("attention_without_query", catch_msg([&] { qv::score_tokens(k, v, 4, 1, 2, qv::Scorer::attention_score); }),
+           ref_msg(qvref_score_tokens(k.data(), 8, v.data(), 8, 4, 1, 2, 2, nullptr, 0, s.data())), all);
+    report("query_shape", catch_msg([&] { qv::score_tokens(k, v, 4, 1, 2, qv::Scorer::attention_score, q); }),
+           ref_msg(qvref_score_tokens(k.data(), 8, v.data(), 8, 4, 1, 2, 2, q.data(), 3, s.data())), all);
+    uint64_t gc;
+    report("group_count_zero", catch_msg([&] { qv::group_count(10, 0); }), ref_msg(qvref_group_count(10, 0, &gc)),
+           all);
+    report("unknown_scorer", catch_msg([&] { qv::scorer_from_name("bogus"); }), "unknown scorer: bogus", all);
+    qv::ModelConfig bad;
+    bad.d_model = 10;
+    report("bad_model", catch_msg([&] { qv::StandInModel m(bad); }), "model config: d_model must equal n_h * d_h",
+           all);
+    report("no_groups", catch_msg([&] {
+               qv::ModelConfig c;
+               qv::StandInModel m(c);
+               qv::prefill(m, {}, qv::PruneConfig{});
+           }),
+           "prefill: no token groups", all);
+    report("empty_frames", catch_msg([&] {
+               qv::ModelConfig c;
+               qv::StandInModel m(c);
+               m.tokenize(qv::FrameBuffer(), 1);
+           }),
+           "tokenize: empty frame buffer", all);
+    report("bad_patch_grid", catch_msg([&] {
+               qv::ModelConfig c;
+               c.tokens_per_frame = 4;
+               qv::StandInModel m(c);
+               m.tokenize(qv::FrameBuffer(2, 3, 3), 1);
+           }),
+           "tokenize: frame size not divisible into the patch grid", all);
+    report("project_layer", catch_msg([&] {
+               qv::ModelConfig c;
+               qv::StandInModel m(c);
+               std::vector<float> a, b;
+               m.project(qv::TokenGroup{}, 5, a, b);
+           }),
+           "project: layer out of range", all);
+    return all ? 0 : 1;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    try {
+        if (argc >= 2 && std::string(argv[1]) == "pipeline" && argc == 16) return pipeline(argv + 2);
+        if (argc >= 2 && std::string(argv[1]) == "errors") return errors();
+    } catch (const std::exception& e) {
+        std::printf("{\"exception\": \"%s\"}\n", e.what());
+        return 2;
+    }
+    std::fprintf(stderr, "usage: parity_driver pipeline <14 args> | errors\n");
+    return 64;
+}

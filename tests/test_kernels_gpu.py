@@ -1,0 +1,303 @@
+"""GPU parity: every kernel of the path called through the C ABI against the oracle on the same inputs.
+
+Bars: score / select / gather / origin bit-exact (no near-tie band is needed — the device reproduces
+the reference's sequential double sums); attention |o - o_ref| <= 1e-2 + 1e-2 |o_ref| (bf16 output) against the
+double restatement and a torch fp32 reference; SnapKV scores rel 1e-4 (fp32 math) with index sets bit-exact unless
+the oracle's boundary gap is within the stated near-tie band.
+"""
+import hashlib
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2505_16175_b200 as qp
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+
+
+def bf16_bits(t: torch.Tensor) -> np.ndarray:
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def f32_of(t: torch.Tensor) -> np.ndarray:
+    return t.float().cpu().numpy()
+
+
+def synth_groups(sizes, heads, width, tag, head_scale, device, seed=1):
+    parts = [qp.synth_bf16(seed, tag, 0, g, n, heads, width, head_scale, device) for g, n in enumerate(sizes)]
+    return torch.cat(parts, 0).contiguous()
+
+
+# ------------------------------------------------------------------------------------------------ synth
+def test_device_synth_matches_host(cuda):
+    d = qp.synth_bf16(1, 1, 0, 3, 300, 4, 128, True, cuda)
+    h = O.synth_bf16(1, 1, 0, 3, 300, 4, 128, True)
+    assert bf16_bits(d).tobytes() == h.tobytes()
+
+
+# ------------------------------------------------------------------------------------------------ scores
+@pytest.mark.parametrize("sizes,heads,width", [([256] * 4, 2, 64), ([4096, 100, 1, 777], 4, 128), ([300], 1, 512)])
+def test_norm_scores_bitexact_bf16(cuda, sizes, heads, width):
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    k = synth_groups(sizes, heads, width, 1, True, cuda)
+    v = synth_groups(sizes, heads, width, 2, False, cuda)
+    for scorer, x, neg in ((qp.Scorer.key_norm_small, k, True), (qp.Scorer.value_norm, v, False)):
+        got = qp.score(k, v, g, heads, width, scorer).cpu().numpy()
+        xf = f32_of(x)
+        for gi, n in enumerate(sizes):
+            t0 = plan.tok_off[gi]
+            want = O.score_norm(xf[t0:t0 + n], heads, width, neg).ravel()
+            seg = got[heads * t0: heads * (t0 + n)]
+            assert seg.tobytes() == want.tobytes(), (scorer, gi)
+
+
+@pytest.mark.parametrize("n,n_h,d_h", [(64, 4, 16), (257, 2, 64), (33, 1, 3)])
+def test_reference_scores_f32_bitexact(cuda, n, n_h, d_h):
+    rng = np.random.default_rng(n)
+    k = (rng.standard_normal(n * n_h * d_h) * np.exp(rng.standard_normal(n * n_h * d_h))).astype(np.float32)
+    v = rng.standard_normal(n * n_h * d_h).astype(np.float32)
+    q = rng.standard_normal(5 * n_h * d_h).astype(np.float32)
+    for scorer in (qp.Scorer.key_norm_small, qp.Scorer.value_norm, qp.Scorer.attention_score):
+        got = qp.score_tokens(k, v, n, n_h, d_h, scorer, q)
+        if O.ref is not None:
+            want = O.ref_score_tokens(k, v, n, n_h, d_h, int(scorer), q)
+        elif scorer == qp.Scorer.attention_score:
+            want = O.score_attention(k, n, n_h, d_h, q, 5)
+        else:
+            want = O.score_norm(k if scorer == 0 else v, 1, n_h * d_h, scorer == 0)[0]
+        assert got.tobytes() == want.tobytes(), scorer
+
+
+# ------------------------------------------------------------------------------------------------ select
+@pytest.mark.parametrize("sizes", [[1], [2, 3, 5], [256] * 4, [4096, 4095, 17], [16384], [30000]])
+@pytest.mark.parametrize("kind", ["normal", "ties", "signed_zero", "constant"])
+def test_select_matches_oracle(cuda, sizes, kind):
+    rng = np.random.default_rng(sum(sizes))
+    heads = 2
+    segs = []
+    for n in sizes:
+        for _h in range(heads):
+            if kind == "normal":
+                s = rng.standard_normal(n)
+            elif kind == "ties":
+                s = rng.integers(-4, 5, n).astype(np.float64) * 0.5
+            elif kind == "signed_zero":
+                s = np.where(rng.random(n) < 0.5, -0.0, 0.0)
+                s[rng.random(n) < 0.1] = 1.0
+            else:
+                s = np.full(n, -3.25)
+            segs.append(s)
+    for rho in (0.125, 0.5, 0.999):
+        plan = qp.GroupPlan.from_sizes(sizes, rho)
+        g = plan.to(cuda)
+        got = qp.select(torch.from_numpy(np.concatenate(segs)).to(cuda), g, heads).cpu().numpy()
+        for gi, n in enumerate(sizes):
+            kk = plan.keep[gi]
+            for h in range(heads):
+                want = O.top_k(segs[gi * heads + h], kk)
+                rows = got[(plan.row_off[gi]) * heads: (plan.row_off[gi] + kk) * heads].reshape(kk, heads)[:, h]
+                assert rows.tolist() == want.tolist(), (gi, h, rho)
+
+
+def test_top_k_indices_mirror(cuda):
+    assert qp.top_k_indices(np.array([1, 3, 2, 3.0]), 2).tolist() == [1, 3]
+    assert qp.top_k_indices(np.array([-0.0, 0.0, -0.0, 0.0]), 2).tolist() == [0, 1]
+    assert qp.top_k_indices(np.array([1.0, 2.0]), 0).tolist() == []
+    assert qp.top_k_indices(np.array([1.0, 2.0]), 5).tolist() == [0, 1]
+
+
+# ------------------------------------------------------------------------------------------------ gather / prune
+def test_golden_gqa_prune(cuda):
+    """C1 GQA variant: per-head pruning on the device == the reference's per-head-slice prune_group fixture."""
+    z = np.load(GOLD / "c1_gqa.npz")
+    G, N, H, D, rho = int(z["G"]), int(z["N"]), int(z["H"]), int(z["D"]), float(z["rho"])
+    plan = qp.GroupPlan.from_sizes([N] * G, rho)
+    g = plan.to(cuda)
+    k = synth_groups([N] * G, H, D, 1, True, cuda)
+    v = synth_groups([N] * G, H, D, 2, False, cuda)
+    kc, vc, origin, idx = qp.prune(k, v, g, H, D, qp.Scorer.key_norm_small, rho)
+    kk = plan.keep[0]
+    idx = idx.cpu().numpy().reshape(-1, H)
+    kcf = f32_of(kc.view(-1, H, D))
+    vcf = f32_of(vc.view(-1, H, D))
+    org = origin.cpu().numpy().reshape(-1, H)
+    for gi in range(G):
+        r0 = plan.row_off[gi]
+        for h in range(H):
+            want = z[f"g{gi}_h{h}_idx"]
+            assert idx[r0:r0 + kk, h].tolist() == want.tolist()
+            assert org[r0:r0 + kk, h].tolist() == (plan.tok_off[gi] + want.astype(np.int64)).tolist()
+            assert hashlib.sha256(np.ascontiguousarray(kcf[r0:r0 + kk, h]).tobytes()).digest() == bytes(
+                z[f"g{gi}_h{h}_k_sha"])
+            assert hashlib.sha256(np.ascontiguousarray(vcf[r0:r0 + kk, h]).tobytes()).digest() == bytes(
+                z[f"g{gi}_h{h}_v_sha"])
+
+
+@pytest.mark.parametrize("rho", [0.125, 0.25, 0.5, 1.0])
+def test_prune_group_mirror_vs_reference(cuda, rho):
+    n, n_h, d_h = 300, 4, 16
+    rng = np.random.default_rng(int(rho * 1000))
+    k = rng.integers(-3, 4, n * n_h * d_h).astype(np.float32)  # many exact score ties
+    v = rng.standard_normal(n * n_h * d_h).astype(np.float32)
+    q = rng.standard_normal(7 * n_h * d_h).astype(np.float32)
+    for scorer in (qp.Scorer.key_norm_small, qp.Scorer.value_norm, qp.Scorer.attention_score):
+        got = qp.prune_group(k, v, n, n_h, d_h, qp.PruneConfig(scorer, rho), q)
+        if O.ref is None:
+            continue
+        kr, vr, ir = O.ref_prune_group(k, v, n, n_h, d_h, int(scorer), rho, q)
+        assert got.indices.tolist() == ir.tolist()
+        assert got.k.tobytes() == kr.tobytes() and got.v.tobytes() == vr.tobytes()
+
+
+def test_prune_properties_full_c2(cuda):
+    """BASELINE configs[1] sizes: 16 groups x 4096 tokens, 4 KV heads x 128: sortedness, counts, origins, copies,
+    monotone inclusion I(rho1) subset I(rho2)."""
+    sizes = [4096] * 16
+    H, D = 4, 128
+    k = synth_groups(sizes, H, D, 1, True, cuda)
+    v = synth_groups(sizes, H, D, 2, False, cuda)
+    sets = {}
+    for rho in (0.125, 0.25, 0.5):
+        plan = qp.GroupPlan.from_sizes(sizes, rho)
+        g = plan.to(cuda)
+        kc, vc, origin, idx = qp.prune(k, v, g, H, D, qp.Scorer.key_norm_small, rho)
+        ix = idx.view(-1, H).cpu().numpy().astype(np.int64)
+        kk = plan.keep[0]
+        assert kk == qp.retained_count(rho, 4096)
+        seg = ix.reshape(16, kk, H)
+        assert (np.diff(seg, axis=1) > 0).all()  # strictly ascending per (group, head)
+        src = (torch.from_numpy(seg).to(cuda) + torch.from_numpy(plan.tok_off[:-1]).to(cuda)[:, None, None])
+        heads = torch.arange(H, device=cuda)[None, None, :]
+        assert torch.equal(k[src.view(-1, H), heads.view(1, H)].reshape(-1), kc.view(-1))
+        assert torch.equal(v[src.view(-1, H), heads.view(1, H)].reshape(-1), vc.view(-1))
+        assert torch.equal(origin.view(-1, H), src.view(-1, H))
+        sets[rho] = seg
+    for a, b in ((0.125, 0.25), (0.25, 0.5)):
+        for gi in range(16):
+            for h in range(H):
+                assert set(sets[a][gi, :, h].tolist()) <= set(sets[b][gi, :, h].tolist())
+    # exact oracle check on two sampled groups
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    kf = f32_of(k)
+    for gi in (0, 11):
+        t0 = plan.tok_off[gi]
+        want = O.select_heads(O.score_norm(kf[t0:t0 + 4096], H, D, True), 4096, H, plan.keep[gi])
+        assert (sets[0.5][gi] == want).all()
+
+
+def test_identity_rho_one(cuda):
+    sizes = [100, 37]
+    plan = qp.GroupPlan.from_sizes(sizes, 1.0)
+    g = plan.to(cuda)
+    k = synth_groups(sizes, 2, 64, 1, True, cuda)
+    v = synth_groups(sizes, 2, 64, 2, False, cuda)
+    kc, vc, origin, _ = qp.prune(k, v, g, 2, 64, qp.Scorer.key_norm_small, 1.0)
+    assert torch.equal(kc.view_as(k), k) and torch.equal(vc.view_as(v), v)
+    assert origin.view(-1, 2)[:, 0].tolist() == list(range(137))
+
+
+# ------------------------------------------------------------------------------------------------ attention
+def torch_attention(q, k, v, sizes, n_q, n_kv, scale):
+    """Plain PyTorch fp32 causal GQA attention per group (reference for the tcgen05 kernel)."""
+    outs, t0 = [], 0
+    for n in sizes:
+        qs = q[t0:t0 + n].float().permute(1, 0, 2)
+        ks = k[t0:t0 + n].float().permute(1, 0, 2).repeat_interleave(n_q // n_kv, 0)
+        vs = v[t0:t0 + n].float().permute(1, 0, 2).repeat_interleave(n_q // n_kv, 0)
+        s = (qs @ ks.transpose(1, 2)) * scale
+        s = s.masked_fill(torch.triu(torch.ones(n, n, dtype=torch.bool, device=q.device), 1), float("-inf"))
+        outs.append((torch.softmax(s, -1) @ vs).permute(1, 0, 2))
+        t0 += n
+    return torch.cat(outs, 0)
+
+
+def check_tol(got, want, what):
+    err = (got.float() - want.float()).abs()
+    bound = 1e-2 + 1e-2 * want.float().abs()
+    bad = (err > bound).sum().item()
+    assert bad == 0, f"{what}: {bad} elements out of tolerance; max abs err {err.max().item():.3e}"
+    return err.max().item()
+
+
+@pytest.mark.parametrize("sizes,n_q,n_kv", [([128], 1, 1), ([256], 2, 1), ([384, 100, 1, 129], 28, 4),
+                                            ([4096], 28, 4), ([4096] * 2 + [1000], 28, 4), ([16384], 4, 4)])
+def test_attention_vs_torch_fp32(cuda, sizes, n_q, n_kv):
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, 128, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, 128, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, 128, 2, False, cuda)
+    o = qp.attention(q, k, v, g, n_q, n_kv)
+    torch.cuda.synchronize()
+    want = torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(128))
+    check_tol(o, want, f"attention {sizes}")
+
+
+def test_attention_vs_double_oracle(cuda):
+    sizes, n_q, n_kv = [300, 129], 28, 4
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, 128, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, 128, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, 128, 2, False, cuda)
+    o = qp.attention(q, k, v, g, n_q, n_kv)
+    t0 = 0
+    for n in sizes:
+        want = O.attention(f32_of(q[t0:t0 + n]), f32_of(k[t0:t0 + n]), f32_of(v[t0:t0 + n]), n_q, n_kv, 128,
+                           1 / math.sqrt(128))
+        check_tol(o[t0:t0 + n], torch.from_numpy(want).to(cuda), f"group of {n}")
+        t0 += n
+
+
+# ------------------------------------------------------------------------------------------------ SnapKV
+@pytest.mark.parametrize("sizes,window,pool", [([256, 100], 32, 1), ([1024], 32, 7), ([20], 32, 1)])
+def test_snapkv_vs_oracle(cuda, sizes, window, pool):
+    n_q, n_kv = 28, 4
+    plan = qp.GroupPlan.from_sizes(sizes, 0.25)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, 128, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, 128, 1, True, cuda)
+    got = qp.snapkv_scores(q, k, g, n_q, n_kv, window, pool).cpu().numpy()
+    t0 = 0
+    for gi, n in enumerate(sizes):
+        want = O.snapkv_scores(f32_of(q[t0:t0 + n]), f32_of(k[t0:t0 + n]), n_q, n_kv, 128, window, pool,
+                               1 / math.sqrt(128))
+        seg = got[n_kv * t0: n_kv * (t0 + n)].reshape(n_kv, n)
+        np.testing.assert_allclose(seg, want, rtol=1e-4, atol=1e-6)
+        # index sets: exact unless the oracle boundary gap is inside the near-tie band (tau = 1e-4 relative)
+        kk = plan.keep[gi]
+        for h in range(n_kv):
+            order = np.argsort(-want[h], kind="stable")
+            gap = want[h][order[kk - 1]] - want[h][order[kk]] if kk < n else np.inf
+            if gap > 1e-4 * abs(want[h][order[kk - 1]]):
+                assert set(O.top_k(seg[h], kk).tolist()) == set(O.top_k(want[h], kk).tolist())
+        t0 += n
+
+
+# ------------------------------------------------------------------------------------------------ full layer
+@pytest.mark.parametrize("scorer,per_head", [(qp.Scorer.key_norm_small, True), (qp.Scorer.value_norm, False),
+                                             (qp.Scorer.snapkv, True)])
+def test_prefill_layer(cuda, scorer, per_head):
+    sizes, n_q, n_kv, D, rho = [1024, 1024, 512], 28, 4, 128, 0.25
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, D, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, D, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, D, 2, False, cuda)
+    buf = qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, scorer, per_head)
+    torch.cuda.synchronize()
+    check_tol(buf.o, torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(D)), "layer attention")
+    heads, width = (n_kv, D) if per_head else (1, n_kv * D)
+    if scorer == qp.Scorer.snapkv:
+        sc = qp.snapkv_scores(q, k, g, n_q, n_kv)
+    else:
+        sc = qp.score(k, v, g, heads, width, scorer)
+    idx = qp.select(sc, g, heads)
+    kc, vc, origin = qp.gather(k, v, g, heads, width, idx)
+    assert torch.equal(buf.idx[: idx.numel()], idx)
+    assert torch.equal(buf.k_cache, kc) and torch.equal(buf.v_cache, vc) and torch.equal(buf.origin, origin)

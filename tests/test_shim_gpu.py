@@ -1,0 +1,52 @@
+"""GPU: the drop-in qv:: API (libqv_prefill.so over libqvk.so) against the UNMODIFIED reference, end to end:
+fill_pattern frames -> StandInModel -> tokenize -> prefill -> KvCache, bit-for-bit (tests/native/parity_driver.cpp),
+plus the reference's error texts for the documented misuse cases and the committed golden fixtures."""
+import json
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
+DRIVER = ROOT / "tests" / "native" / "build" / "parity_driver"
+needs_driver = pytest.mark.skipif(not DRIVER.exists(), reason="parity driver not built (needs reference headers)")
+
+PAT = {"gradient": 0, "noise": 1, "constant": 2, "checker": 3}
+
+
+def run(*args):
+    r = subprocess.run([str(DRIVER), *map(str, args)], capture_output=True, text=True, timeout=600)
+    return r.returncode, r.stdout, r.stderr
+
+
+@needs_driver
+@pytest.mark.parametrize("pattern", ["gradient", "checker", "noise", "constant"])
+@pytest.mark.parametrize("scorer,rho", [("key_norm_small", 0.5), ("value_norm", 0.25), ("attention_score", 0.5),
+                                        ("key_norm_small", 1.0), ("key_norm_small", 0.125)])
+def test_pipeline_bitexact_c1(cuda, pattern, scorer, rho):
+    # BASELINE configs[0] through the reference's own MHA API: d 256 = 4 x 64, 16 frames x 64 tokens, 4 frames/group
+    rc, out, err = run("pipeline", PAT[pattern], 1, 16, 64, 64, 256, 4, 64, 1, 64, 16, 4, scorer, rho)
+    res = json.loads(out.strip().splitlines()[-1])
+    assert rc == 0, (res, err)
+    assert res["cache_equal"] and res["tokens_equal"] and res["query_equal"] and res["stats_equal"]
+
+
+@needs_driver
+@pytest.mark.parametrize("args", [
+    (0, 7, 5, 32, 32, 64, 4, 16, 2, 4, 8, 2, "key_norm_small", 0.5),      # ragged last group, 2 layers
+    (1, 3, 9, 48, 24, 96, 3, 32, 3, 6, 5, 4, "attention_score", 0.3),    # non-square patch grid, 3 layers
+    (3, 2, 3, 16, 16, 32, 2, 16, 1, 1, 2, 1, "value_norm", 0.9),          # one token per frame
+    (2, 5, 12, 64, 64, 128, 2, 64, 1, 16, 4, 5, "key_norm_small", 0.05),  # constant frames: 64-fold exact ties
+])
+def test_pipeline_bitexact_misc(cuda, args):
+    rc, out, err = run("pipeline", *args)
+    res = json.loads(out.strip().splitlines()[-1])
+    assert rc == 0, (res, err)
+
+
+@needs_driver
+def test_error_texts_match_reference(cuda):
+    rc, out, err = run("errors")
+    assert rc == 0, out + err
+    assert out.count("OK\t") >= 14
