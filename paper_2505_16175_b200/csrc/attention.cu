@@ -22,6 +22,8 @@
 // Algorithmic FLOPs per (group, q head): 4 * d * N (N + 1) / 2 (causal, diagonal included; masked work uncredited).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -41,6 +43,23 @@ constexpr int kRegsSoftmax = 224;             // 2*128*224 + 128*56 = 64512 <= 6
 constexpr int kRegsProducer = 56;
 constexpr float kRescaleThreshold = 8.0f;     // log2 units: rescale O only when a row max grows by > 256x
 
+#ifdef QVK_ATTN_TRACE
+// Debug timeline (tools/attn_trace.cu): clock64 stamps of CTA 0 (the heaviest query-tile pair).
+__device__ long long g_attn_trace[1024];
+#define QVK_TRACE(slot)                                                                   \
+    do {                                                                                  \
+        if (blockIdx.x == 0) {                                                            \
+            long long _c;                                                                 \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c));                            \
+            g_attn_trace[(slot)] = _c;                                                    \
+        }                                                                                 \
+    } while (0)
+#else
+#define QVK_TRACE(slot) \
+    do {                \
+    } while (0)
+#endif
+
 struct AttnParams {
     const int64_t* tok_off;
     int n_groups;
@@ -56,7 +75,7 @@ struct Barriers {
     uint64_t kv_full[kStages];
     uint64_t kv_empty[kStages];
     uint64_t s_full[2];
-    uint64_t p_full[2];
+    uint64_t p_full[2][2];  // [tile][half]: P columns 0..63 / 64..127 of the tile are in TMEM
     uint64_t o_done[2];
     uint32_t tmem_base;
 };
@@ -72,6 +91,7 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t tile_addr, int kk) {
     return ptx::umma_desc_sw128(tile_addr + kk * 16 * 128, kChunkBytes, 1024);
 }
 
+template <int kPolyPairs>
 __global__ void __launch_bounds__(kThreads, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -96,6 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nkv = n1 ? n1 : n0;
     const int hk = hq / (p.n_q / p.n_kv);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) QVK_TRACE(1022);
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bar->q_full, 1);
@@ -105,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int t = 0; t < 2; ++t) {
             ptx::mbar_init(&bar->s_full[t], 1);
-            ptx::mbar_init(&bar->p_full[t], 128);
+            ptx::mbar_init(&bar->p_full[t][0], 128);
+            ptx::mbar_init(&bar->p_full[t][1], 128);
             ptx::mbar_init(&bar->o_done[t], 1);
         }
         ptx::fence_mbar_init();
@@ -163,11 +185,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < kD / 16; ++kk)
                     ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
             };
-            auto issue_pv = [&](int t, uint32_t v_addr, bool acc) {
+            // PV in two halves: the first 4 k-steps only need P columns 0..63, which the softmax warps publish
+            // (p_full[t][0]) before they compute the second half — the tensor pipe starts PV while they finish.
+            auto issue_pv = [&](int t, uint32_t v_addr, bool acc, int j) {
 #pragma unroll
-                for (int kk = 0; kk < kBN / 16; ++kk)
-                    ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_addr, kk), kIdPV,
-                                (acc || kk > 0) ? 1u : 0u);
+                for (int h = 0; h < 2; ++h) {
+                    ptx::mbar_wait(&bar->p_full[t][h], j & 1);
+                    QVK_TRACE(j * 8 + 1 + 3 * t + h);
+                    ptx::tc_fence_after();
+#pragma unroll
+                    for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+                        ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_addr, kk), kIdPV,
+                                    (acc || kk > 0) ? 1u : 0u);
+                }
             };
 
             ptx::mbar_wait(&bar->q_full, 0);
@@ -183,11 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < nkv; ++j) {
                 const int v_item = 2 * j + 1;
                 const uint32_t v_addr = wait_item(v_item);
+                QVK_TRACE(j * 8);
                 const bool more = j + 1 < nkv;
                 if (j < n0) {
-                    ptx::mbar_wait(&bar->p_full[0], j & 1);
-                    ptx::tc_fence_after();
-                    issue_pv(0, v_addr, j > 0);
+                    issue_pv(0, v_addr, j > 0, j);
                     if (j == n0 - 1) ptx::mma_commit(&bar->o_done[0]);
                 }
                 uint32_t kn = 0;
@@ -195,17 +224,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (j + 1 < n0) {
                     issue_s(0, kn);
                     ptx::mma_commit(&bar->s_full[0]);
+                    QVK_TRACE(j * 8 + 3);
                 }
                 if (j < n1) {
-                    ptx::mbar_wait(&bar->p_full[1], j & 1);
-                    ptx::tc_fence_after();
-                    issue_pv(1, v_addr, j > 0);
+                    issue_pv(1, v_addr, j > 0, j);
                     if (j == n1 - 1) ptx::mma_commit(&bar->o_done[1]);
                 }
                 ptx::mma_commit(&bar->kv_empty[v_item % kStages]);
                 if (j + 1 < n1) {
                     issue_s(1, kn);
                     ptx::mma_commit(&bar->s_full[1]);
+                    QVK_TRACE(j * 8 + 6);
                 }
                 if (more) ptx::mma_commit(&bar->kv_empty[(v_item + 1) % kStages]);
             }
@@ -227,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float m_ref = -INFINITY, l = 0.f;
             for (int j = 0; j < nt; ++j) {
                 ptx::mbar_wait(&bar->s_full[t], j & 1);
+                if (row == 0) QVK_TRACE(512 + t * 256 + j * 8);
                 ptx::tc_fence_after();
                 float x[128];
                 QVK_TMEM_LD32F(s_col + 0, (x + 0));
@@ -248,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mx3 = fmaxf(mx3, x[c + 3]);
                 }
                 const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+                if (row == 0) QVK_TRACE(512 + t * 256 + j * 8 + 1);
                 const float m_new = mx * sl2;
                 if (j == 0) {
                     m_ref = m_new;
@@ -270,27 +301,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tmem_st_wait();
                     }
                 }
-                const float neg = -m_ref;
-                float sum = 0.f;
+                const ptx::f2 sl2x2 = ptx::f2_make(sl2, sl2);
+                const ptx::f2 negx2 = ptx::f2_make(-m_ref, -m_ref);
+                ptx::f2 acc0 = ptx::f2_make(0.f, 0.f), acc1 = acc0;
 #pragma unroll
                 for (int half = 0; half < 2; ++half) {  // 64 probabilities -> 32 packed bf16x2 columns per store
                     uint32_t pk[32];
 #pragma unroll
                     for (int c = 0; c < 32; ++c) {
-                        const float p0 = ptx::ex2(fmaf(x[64 * half + 2 * c], sl2, neg));
-                        const float p1 = ptx::ex2(fmaf(x[64 * half + 2 * c + 1], sl2, neg));
-                        sum += p0 + p1;
+                        // x*scale - max on FFMA2; 2^x on the MUFU, except kPolyPairs of every 16 pairs on the FMA
+                        // pipe (ex2_poly2) so the two pipes share the exponentials.
+                        const ptx::f2 y = ptx::f2_fma(ptx::f2_make(x[64 * half + 2 * c], x[64 * half + 2 * c + 1]),
+                                                      sl2x2, negx2);
+                        float p0, p1;
+                        ptx::f2_split(y, p0, p1);
+                        if ((c & 15) < kPolyPairs) {
+                            ptx::ex2_poly2(p0, p1);
+                        } else {
+                            p0 = ptx::ex2(p0);
+                            p1 = ptx::ex2(p1);
+                        }
+                        if (c & 1) acc1 = ptx::f2_add(acc1, ptx::f2_make(p0, p1));
+                        else acc0 = ptx::f2_add(acc0, ptx::f2_make(p0, p1));
                         pk[c] = ptx::pack_bf16(p0, p1);
                     }
                     QVK_TMEM_ST32(s_col + 32 * half, pk);
+                    ptx::tmem_st_wait();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bar->p_full[t][half]);
+                    if (row == 0) QVK_TRACE(512 + t * 256 + j * 8 + 2 + half);
                 }
-                l += sum;
-                ptx::tmem_st_wait();
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&bar->p_full[t]);
+                float s0, s1, s2, s3;
+                ptx::f2_split(acc0, s0, s1);
+                ptx::f2_split(acc1, s2, s3);
+                l += (s0 + s1) + (s2 + s3);
             }
             // ---- epilogue: O / l -> bf16 -> HBM ----
             ptx::mbar_wait(&bar->o_done[t], 0);
+            if (row == 0) QVK_TRACE(512 + t * 256 + 255);
             ptx::tc_fence_after();
             const float inv = 1.f / l;
             const int qrow = mt * kBM + row;
@@ -366,12 +414,21 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
         set_error("attention: cuTensorMapEncodeTiled failed");
         return QVK_E_CUDA;
     }
-    static bool attr = false;
-    if (!attr) {
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // kPolyPairs: of every 16 exponential pairs, this many run on the FMA pipe (tuning knob QVK_ATTN_POLY;
+    // 4 measured best on B200).
+    static int poly = -1;
+    if (poly < 0) {
+        const char* e = getenv("QVK_ATTN_POLY");
+        poly = e ? atoi(e) : 4;
+        if (poly != 0 && poly != 4 && poly != 6) poly = 4;
+        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(kSmemBytes)));
-        attr = true;
+        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmemBytes)));
+        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmemBytes)));
     }
+    auto* kern = poly == 0 ? attention_fwd_kernel<0> : poly == 6 ? attention_fwd_kernel<6> : attention_fwd_kernel<4>;
     AttnParams prm;
     prm.tok_off = g->tok_off_d;
     prm.n_groups = g->n_groups;
@@ -383,7 +440,7 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     prm.o = static_cast<__nv_bfloat16*>(o);
     const int64_t blocks = static_cast<int64_t>(prm.pairs_max) * g->n_groups * n_q;
     if (blocks > 0x7fffffff) QVK_INVALID("attention: grid too large");
-    attention_fwd_kernel<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, stream>>>(mq, mk, mv, prm);
+    kern<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, stream>>>(mq, mk, mv, prm);
     QVK_LAUNCH_CHECK();
     return QVK_OK;
 }

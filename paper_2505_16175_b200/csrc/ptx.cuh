@@ -35,6 +35,11 @@ __device__ __forceinline__ void setmaxnreg_dec() {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 
+// Named barrier among `count` threads (multiple of 32) of the CTA; id 0 is __syncthreads'.
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ---- mbarrier -------------------------------------------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -142,6 +147,19 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),           \
         "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
 
+#define QVK_TMEM_LD16(taddr, r)                                                                                   \
+    asm volatile(                                                                                                 \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"   \
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),         \
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])    \
+        : "r"(taddr))
+
+#define QVK_TMEM_ST16(taddr, r)                                                                                   \
+    asm volatile(                                                                                                 \
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"   \
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),      \
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]))
+
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -175,6 +193,51 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
+}
+
+// ---- packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two fp32 lanes per instruction) -------------------
+struct f2 {
+    uint64_t v;
+};
+__device__ __forceinline__ f2 f2_make(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_split(f2 a, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+__device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+
+// 2^x for a pair on the FMA pipe (offloads the MUFU, which is the softmax bottleneck on B200): round-to-nearest
+// split x = j + f with the 1.5*2^23 trick, degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (max rel. error
+// 7.5e-5, far below the bf16 rounding of P), exponent added in the integer domain.  x is clamped to >= -126 so
+// -inf (masked) and huge negative arguments give ~0 instead of wrapping.
+__device__ __forceinline__ void ex2_poly2(float& a, float& b) {
+    const float ca = fmaxf(a, -126.f), cb = fmaxf(b, -126.f);
+    const f2 magic = f2_make(12582912.f, 12582912.f);
+    const f2 nmagic = f2_make(-12582912.f, -12582912.f);
+    const f2 x = f2_make(ca, cb);
+    const f2 t = f2_add(x, magic);                 // low mantissa bits of t hold round(x)
+    const f2 j = f2_add(t, nmagic);                                  // round(x) as float
+    const f2 fr = f2_fma(j, f2_make(-1.f, -1.f), x);                 // x - round(x) in [-0.5, 0.5]
+    f2 p = f2_fma(fr, f2_make(0.05517146f, 0.05517146f), f2_make(0.24261086f, 0.24261086f));
+    p = f2_fma(p, fr, f2_make(0.69326097f, 0.69326097f));
+    p = f2_fma(p, fr, f2_make(0.9999281f, 0.9999281f));
+    float pl, ph, tl, th;
+    f2_split(p, pl, ph);
+    f2_split(t, tl, th);
+    a = __uint_as_float(__float_as_uint(pl) + (__float_as_uint(tl) << 23));
+    b = __uint_as_float(__float_as_uint(ph) + (__float_as_uint(th) << 23));
 }
 
 }  // namespace ptx
