@@ -85,6 +85,53 @@ __global__ void __launch_bounds__(kScoreThreads) score_norm_kernel(const T* __re
     }
 }
 
+// bf16 fast path: one thread per (token, head) row, the row read straight from HBM with kBatch 16-byte loads in
+// flight per thread (a warp's loads cover 32 adjacent rows, so every fetched sector is used — the second half by
+// the next load through L1), then summed in the reference's sequential order.  For bf16 inputs double(x)*double(x)
+// is exact (16 significant bits), so fma(d, d, acc) rounds exactly like acc + d*d (prefill.cpp:207) — bit-identical.
+constexpr int kSeqThreads = 256;
+
+template <int kBatch>
+__global__ void __launch_bounds__(kSeqThreads) score_norm_bf16_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                      int64_t units, int width, int heads,
+                                                                      const int64_t* __restrict__ tok_off,
+                                                                      int n_groups, int negate,
+                                                                      double* __restrict__ out) {
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kSeqThreads + threadIdx.x;
+    if (u >= units) return;
+    const uint4* row = reinterpret_cast<const uint4*>(x + u * width);
+    const int chunks = width >> 3;
+    double acc = 0.0;
+    for (int c0 = 0; c0 < chunks; c0 += kBatch) {
+        uint4 v[kBatch];
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) v[b] = c0 + b < chunks ? __ldg(row + c0 + b) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            if (c0 + b >= chunks) break;
+            const uint32_t w[4] = {v[b].x, v[b].y, v[b].z, v[b].w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t bits = (q & 1) ? (w[q >> 1] & 0xffff0000u) : (w[q >> 1] << 16);
+                const double d = static_cast<double>(__uint_as_float(bits));
+                acc = __fma_rn(d, d, acc);
+            }
+        }
+    }
+    const double norm = __dsqrt_rn(acc);
+    const double sc = negate ? -norm : norm;  // zero key -> -0.0 exactly like the reference
+    if (heads == 1) {
+        out[u] = sc;
+    } else {
+        const int64_t t = u / heads;
+        const int hh = static_cast<int>(u - t * heads);
+        const int g = find_group(tok_off, n_groups, t);
+        const int64_t t0 = __ldg(tok_off + g);
+        const int64_t n = __ldg(tok_off + g + 1) - t0;
+        out[heads * t0 + hh * n + (t - t0)] = sc;
+    }
+}
+
 // attention_score (prefill.cpp:213-230): s_i = (sum_t sum_j double(k_ij) * q_tj) / (T * n_h), t-outer, j-inner,
 // one running double — reproduced in the same order.  q rows are read by every thread at the same time (broadcast);
 // each thread walks its own key row (L1-resident across the t loop).
@@ -115,7 +162,17 @@ int launch_score(cudaStream_t stream, const qvk_groups* g, int64_t total_tokens,
         if (units == 0) return QVK_OK;
         const unsigned blocks = static_cast<unsigned>((units + kScoreThreads - 1) / kScoreThreads);
         const int negate = scorer == QVK_KEY_NORM_SMALL;
-        if (dtype == QVK_F32)
+        const bool fast = dtype == QVK_BF16 && width % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+        if (fast) {
+            const unsigned grid = static_cast<unsigned>((units + kSeqThreads - 1) / kSeqThreads);
+            const auto* xb = static_cast<const __nv_bfloat16*>(x);
+            if (width <= 64)
+                score_norm_bf16_kernel<8><<<grid, kSeqThreads, 0, stream>>>(xb, units, width, heads, g->tok_off_d,
+                                                                            g->n_groups, negate, scores);
+            else
+                score_norm_bf16_kernel<16><<<grid, kSeqThreads, 0, stream>>>(xb, units, width, heads, g->tok_off_d,
+                                                                             g->n_groups, negate, scores);
+        } else if (dtype == QVK_F32)
             score_norm_kernel<float><<<blocks, kScoreThreads, 0, stream>>>(
                 static_cast<const float*>(x), units, width, heads, g->tok_off_d, g->n_groups, negate, scores);
         else

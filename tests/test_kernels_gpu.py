@@ -56,6 +56,25 @@ def test_norm_scores_bitexact_bf16(cuda, sizes, heads, width):
             assert seg.tobytes() == want.tobytes(), (scorer, gi)
 
 
+def test_norm_scores_bitexact_bf16_extremes(cuda):
+    """Arbitrary finite bf16 bit patterns (subnormals, zeros, +-huge, mixed scales): still bit-identical."""
+    rng = np.random.default_rng(7)
+    sizes, heads, width = [513, 64], 4, 128
+    bits = rng.integers(0, 1 << 16, (sum(sizes), heads, width), dtype=np.uint32).astype(np.uint16)
+    bits[(bits & 0x7f80) == 0x7f80] &= 0xbfff  # no inf/nan
+    bits[:, 1, :] = 0  # all-zero rows -> -0.0
+    bits[5, 2, :] = 0x0001  # all-subnormal row
+    x = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).to(cuda)
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    got = qp.score(x, x, g, heads, width, qp.Scorer.key_norm_small).cpu().numpy()
+    xf = f32_of(x)
+    for gi, n in enumerate(sizes):
+        t0 = plan.tok_off[gi]
+        want = O.score_norm(xf[t0:t0 + n], heads, width, True).ravel()
+        assert got[heads * t0: heads * (t0 + n)].tobytes() == want.tobytes(), gi
+
+
 @pytest.mark.parametrize("n,n_h,d_h", [(64, 4, 16), (257, 2, 64), (33, 1, 3)])
 def test_reference_scores_f32_bitexact(cuda, n, n_h, d_h):
     rng = np.random.default_rng(n)
