@@ -309,6 +309,8 @@ def main():
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
     pb = bytes_prune(local_plan, n_kv, d)
+    prof_p = ROOT / "profiles" / "ncu_prune_summary.json"
+    traffic_p = json.loads(prof_p.read_text()).get("dram_bytes_per_launch") if prof_p.exists() else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -326,7 +328,7 @@ def main():
                          "avg_launch_ms": attn_avg},
             "secondary": {"kernels": "score+select+gather (qvk_prune)", "avg_ms": prune_avg,
                           "algorithmic_bytes": pb, "achieved_gbs": pb / (prune_avg / 1e3) / 1e9,
-                          "hbm_peak_gbs": hbm, "frac": pb / (prune_avg / 1e3) / 1e9 / hbm},
+                          "hbm_peak_gbs": hbm, "frac": pb / (prune_avg / 1e3) / 1e9 / hbm, "traffic": traffic_p},
             "clocks": clocks, "e2e": e2e, "gpu_launches": 4 * args.steps,
         }
         if world == 1 and not args.no_cpu_baseline:
