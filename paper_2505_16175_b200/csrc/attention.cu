@@ -1,20 +1,23 @@
 // (a4) Per-group causal GQA attention prefill on sm_100a: TMA -> smem ring -> tcgen05.mma into TMEM, online
-// softmax in registers, P kept in TMEM (TS-MMA), no reference counterpart (PAPER.md:221-223; DESIGN.md §2.4).
+// softmax in registers, P kept in TMEM (TS-MMA), no reference counterpart (PAPER.md:221-223; DESIGN.md §3.1).
 //
-// Work unit = (group g, query head hq, query-tile pair p): two 128-row query tiles (rows [256p, 256p+256) of the
-// group) share every K/V tile the CTA streams (the second tile needs one extra, diagonal, K/V tile).
+// Persistent kernel: one CTA per SM loops over work units in heaviest-first order (unit = group g, query head hq,
+// query-tile pair p: two 128-row query tiles, rows [256p, 256p+256) of the group, sharing every K/V tile the CTA
+// streams; the second tile needs one extra, diagonal, K/V tile).  Consecutive units of a CTA overlap: the next
+// unit's Q load and first S MMAs run while the dedicated epilogue warpgroup drains the previous unit's O.
 //
-// Warp roles (320 threads, 1 CTA per SM):
-//   warps 0-3  softmax for query tile 0   (thread = one TMEM lane = one query row; the whole S row is thread-local)
-//   warps 4-7  softmax for query tile 1
-//   warp  8    TMA producer  (Q0, Q1 once; then K0, V0, K1, V1, ... through a 4-stage 32 KB ring)
-//   warp  9    MMA issuer    (one elected lane) + TMEM owner (512 columns: S0 | S1 | O0 | O1, 128 each)
+// Warp roles (512 threads):
+//   warps 0-3   softmax for query tile 0   (thread = one TMEM lane = one query row; the whole S row is thread-local)
+//   warps 4-7   softmax for query tile 1
+//   warps 8-11  epilogue: O / l -> bf16 -> HBM, then release O's TMEM columns to the MMA warp
+//   warp  12    TMA producer  (Q0, Q1 per unit; K0, V0, K1, V1, ... through a 4-stage 32 KB ring)
+//   warp  13    MMA issuer    (one elected lane) + TMEM owner (512 columns: S0 | S1 | O0 | O1, 128 each)
 // MMA order per K/V step j (FA4-style ping-pong, so the tensor pipe works on one tile while the other's softmax
 // runs):  PV0(j)  S0(j+1)  PV1(j)  S1(j+1).  P_t(j) (bf16) is written by the softmax warps over the first 64 columns
 // of S_t and consumed as the TMEM A operand of PV_t(j); tcgen05 ops execute in issue order, so S_t(j+1) (issued
 // after PV_t(j)) never overwrites P_t(j) early, and the commit of S_t(j+1) also proves PV_t(j) retired — which is
 // what lets the softmax warps rescale O_t in TMEM (lazily, only when a row max grows by > 2^8) without another
-// barrier.
+// barrier.  PV_t(0) of a unit (accumulate = 0) waits until the epilogue released O_t of the previous unit.
 //
 // Layouts: Q/K/V are (tokens, heads, 128) bf16.  Each 128x128 tile lands in smem as two 128-row x 128-byte
 // SWIZZLE_128B chunks (d 0..63, d 64..127) via 3-D TMA boxes {64, 1, 128}.  S = Q K^T uses K-major A and B
@@ -36,19 +39,22 @@ constexpr int kD = 128;                       // head dim
 constexpr int kStages = 4;                    // K/V ring depth
 constexpr uint32_t kTileBytes = kBM * kD * 2; // 32 KB (one bf16 128x128 tile)
 constexpr uint32_t kChunkBytes = kTileBytes / 2;
-constexpr int kThreads = 384;                 // 3 warpgroups: softmax0, softmax1, {TMA, MMA, 2 spare}
-constexpr int kTmaWarp = 8;
-constexpr int kMmaWarp = 9;
-constexpr int kRegsSoftmax = 224;             // 2*128*224 + 128*56 = 64512 <= 65536 registers per SM
-constexpr int kRegsProducer = 56;
+constexpr int kThreads = 512;                 // 4 warpgroups: softmax0, softmax1, epilogue, {TMA, MMA, 2 spare}
+constexpr int kEpiWarp0 = 8;
+constexpr int kTmaWarp = 12;
+constexpr int kMmaWarp = 13;
+// Launch pool 512 * 128 registers: 2*128*184 (softmax) + 128*48 (epilogue) + 128*96 (TMA/MMA) = 65536.
+constexpr int kRegsSoftmax = 184;
+constexpr int kRegsEpilogue = 48;
+constexpr int kRegsProducer = 96;
 constexpr float kRescaleThreshold = 8.0f;     // log2 units: rescale O only when a row max grows by > 256x
 
 #ifdef QVK_ATTN_TRACE
-// Debug timeline (tools/attn_trace.cu): clock64 stamps of CTA 0 (the heaviest query-tile pair).
+// Debug timeline (tools/attn_trace.cu): clock64 stamps of CTA 0's first (heaviest) unit.
 __device__ long long g_attn_trace[1024];
 #define QVK_TRACE(slot)                                                                   \
     do {                                                                                  \
-        if (blockIdx.x == 0) {                                                            \
+        if (blockIdx.x == 0 && unit_iter == 0) {                                          \
             long long _c;                                                                 \
             asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c));                            \
             g_attn_trace[(slot)] = _c;                                                    \
@@ -66,18 +72,23 @@ struct AttnParams {
     int n_q;
     int n_kv;
     int pairs_max;
+    int total_units;
     float scale_log2;
     __nv_bfloat16* o;
 };
 
 struct Barriers {
     uint64_t q_full;
+    uint64_t q_empty;
     uint64_t kv_full[kStages];
     uint64_t kv_empty[kStages];
     uint64_t s_full[2];
     uint64_t p_full[2][2];  // [tile][half]: P columns 0..63 / 64..127 of the tile are in TMEM
-    uint64_t o_done[2];
+    uint64_t o_done[2];     // last PV of the tile retired (MMA commit)
+    uint64_t o_free[2];     // epilogue has O_t in registers: TMEM columns reusable (128 arrivals)
+    uint64_t l_full[2];     // softmax published the row sums of the tile (128 arrivals)
     uint32_t tmem_base;
+    float row_sum[2][2][kBM];  // [unit parity][tile][row]
 };
 
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + (2 + kStages) * kTileBytes + sizeof(Barriers);
@@ -91,6 +102,32 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t tile_addr, int kk) {
     return ptx::umma_desc_sw128(tile_addr + kk * 16 * 128, kChunkBytes, 1024);
 }
 
+// Work unit u (heaviest first: query-tile pairs from the last one down, then group, then q head fastest so the
+// CTAs that run concurrently share K/V tiles through L2).
+struct Unit {
+    int g, hq, hk, mt0, mt1, n, n0, n1, nkv;
+    int64_t tok0;
+    bool valid;
+};
+__device__ __forceinline__ Unit decode_unit(const AttnParams& p, int u) {
+    Unit w;
+    const int per_pair = p.n_groups * p.n_q;
+    const int pair = p.pairs_max - 1 - u / per_pair;
+    const int rem = u % per_pair;
+    w.g = rem / p.n_q;
+    w.hq = rem - w.g * p.n_q;
+    w.hk = w.hq / (p.n_q / p.n_kv);
+    w.tok0 = __ldg(p.tok_off + w.g);
+    w.n = static_cast<int>(__ldg(p.tok_off + w.g + 1) - w.tok0);
+    w.mt0 = 2 * pair;
+    w.mt1 = 2 * pair + 1;
+    w.valid = w.mt0 * kBM < w.n;
+    w.n0 = w.mt0 + 1;                           // K/V tiles of query tile 0 (last one is diagonal)
+    w.n1 = w.mt1 * kBM < w.n ? w.mt1 + 1 : 0;   // K/V tiles of query tile 1 (0: tile absent)
+    w.nkv = w.n1 ? w.n1 : w.n0;
+    return w;
+}
+
 template <int kPolyPairs>
 __global__ void __launch_bounds__(kThreads, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -100,26 +137,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sQ = smem;                       // Q0, Q1
     uint8_t* sKV = smem + 2 * kTileBytes;     // ring
     Barriers* bar = reinterpret_cast<Barriers*>(smem + (2 + kStages) * kTileBytes);
-
-    // ---- work unit (heaviest query-tile pairs first) ----
-    const int per_pair = p.n_groups * p.n_q;
-    const int pair = p.pairs_max - 1 - static_cast<int>(blockIdx.x) / per_pair;
-    const int rem = static_cast<int>(blockIdx.x) % per_pair;
-    const int g = rem / p.n_q;
-    const int hq = rem - g * p.n_q;
-    const int64_t tok0 = p.tok_off[g];
-    const int n = static_cast<int>(p.tok_off[g + 1] - tok0);
-    const int mt0 = 2 * pair, mt1 = 2 * pair + 1;
-    if (mt0 * kBM >= n) return;  // CTA-uniform, before any barrier
-    const int n0 = mt0 + 1;                          // K/V tiles of query tile 0 (last one is diagonal)
-    const int n1 = mt1 * kBM < n ? mt1 + 1 : 0;      // K/V tiles of query tile 1 (0: tile absent)
-    const int nkv = n1 ? n1 : n0;
-    const int hk = hq / (p.n_q / p.n_kv);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int unit_iter = 0;  // per-role count of valid units processed (barrier phases; trace)
     if (threadIdx.x == 0) QVK_TRACE(1022);
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(&bar->q_full, 1);
+        ptx::mbar_init(&bar->q_empty, 1);
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&bar->kv_full[s], 1);
             ptx::mbar_init(&bar->kv_empty[s], 1);
@@ -129,6 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bar->p_full[t][0], 128);
             ptx::mbar_init(&bar->p_full[t][1], 128);
             ptx::mbar_init(&bar->o_done[t], 1);
+            ptx::mbar_init(&bar->o_free[t], 128);
+            ptx::mbar_init(&bar->l_full[t], 128);
         }
         ptx::fence_mbar_init();
     }
@@ -138,124 +164,202 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = bar->tmem_base;
 
-    // Register rebalancing (warpgroup-uniform): producer/issuer warpgroup gives registers to the softmax ones.
-    if (warp >= 8) {
-      ptx::setmaxnreg_dec<kRegsProducer>();
-      if (warp == kTmaWarp) {
-        // ===================== TMA producer =====================
-        if (ptx::elect_one()) {
+    // Register rebalancing (warpgroup-uniform).
+    if (warp >= kTmaWarp) {
+        if (kRegsProducer < 128) ptx::setmaxnreg_dec<kRegsProducer>();
+        if (warp == kTmaWarp && ptx::elect_one()) {
+            // ===================== TMA producer =====================
             ptx::prefetch_tmap(&tm_q);
             ptx::prefetch_tmap(&tm_k);
             ptx::prefetch_tmap(&tm_v);
-            ptx::mbar_arrive_expect_tx(&bar->q_full, n1 ? 2 * kTileBytes : kTileBytes);
-            const int r0 = static_cast<int>(tok0) + mt0 * kBM;
-            ptx::tma_load_3d(sQ, &tm_q, &bar->q_full, 0, hq, r0);
-            ptx::tma_load_3d(sQ + kChunkBytes, &tm_q, &bar->q_full, 64, hq, r0);
-            if (n1) {
-                ptx::tma_load_3d(sQ + kTileBytes, &tm_q, &bar->q_full, 0, hq, r0 + kBM);
-                ptx::tma_load_3d(sQ + kTileBytes + kChunkBytes, &tm_q, &bar->q_full, 64, hq, r0 + kBM);
+            uint32_t item = 0;
+            for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+                const Unit w = decode_unit(p, u);
+                if (!w.valid) continue;
+                ptx::mbar_wait(&bar->q_empty, (unit_iter & 1) ^ 1);  // previous unit's S MMAs retired
+                ptx::mbar_arrive_expect_tx(&bar->q_full, w.n1 ? 2 * kTileBytes : kTileBytes);
+                const int r0 = static_cast<int>(w.tok0) + w.mt0 * kBM;
+                ptx::tma_load_3d(sQ, &tm_q, &bar->q_full, 0, w.hq, r0);
+                ptx::tma_load_3d(sQ + kChunkBytes, &tm_q, &bar->q_full, 64, w.hq, r0);
+                if (w.n1) {
+                    ptx::tma_load_3d(sQ + kTileBytes, &tm_q, &bar->q_full, 0, w.hq, r0 + kBM);
+                    ptx::tma_load_3d(sQ + kTileBytes + kChunkBytes, &tm_q, &bar->q_full, 64, w.hq, r0 + kBM);
+                }
+                // Warm L2 with the CTA's next unit's Q (its load is issued only once this unit's S MMAs retire).
+                for (int un = u + static_cast<int>(gridDim.x); un < p.total_units; un += gridDim.x) {
+                    const Unit nx = decode_unit(p, un);
+                    if (!nx.valid) continue;
+                    const int nr0 = static_cast<int>(nx.tok0) + nx.mt0 * kBM;
+                    ptx::tma_prefetch_3d(&tm_q, 0, nx.hq, nr0);
+                    ptx::tma_prefetch_3d(&tm_q, 64, nx.hq, nr0);
+                    if (nx.n1) {
+                        ptx::tma_prefetch_3d(&tm_q, 0, nx.hq, nr0 + kBM);
+                        ptx::tma_prefetch_3d(&tm_q, 64, nx.hq, nr0 + kBM);
+                    }
+                    break;
+                }
+                for (int it = 0; it < 2 * w.nkv; ++it, ++item) {
+                    const uint32_t st = item % kStages;
+                    ptx::mbar_wait(&bar->kv_empty[st], ((item / kStages) & 1) ^ 1);
+                    const CUtensorMap* map = (it & 1) ? &tm_v : &tm_k;
+                    const int row = static_cast<int>(w.tok0) + (it >> 1) * kBN;
+                    uint8_t* dst = sKV + st * kTileBytes;
+                    ptx::mbar_arrive_expect_tx(&bar->kv_full[st], kTileBytes);
+                    ptx::tma_load_3d(dst, map, &bar->kv_full[st], 0, w.hk, row);
+                    ptx::tma_load_3d(dst + kChunkBytes, map, &bar->kv_full[st], 64, w.hk, row);
+                }
+                ++unit_iter;
             }
-            for (int item = 0; item < 2 * nkv; ++item) {
-                const int st = item % kStages;
-                ptx::mbar_wait(&bar->kv_empty[st], ((item / kStages) & 1) ^ 1);
-                const CUtensorMap* map = (item & 1) ? &tm_v : &tm_k;
-                const int row = static_cast<int>(tok0) + (item >> 1) * kBN;
-                uint8_t* dst = sKV + st * kTileBytes;
-                ptx::mbar_arrive_expect_tx(&bar->kv_full[st], kTileBytes);
-                ptx::tma_load_3d(dst, map, &bar->kv_full[st], 0, hk, row);
-                ptx::tma_load_3d(dst + kChunkBytes, map, &bar->kv_full[st], 64, hk, row);
-            }
-        }
-    } else if (warp == kMmaWarp) {
-        // ===================== MMA issuer =====================
-        if (ptx::elect_one()) {
+        } else if (warp == kMmaWarp && ptx::elect_one()) {
+            // ===================== MMA issuer =====================
             constexpr uint32_t kIdS = ptx::idesc_bf16_f32(kBM, kBN, false, false);
             constexpr uint32_t kIdPV = ptx::idesc_bf16_f32(kBM, kD, false, true);
             const uint32_t q_addr = ptx::smem_u32(sQ);
             const uint32_t ring = ptx::smem_u32(sKV);
-            auto wait_item = [&](int item) -> uint32_t {
-                const int st = item % kStages;
-                ptx::mbar_wait(&bar->kv_full[st], (item / kStages) & 1);
+            uint32_t item = 0;
+            uint32_t pv_step[2] = {0, 0};  // P publications consumed per tile (p_full phases)
+            uint32_t o_units[2] = {0, 0};  // units per tile (o_free phases)
+            for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+                const Unit w = decode_unit(p, u);
+                if (!w.valid) continue;
+                const int nt[2] = {w.n0, w.n1};
+                ptx::mbar_wait(&bar->q_full, unit_iter & 1);
                 ptx::tc_fence_after();
-                return ring + st * kTileBytes;
-            };
-            auto issue_s = [&](int t, uint32_t k_addr) {
-                const uint32_t qa = q_addr + t * kTileBytes;
+                // S_t(j) into TMEM columns [128 t, 128 t + 128)
+                auto issue_s = [&](int t, uint32_t k_addr) {
+                    const uint32_t qa = q_addr + t * kTileBytes;
 #pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk)
-                    ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
-            };
-            // PV in two halves: the first 4 k-steps only need P columns 0..63, which the softmax warps publish
-            // (p_full[t][0]) before they compute the second half — the tensor pipe starts PV while they finish.
-            auto issue_pv = [&](int t, uint32_t v_addr, bool acc, int j) {
+                    for (int kk = 0; kk < kD / 16; ++kk)
+                        ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
+                };
+                // O_t += P_t(j) V(j), in two halves as the softmax publishes P (p_full[t][0], p_full[t][1]).
+                auto issue_pv = [&](int t, uint32_t v_addr, int j) {
+                    if (j == 0) ptx::mbar_wait(&bar->o_free[t], (o_units[t] & 1) ^ 1);
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    ptx::mbar_wait(&bar->p_full[t][h], j & 1);
-                    QVK_TRACE(j * 8 + 1 + 3 * t + h);
+                    for (int h = 0; h < 2; ++h) {
+                        ptx::mbar_wait(&bar->p_full[t][h], pv_step[t] & 1);
+                        QVK_TRACE(j * 8 + 1 + 3 * t + h);
+                        ptx::tc_fence_after();
+#pragma unroll
+                        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+                            ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_addr, kk),
+                                        kIdPV, (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    ++pv_step[t];
+                    if (j == nt[t] - 1) {
+                        ptx::mma_commit(&bar->o_done[t]);
+                        ++o_units[t];
+                    }
+                };
+                auto wait_item = [&](uint32_t it) -> uint32_t {
+                    const uint32_t st = it % kStages;
+                    ptx::mbar_wait(&bar->kv_full[st], (it / kStages) & 1);
                     ptx::tc_fence_after();
-#pragma unroll
-                    for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
-                        ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_addr, kk), kIdPV,
-                                    (acc || kk > 0) ? 1u : 0u);
-                }
-            };
-
-            ptx::mbar_wait(&bar->q_full, 0);
-            ptx::tc_fence_after();
-            uint32_t k_addr = wait_item(0);
-            issue_s(0, k_addr);
-            ptx::mma_commit(&bar->s_full[0]);
-            if (n1) {
-                issue_s(1, k_addr);
-                ptx::mma_commit(&bar->s_full[1]);
-            }
-            ptx::mma_commit(&bar->kv_empty[0]);
-            for (int j = 0; j < nkv; ++j) {
-                const int v_item = 2 * j + 1;
-                const uint32_t v_addr = wait_item(v_item);
-                QVK_TRACE(j * 8);
-                const bool more = j + 1 < nkv;
-                if (j < n0) {
-                    issue_pv(0, v_addr, j > 0, j);
-                    if (j == n0 - 1) ptx::mma_commit(&bar->o_done[0]);
-                }
-                uint32_t kn = 0;
-                if (more) kn = wait_item(v_item + 1);
-                if (j + 1 < n0) {
-                    issue_s(0, kn);
-                    ptx::mma_commit(&bar->s_full[0]);
-                    QVK_TRACE(j * 8 + 3);
-                }
-                if (j < n1) {
-                    issue_pv(1, v_addr, j > 0, j);
-                    if (j == n1 - 1) ptx::mma_commit(&bar->o_done[1]);
-                }
-                ptx::mma_commit(&bar->kv_empty[v_item % kStages]);
-                if (j + 1 < n1) {
-                    issue_s(1, kn);
+                    return ring + st * kTileBytes;
+                };
+                const uint32_t k0 = wait_item(item);
+                issue_s(0, k0);
+                ptx::mma_commit(&bar->s_full[0]);
+                if (w.n1) {
+                    issue_s(1, k0);
                     ptx::mma_commit(&bar->s_full[1]);
-                    QVK_TRACE(j * 8 + 6);
                 }
-                if (more) ptx::mma_commit(&bar->kv_empty[(v_item + 1) % kStages]);
+                if (w.nkv == 1) ptx::mma_commit(&bar->q_empty);  // every S of the unit issued
+                ptx::mma_commit(&bar->kv_empty[item % kStages]);
+                for (int j = 0; j < w.nkv; ++j) {
+                    const uint32_t v_item = item + 2 * j + 1;
+                    const uint32_t v_addr = wait_item(v_item);
+                    QVK_TRACE(j * 8);
+                    const bool more = j + 1 < w.nkv;
+                    if (j < w.n0) issue_pv(0, v_addr, j);
+                    uint32_t kn = 0;
+                    if (more) kn = wait_item(v_item + 1);
+                    if (j + 1 < w.n0) {
+                        issue_s(0, kn);
+                        ptx::mma_commit(&bar->s_full[0]);
+                        QVK_TRACE(j * 8 + 3);
+                    }
+                    if (j < w.n1) issue_pv(1, v_addr, j);
+                    ptx::mma_commit(&bar->kv_empty[v_item % kStages]);
+                    if (j + 1 < w.n1) {
+                        issue_s(1, kn);
+                        ptx::mma_commit(&bar->s_full[1]);
+                        QVK_TRACE(j * 8 + 6);
+                    }
+                    if (j + 2 == w.nkv) ptx::mma_commit(&bar->q_empty);  // the unit's last S was just issued
+                    if (more) ptx::mma_commit(&bar->kv_empty[(v_item + 1) % kStages]);
+                }
+                item += 2 * w.nkv;
+                ++unit_iter;
             }
         }
-      }
+    } else if (warp >= kEpiWarp0) {
+        ptx::setmaxnreg_dec<kRegsEpilogue>();
+        // ===================== epilogue: O / l -> bf16 -> HBM =====================
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        uint32_t t_units[2] = {0, 0};
+        for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+            const Unit w = decode_unit(p, u);
+            if (!w.valid) continue;
+            for (int t = 0; t < 2; ++t) {
+                if (t == 1 && !w.n1) continue;
+                const uint32_t ph = t_units[t] & 1;
+                ptx::mbar_wait(&bar->l_full[t], ph);
+                const float inv = 1.f / bar->row_sum[ph][t][row];
+                ptx::mbar_wait(&bar->o_done[t], ph);
+                ptx::tc_fence_after();
+                const uint32_t o_col = tmem + lane_off + 256 + t * 128;
+                const int qrow = (t ? w.mt1 : w.mt0) * kBM + row;
+                __nv_bfloat16* dst = p.o + ((w.tok0 + qrow) * p.n_q + w.hq) * static_cast<int64_t>(kD);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t o[16];
+                    QVK_TMEM_LD16(o_col + c * 16, o);
+                    ptx::tmem_ld_wait();
+                    if (c == 7) {  // all of O_t has been read: hand its TMEM columns back to the MMA warp
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(&bar->o_free[t]);
+                    }
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        pk[e] = ptx::pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
+                    if (qrow < w.n) {
+                        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 16);
+                        d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    }
+                }
+                ++t_units[t];
+            }
+            ++unit_iter;
+        }
     } else {
         ptx::setmaxnreg_inc<kRegsSoftmax>();
-        // ===================== softmax / correction / epilogue =====================
+        // ===================== softmax (+ lazy O correction) =====================
         const int t = warp >> 2;                 // query tile handled by this warpgroup
         const int quarter = warp & 3;            // TMEM lane quarter this warp may access
         const int row = quarter * 32 + lane;
-        const int mt = t ? mt1 : mt0;
-        const int nt = t ? n1 : n0;
-        if (nt > 0) {
-            const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-            const uint32_t s_col = tmem + lane_off + t * 128;
-            const uint32_t o_col = tmem + lane_off + 256 + t * 128;
-            const float sl2 = p.scale_log2;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t s_col = tmem + lane_off + t * 128;
+        const uint32_t o_col = tmem + lane_off + 256 + t * 128;
+        const float sl2 = p.scale_log2;
+        uint32_t step = 0;   // S tiles consumed (s_full phases)
+        uint32_t units = 0;  // units with this tile (row_sum buffer / l_full phases)
+        for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+            const Unit w = decode_unit(p, u);
+            if (!w.valid) continue;
+            const int mt = t ? w.mt1 : w.mt0;
+            const int nt = t ? w.n1 : w.n0;
+            if (nt == 0) {
+                ++unit_iter;
+                continue;
+            }
             float m_ref = -INFINITY, l = 0.f;
-            for (int j = 0; j < nt; ++j) {
-                ptx::mbar_wait(&bar->s_full[t], j & 1);
+            for (int j = 0; j < nt; ++j, ++step) {
+                ptx::mbar_wait(&bar->s_full[t], step & 1);
                 if (row == 0) QVK_TRACE(512 + t * 256 + j * 8);
                 ptx::tc_fence_after();
                 float x[128];
@@ -290,13 +394,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         l *= f;
                         m_ref = m_upd;
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            uint32_t o[32];
-                            QVK_TMEM_LD32(o_col + c * 32, o);
+                        for (int c = 0; c < 8; ++c) {
+                            uint32_t o[16];
+                            QVK_TMEM_LD16(o_col + c * 16, o);
                             ptx::tmem_ld_wait();
 #pragma unroll
-                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-                            QVK_TMEM_ST32(o_col + c * 32, o);
+                            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                            QVK_TMEM_ST16(o_col + c * 16, o);
                         }
                         ptx::tmem_st_wait();
                     }
@@ -336,28 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::f2_split(acc1, s2, s3);
                 l += (s0 + s1) + (s2 + s3);
             }
-            // ---- epilogue: O / l -> bf16 -> HBM ----
-            ptx::mbar_wait(&bar->o_done[t], 0);
-            if (row == 0) QVK_TRACE(512 + t * 256 + 255);
-            ptx::tc_fence_after();
-            const float inv = 1.f / l;
-            const int qrow = mt * kBM + row;
-            __nv_bfloat16* dst = p.o + ((tok0 + qrow) * p.n_q + hq) * static_cast<int64_t>(kD);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t o[32];
-                QVK_TMEM_LD32(o_col + c * 32, o);
-                ptx::tmem_ld_wait();
-                uint32_t pk[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e)
-                    pk[e] = ptx::pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
-                if (qrow < n) {
-                    uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) d4[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
-                }
-            }
+            bar->row_sum[units & 1][t][row] = l;
+            ptx::mbar_arrive(&bar->l_full[t]);
+            ++units;
+            ++unit_iter;
         }
     }
     ptx::tc_fence_before();
@@ -438,9 +524,17 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     prm.pairs_max = static_cast<int>((tiles + 1) / 2);
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.o = static_cast<__nv_bfloat16*>(o);
-    const int64_t blocks = static_cast<int64_t>(prm.pairs_max) * g->n_groups * n_q;
-    if (blocks > 0x7fffffff) QVK_INVALID("attention: grid too large");
-    kern<<<static_cast<unsigned>(blocks), kThreads, kSmemBytes, stream>>>(mq, mk, mv, prm);
+    const int64_t units = static_cast<int64_t>(prm.pairs_max) * g->n_groups * n_q;
+    if (units > 0x7fffffff) QVK_INVALID("attention: too many work units");
+    prm.total_units = static_cast<int>(units);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        QVK_CUDA_CHECK(cudaGetDevice(&dev));
+        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
+    kern<<<grid, kThreads, kSmemBytes, stream>>>(mq, mk, mv, prm);
     QVK_LAUNCH_CHECK();
     return QVK_OK;
 }
