@@ -35,10 +35,11 @@ namespace {
 
 constexpr int kBM = 128;                      // query rows per tile
 constexpr int kBN = 128;                      // kv rows per tile
-constexpr int kD = 128;                       // head dim
 constexpr int kStages = 4;                    // K/V ring depth
-constexpr uint32_t kTileBytes = kBM * kD * 2; // 32 KB (one bf16 128x128 tile)
-constexpr uint32_t kChunkBytes = kTileBytes / 2;
+constexpr uint32_t kChunkBytes = kBM * 64 * 2; // one 128-row x 128-byte SW128 chunk (64 head-dim columns)
+// Head dim D in {64, 128}: a 128-row Q/K/V tile is D/64 chunks.
+template <int D>
+__host__ __device__ constexpr uint32_t tile_bytes() { return kChunkBytes * (D / 64); }
 constexpr int kThreads = 512;                 // 4 warpgroups: softmax0, softmax1, epilogue, {TMA, MMA, 2 spare}
 constexpr int kEpiWarp0 = 8;
 constexpr int kTmaWarp = 12;
@@ -91,7 +92,8 @@ struct Barriers {
     float row_sum[2][2][kBM];  // [unit parity][tile][row]
 };
 
-constexpr size_t kSmemBytes = 1024 /*align slack*/ + (2 + kStages) * kTileBytes + sizeof(Barriers);
+template <int D>
+constexpr size_t smem_bytes() { return 1024 /*align slack*/ + (2 + kStages) * tile_bytes<D>() + sizeof(Barriers); }
 
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_addr, int kk) {
     // k-step kk (16 elements) of a K-major SW128 tile: chunk kk/4, +32 B per step inside the 128-byte row.
@@ -128,10 +130,11 @@ __device__ __forceinline__ Unit decode_unit(const AttnParams& p, int u) {
     return w;
 }
 
-template <int kPolyPairs>
+template <int D, int kPolyPairs>
 __global__ void __launch_bounds__(kThreads, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+    constexpr uint32_t kTileBytes = tile_bytes<D>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                       // Q0, Q1
@@ -179,22 +182,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(&bar->q_empty, (unit_iter & 1) ^ 1);  // previous unit's S MMAs retired
                 ptx::mbar_arrive_expect_tx(&bar->q_full, w.n1 ? 2 * kTileBytes : kTileBytes);
                 const int r0 = static_cast<int>(w.tok0) + w.mt0 * kBM;
-                ptx::tma_load_3d(sQ, &tm_q, &bar->q_full, 0, w.hq, r0);
-                ptx::tma_load_3d(sQ + kChunkBytes, &tm_q, &bar->q_full, 64, w.hq, r0);
-                if (w.n1) {
-                    ptx::tma_load_3d(sQ + kTileBytes, &tm_q, &bar->q_full, 0, w.hq, r0 + kBM);
-                    ptx::tma_load_3d(sQ + kTileBytes + kChunkBytes, &tm_q, &bar->q_full, 64, w.hq, r0 + kBM);
+#pragma unroll
+                for (int c = 0; c < D / 64; ++c) {
+                    ptx::tma_load_3d(sQ + c * kChunkBytes, &tm_q, &bar->q_full, 64 * c, w.hq, r0);
+                    if (w.n1)
+                        ptx::tma_load_3d(sQ + kTileBytes + c * kChunkBytes, &tm_q, &bar->q_full, 64 * c, w.hq,
+                                         r0 + kBM);
                 }
                 // Warm L2 with the CTA's next unit's Q (its load is issued only once this unit's S MMAs retire).
                 for (int un = u + static_cast<int>(gridDim.x); un < p.total_units; un += gridDim.x) {
                     const Unit nx = decode_unit(p, un);
                     if (!nx.valid) continue;
                     const int nr0 = static_cast<int>(nx.tok0) + nx.mt0 * kBM;
-                    ptx::tma_prefetch_3d(&tm_q, 0, nx.hq, nr0);
-                    ptx::tma_prefetch_3d(&tm_q, 64, nx.hq, nr0);
-                    if (nx.n1) {
-                        ptx::tma_prefetch_3d(&tm_q, 0, nx.hq, nr0 + kBM);
-                        ptx::tma_prefetch_3d(&tm_q, 64, nx.hq, nr0 + kBM);
+#pragma unroll
+                    for (int c = 0; c < D / 64; ++c) {
+                        ptx::tma_prefetch_3d(&tm_q, 64 * c, nx.hq, nr0);
+                        if (nx.n1) ptx::tma_prefetch_3d(&tm_q, 64 * c, nx.hq, nr0 + kBM);
                     }
                     break;
                 }
@@ -205,15 +208,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int row = static_cast<int>(w.tok0) + (it >> 1) * kBN;
                     uint8_t* dst = sKV + st * kTileBytes;
                     ptx::mbar_arrive_expect_tx(&bar->kv_full[st], kTileBytes);
-                    ptx::tma_load_3d(dst, map, &bar->kv_full[st], 0, w.hk, row);
-                    ptx::tma_load_3d(dst + kChunkBytes, map, &bar->kv_full[st], 64, w.hk, row);
+#pragma unroll
+                    for (int c = 0; c < D / 64; ++c)
+                        ptx::tma_load_3d(dst + c * kChunkBytes, map, &bar->kv_full[st], 64 * c, w.hk, row);
                 }
                 ++unit_iter;
             }
         } else if (warp == kMmaWarp && ptx::elect_one()) {
             // ===================== MMA issuer =====================
             constexpr uint32_t kIdS = ptx::idesc_bf16_f32(kBM, kBN, false, false);
-            constexpr uint32_t kIdPV = ptx::idesc_bf16_f32(kBM, kD, false, true);
+            constexpr uint32_t kIdPV = ptx::idesc_bf16_f32(kBM, D, false, true);
             const uint32_t q_addr = ptx::smem_u32(sQ);
             const uint32_t ring = ptx::smem_u32(sKV);
             uint32_t item = 0;
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 auto issue_s = [&](int t, uint32_t k_addr) {
                     const uint32_t qa = q_addr + t * kTileBytes;
 #pragma unroll
-                    for (int kk = 0; kk < kD / 16; ++kk)
+                    for (int kk = 0; kk < D / 16; ++kk)
                         ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
                 };
                 // O_t += P_t(j) V(j), in two halves as the softmax publishes P (p_full[t][0], p_full[t][1]).
@@ -312,13 +316,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t o_col = tmem + lane_off + 256 + t * 128;
                 const int qrow = (t ? w.mt1 : w.mt0) * kBM + row;
-                __nv_bfloat16* dst = p.o + ((w.tok0 + qrow) * p.n_q + w.hq) * static_cast<int64_t>(kD);
+                __nv_bfloat16* dst = p.o + ((w.tok0 + qrow) * p.n_q + w.hq) * static_cast<int64_t>(D);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                for (int c = 0; c < D / 16; ++c) {
                     uint32_t o[16];
                     QVK_TMEM_LD16(o_col + c * 16, o);
                     ptx::tmem_ld_wait();
-                    if (c == 7) {  // all of O_t has been read: hand its TMEM columns back to the MMA warp
+                    if (c == D / 16 - 1) {  // all of O_t has been read: hand its TMEM columns back to the MMA warp
                         ptx::tc_fence_before();
                         ptx::mbar_arrive(&bar->o_free[t]);
                     }
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         l *= f;
                         m_ref = m_upd;
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) {
+                        for (int c = 0; c < D / 16; ++c) {
                             uint32_t o[16];
                             QVK_TMEM_LD16(o_col + c * 16, o);
                             ptx::tmem_ld_wait();
@@ -467,7 +471,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // (tokens, heads, 128) bf16 viewed as a 3-D tensor {d, heads, tokens}; box {64, 1, 128}, 128-byte swizzle.
-bool make_map(CUtensorMap* m, const void* base, int heads, int64_t tokens) {
+bool make_map(CUtensorMap* m, const void* base, int heads, int64_t tokens, int kD) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(kD), static_cast<cuuint64_t>(heads),
@@ -480,12 +484,27 @@ bool make_map(CUtensorMap* m, const void* base, int heads, int64_t tokens) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int D, int kPoly>
+int launch_attention_d(cudaStream_t stream, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                       const AttnParams& prm, unsigned grid) {
+    static bool attr = false;
+    if (!attr) {
+        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<D, kPoly>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem_bytes<D>())));
+        attr = true;
+    }
+    attention_fwd_kernel<D, kPoly><<<grid, kThreads, smem_bytes<D>(), stream>>>(mq, mk, mv, prm);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
 }  // namespace
 
 int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, const void* v, int n_q,
                      int n_kv, int d_h, float scale, void* o) {
-    if (d_h != kD) {
-        set_error("attention: only head_dim 128 is implemented (got " + std::to_string(d_h) + ")");
+    if (d_h != 128 && d_h != 64) {
+        set_error("attention: head_dim must be 64 or 128 (got " + std::to_string(d_h) + ")");
         return QVK_E_UNSUPPORTED;
     }
     if (n_q <= 0 || n_kv <= 0 || n_q % n_kv != 0) QVK_INVALID("attention: n_q must be a positive multiple of n_kv");
@@ -495,26 +514,11 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     if (g->total_tokens == 0 || g->max_tokens == 0) return QVK_OK;
     if (g->total_tokens > 0x7fffffff) QVK_INVALID("attention: more than 2^31 token rows");
     CUtensorMap mq, mk, mv;
-    if (!make_map(&mq, q, n_q, g->total_tokens) || !make_map(&mk, k, n_kv, g->total_tokens) ||
-        !make_map(&mv, v, n_kv, g->total_tokens)) {
+    if (!make_map(&mq, q, n_q, g->total_tokens, d_h) || !make_map(&mk, k, n_kv, g->total_tokens, d_h) ||
+        !make_map(&mv, v, n_kv, g->total_tokens, d_h)) {
         set_error("attention: cuTensorMapEncodeTiled failed");
         return QVK_E_CUDA;
     }
-    // kPolyPairs: of every 16 exponential pairs, this many run on the FMA pipe (tuning knob QVK_ATTN_POLY;
-    // 4 measured best on B200).
-    static int poly = -1;
-    if (poly < 0) {
-        const char* e = getenv("QVK_ATTN_POLY");
-        poly = e ? atoi(e) : 4;
-        if (poly != 0 && poly != 4 && poly != 6) poly = 4;
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(kSmemBytes)));
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(kSmemBytes)));
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(kSmemBytes)));
-    }
-    auto* kern = poly == 0 ? attention_fwd_kernel<0> : poly == 6 ? attention_fwd_kernel<6> : attention_fwd_kernel<4>;
     AttnParams prm;
     prm.tok_off = g->tok_off_d;
     prm.n_groups = g->n_groups;
@@ -534,9 +538,17 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
         QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
-    kern<<<grid, kThreads, kSmemBytes, stream>>>(mq, mk, mv, prm);
-    QVK_LAUNCH_CHECK();
-    return QVK_OK;
+    // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 4).
+    static int poly = -1;
+    if (poly < 0) {
+        const char* e = getenv("QVK_ATTN_POLY");
+        poly = (e && atoi(e) == 0) ? 0 : 4;
+    }
+    if (d_h == 128)
+        return poly ? launch_attention_d<128, 4>(stream, mq, mk, mv, prm, grid)
+                    : launch_attention_d<128, 0>(stream, mq, mk, mv, prm, grid);
+    return poly ? launch_attention_d<64, 4>(stream, mq, mk, mv, prm, grid)
+                : launch_attention_d<64, 0>(stream, mq, mk, mv, prm, grid);
 }
 
 }  // namespace qvk

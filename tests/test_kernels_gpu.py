@@ -243,18 +243,35 @@ def check_tol(got, want, what):
     return err.max().item()
 
 
-@pytest.mark.parametrize("sizes,n_q,n_kv", [([128], 1, 1), ([256], 2, 1), ([384, 100, 1, 129], 28, 4),
-                                            ([4096], 28, 4), ([4096] * 2 + [1000], 28, 4), ([16384], 4, 4)])
-def test_attention_vs_torch_fp32(cuda, sizes, n_q, n_kv):
+@pytest.mark.parametrize("sizes,n_q,n_kv,d", [([128], 1, 1, 128), ([256], 2, 1, 128), ([384, 100, 1, 129], 28, 4, 128),
+                                              ([4096], 28, 4, 128), ([4096] * 2 + [1000], 28, 4, 128),
+                                              ([16384], 4, 4, 128), ([256] * 4, 4, 2, 64), ([1000, 37, 4096], 28, 4, 64)])
+def test_attention_vs_torch_fp32(cuda, sizes, n_q, n_kv, d):
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, d, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, d, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, d, 2, False, cuda)
+    o = qp.attention(q, k, v, g, n_q, n_kv)
+    torch.cuda.synchronize()
+    want = torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(d))
+    check_tol(o, want, f"attention {sizes} d={d}")
+
+
+def test_attention_persistent_many_units(cuda):
+    """More work units than SMs with ragged groups: every CTA runs several units back to back (TMEM / barrier
+    phases carried across units), including units whose second query tile is absent."""
+    sizes, n_q, n_kv = [1100, 129, 4096, 300, 2000, 77], 28, 4
     plan = qp.GroupPlan.from_sizes(sizes, 0.5)
     g = plan.to(cuda)
     q = synth_groups(sizes, n_q, 128, 3, False, cuda)
     k = synth_groups(sizes, n_kv, 128, 1, True, cuda)
     v = synth_groups(sizes, n_kv, 128, 2, False, cuda)
-    o = qp.attention(q, k, v, g, n_q, n_kv)
+    o1 = qp.attention(q, k, v, g, n_q, n_kv)
+    o2 = qp.attention(q, k, v, g, n_q, n_kv)
     torch.cuda.synchronize()
-    want = torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(128))
-    check_tol(o, want, f"attention {sizes}")
+    assert torch.equal(o1, o2), "attention must be deterministic"
+    check_tol(o1, torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(128)), "persistent")
 
 
 def test_attention_vs_double_oracle(cuda):
