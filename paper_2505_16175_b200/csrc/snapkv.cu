@@ -4,7 +4,12 @@
 // Two passes over K per (group, head): (1) per window row max/sum of the causal logits, (2) per key the sum of the
 // normalised probabilities.  fp32 FMA on CUDA cores; HBM reads of K are the algorithmic bytes
 // (N * d * 2 + W * n_q * d * 2 read, N * n_kv * 8 written per group).
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace qvk {
 namespace {
@@ -142,6 +147,246 @@ __global__ void snap_pool_kernel(const float* __restrict__ raw, const int64_t* _
     }
 }
 
+// ---------------------------------------------------------------------------------------------------------------
+// tcgen05 path (d_h = 128, gq * W <= 256 with gq = n_q / n_kv): the 224 window query rows of a KV head (gq heads x
+// W rows) are one smem operand; both passes run on the tensor pipe and the exponentials on the CUDA cores.
+//   pass 1  S  = Q_obs K_t^T  (M = 128 window rows per MMA, two M-tiles; N = 128 keys): row max / sum, online over
+//           key tiles — thread-local (thread = TMEM lane = window row);
+//   pass 2  S' = K_t Q_obs^T  (M = 128 keys, N = ceil32(gq W) window rows): per-key sum of the normalised
+//           probabilities — again thread-local (thread = key), so no cross-thread column reduction is needed.
+// Work item = (group, KV head), persistent over items.  320 threads: warps 0-3 / 4-7 = two compute sets (pass 1:
+// M-tile A / B rows; pass 2: the first / second half of the window columns, combined through smem), warp 8 TMA,
+// warp 9 MMA.  TMEM: pass-1 S_A | S_B (256 columns), pass-2 S' (<= 256 columns).
+// Algorithmic bytes per (group, layer): K read once from HBM (pass 2 re-reads it from L2) + the window Q rows +
+// n_kv * N * 8 score bytes.
+constexpr int kSnapStages = 3;
+constexpr uint32_t kSnapChunk = 128 * 128;          // 128 rows x 128 B (one SW128 chunk of a key tile)
+constexpr uint32_t kSnapKTile = 2 * kSnapChunk;      // 128 keys x 128 d bf16
+constexpr uint32_t kSnapQChunk = 256 * 128;          // window-row operand: up to 256 rows x 128 B per d-chunk
+constexpr int kSnapThreads = 320;
+
+struct SnapShared {
+    uint64_t q_full, q_empty, acc_full, acc_empty;
+    uint64_t kv_full[kSnapStages], kv_empty[kSnapStages];
+    uint32_t tmem_base;
+    float bias[256];       // per window column: m + log2(l) (log2 domain); +inf for invalid rows
+    int pos[256];          // per window column: token position of its query row inside the group (-1: invalid)
+    float part[2][128];    // pass-2 partial sums of the second column half, by key tile parity
+};
+constexpr size_t kSnapSmem = 1024 + 2 * kSnapQChunk + kSnapStages * kSnapKTile + sizeof(SnapShared);
+
+struct SnapParams {
+    const int64_t* tok_off;
+    int n_groups, n_kv, gq, window, rows, rows_pad;
+    float sl2;
+    float* raw;  // (group, head, token) layout
+};
+
+__device__ __forceinline__ uint64_t snap_desc(uint32_t chunk_addr, uint32_t chunk_stride, int kk) {
+    // k-step kk (16 of the 128 head-dim columns) of a K-major SW128 operand stored as two d-chunks.
+    return ptx::umma_desc_sw128(chunk_addr + (kk >> 2) * chunk_stride + (kk & 3) * 32, 16, 1024);
+}
+
+__global__ void __launch_bounds__(kSnapThreads, 1)
+    snapkv_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                     const SnapParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = smem + 2 * kSnapQChunk;
+    SnapShared* sh = reinterpret_cast<SnapShared*>(sK + kSnapStages * kSnapKTile);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int items = p.n_groups * p.n_kv;
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&sh->q_full, 1);
+        ptx::mbar_init(&sh->q_empty, 1);
+        ptx::mbar_init(&sh->acc_full, 1);
+        ptx::mbar_init(&sh->acc_empty, 256);
+        for (int st = 0; st < kSnapStages; ++st) {
+            ptx::mbar_init(&sh->kv_full[st], 1);
+            ptx::mbar_init(&sh->kv_empty[st], 1);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 9) ptx::tmem_alloc<512>(&sh->tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = sh->tmem_base;
+
+    if (warp == 8) {
+        if (ptx::elect_one()) {  // ===== TMA producer =====
+            uint32_t item_no = 0, tile_no = 0;
+            for (int it = blockIdx.x; it < items; it += gridDim.x, ++item_no) {
+                const int g = it / p.n_kv, hk = it - g * p.n_kv;
+                const int64_t t0 = __ldg(p.tok_off + g);
+                const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - t0);
+                const int nt = (n + 127) / 128;
+                ptx::mbar_wait(&sh->q_empty, (item_no & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&sh->q_full, 2 * p.rows * 128);
+                const int w0 = static_cast<int>(t0) + n - p.window;  // may start before the group: rows masked
+                ptx::tma_load_3d(sQ, &tm_q, &sh->q_full, 0, hk * p.gq, w0);
+                ptx::tma_load_3d(sQ + kSnapQChunk, &tm_q, &sh->q_full, 64, hk * p.gq, w0);
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int jt = 0; jt < nt; ++jt, ++tile_no) {
+                        const uint32_t st = tile_no % kSnapStages;
+                        ptx::mbar_wait(&sh->kv_empty[st], ((tile_no / kSnapStages) & 1) ^ 1);
+                        uint8_t* dst = sK + st * kSnapKTile;
+                        ptx::mbar_arrive_expect_tx(&sh->kv_full[st], kSnapKTile);
+                        const int row = static_cast<int>(t0) + jt * 128;
+                        ptx::tma_load_3d(dst, &tm_k, &sh->kv_full[st], 0, hk, row);
+                        ptx::tma_load_3d(dst + kSnapChunk, &tm_k, &sh->kv_full[st], 64, hk, row);
+                    }
+            }
+        }
+    } else if (warp == 9) {
+        if (ptx::elect_one()) {  // ===== MMA issuer =====
+            const uint32_t id1 = ptx::idesc_bf16_f32(128, 128, false, false);
+            const uint32_t id2 = ptx::idesc_bf16_f32(128, p.rows_pad, false, false);
+            const uint32_t q_addr = ptx::smem_u32(sQ), k_base = ptx::smem_u32(sK);
+            uint32_t item_no = 0, tile_no = 0, acc_no = 0;
+            for (int it = blockIdx.x; it < items; it += gridDim.x, ++item_no) {
+                const int g = it / p.n_kv;
+                const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - __ldg(p.tok_off + g));
+                const int nt = (n + 127) / 128;
+                ptx::mbar_wait(&sh->q_full, item_no & 1);
+                ptx::tc_fence_after();
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int jt = 0; jt < nt; ++jt, ++tile_no, ++acc_no) {
+                        const uint32_t st = tile_no % kSnapStages;
+                        ptx::mbar_wait(&sh->kv_full[st], (tile_no / kSnapStages) & 1);
+                        ptx::mbar_wait(&sh->acc_empty, (acc_no & 1) ^ 1);
+                        ptx::tc_fence_after();
+                        const uint32_t ka = k_base + st * kSnapKTile;
+                        if (pass == 0) {
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk) {
+                                const uint64_t bk = snap_desc(ka, kSnapChunk, kk);
+                                ptx::mma_ss(tmem, snap_desc(q_addr, kSnapQChunk, kk), bk, id1, kk > 0);
+                                ptx::mma_ss(tmem + 128, snap_desc(q_addr + 128 * 128, kSnapQChunk, kk), bk, id1,
+                                            kk > 0);
+                            }
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk)
+                                ptx::mma_ss(tmem + 256, snap_desc(ka, kSnapChunk, kk),
+                                            snap_desc(q_addr, kSnapQChunk, kk), id2, kk > 0);
+                        }
+                        ptx::mma_commit(&sh->kv_empty[st]);
+                        ptx::mma_commit(&sh->acc_full);
+                        if (pass == 1 && jt == nt - 1) ptx::mma_commit(&sh->q_empty);
+                    }
+            }
+        }
+    } else {
+        // ===== compute: warps 0-3 (set 0) and 4-7 (set 1) =====
+        const int set = warp >> 2, quarter = warp & 3;
+        const int i = quarter * 32 + lane;  // TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const float sl2 = p.sl2;
+        uint32_t acc_no = 0;
+        const int nchunks = p.rows_pad / 32;
+        const int half_chunks = (nchunks + 1) / 2;
+        const int c_lo = set ? half_chunks : 0, c_hi = set ? nchunks : half_chunks;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            const int g = it / p.n_kv, hk = it - g * p.n_kv;
+            const int64_t t0 = __ldg(p.tok_off + g);
+            const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - t0);
+            const int nt = (n + 127) / 128;
+            // window column c = r * gq + h -> query token position n - W + r (invalid when < 0)
+            const int c_row = set * 128 + i;
+            const int my_pos = c_row < p.rows ? n - p.window + c_row / p.gq : -1;
+            // ---- pass 1: row max / sum of window row c_row (set 0: rows 0..127, set 1: rows 128..255) ----
+            float m = -INFINITY, l = 0.f;
+            for (int jt = 0; jt < nt; ++jt, ++acc_no) {
+                ptx::mbar_wait(&sh->acc_full, acc_no & 1);
+                ptx::tc_fence_after();
+                float x[128];
+                const uint32_t col = tmem + lane_off + set * 128;
+                QVK_TMEM_LD32F(col + 0, (x + 0));
+                QVK_TMEM_LD32F(col + 32, (x + 32));
+                QVK_TMEM_LD32F(col + 64, (x + 64));
+                QVK_TMEM_LD32F(col + 96, (x + 96));
+                ptx::tmem_ld_wait();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&sh->acc_empty);
+                if (my_pos >= 0) {
+                    const int j0 = jt * 128;
+                    if (j0 + 127 > my_pos) {
+#pragma unroll
+                        for (int c = 0; c < 128; ++c)
+                            if (j0 + c > my_pos) x[c] = -INFINITY;
+                    }
+                    float mx = x[0];
+#pragma unroll
+                    for (int c = 1; c < 128; ++c) mx = fmaxf(mx, x[c]);
+                    const float mn = fmaxf(m, mx * sl2);
+                    float sum = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 128; ++c) sum += ptx::ex2(fmaf(x[c], sl2, -mn));
+                    l = (m == -INFINITY ? 0.f : l * ptx::ex2(m - mn)) + sum;
+                    m = mn;
+                }
+            }
+            sh->bias[c_row] = my_pos >= 0 ? m + __log2f(l) : INFINITY;
+            sh->pos[c_row] = my_pos;
+            ptx::named_bar_sync(1, 256);
+            // ---- pass 2: key j = jt*128 + i, columns [32 c_lo, 32 c_hi) of this set ----
+            for (int jt = 0; jt < nt; ++jt, ++acc_no) {
+                ptx::mbar_wait(&sh->acc_full, acc_no & 1);
+                ptx::tc_fence_after();
+                const int j = jt * 128 + i;
+                const bool edge = jt * 128 + 127 > n - p.window;  // some window rows precede some keys
+                float acc = 0.f;
+                for (int ch = c_lo; ch < c_hi; ++ch) {
+                    float x[32];
+                    QVK_TMEM_LD32F(tmem + lane_off + 256 + 32 * ch, x);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const int c = 32 * ch + e;
+                        float y = fmaf(x[e], sl2, -sh->bias[c]);
+                        if (edge && j > sh->pos[c]) y = -INFINITY;
+                        acc += ptx::ex2(y);
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&sh->acc_empty);
+                if (set) sh->part[jt & 1][i] = acc;
+                ptx::named_bar_sync(2 + quarter, 64);
+                if (!set && j < n) p.raw[p.n_kv * t0 + static_cast<int64_t>(hk) * n + j] = acc + sh->part[jt & 1][i];
+            }
+            ptx::named_bar_sync(1, 256);  // bias / pos reused by the next item
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+bool snap_map(CUtensorMap* m, const void* base, int heads, int64_t tokens, uint32_t box_heads, uint32_t box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(tokens)};
+    cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(heads) * 256};
+    cuuint32_t box[3] = {64, box_heads, box_rows};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, int n_q, int n_kv,
@@ -158,9 +403,41 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
     float2* stats = nullptr;
     float* raw = nullptr;
     const int64_t total = g->total_tokens * n_kv;
+    QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
+    const int gq = n_q / n_kv;
+    if (gq * window <= 256 && window <= 256 && !getenv("QVK_SNAPKV_SIMT")) {
+        CUtensorMap mq, mk;
+        if (!snap_map(&mq, q, n_q, g->total_tokens, static_cast<uint32_t>(gq), static_cast<uint32_t>(window)) ||
+            !snap_map(&mk, k, n_kv, g->total_tokens, 1, 128)) {
+            cudaFreeAsync(raw, stream);
+            set_error("snapkv: cuTensorMapEncodeTiled failed");
+            return QVK_E_CUDA;
+        }
+        static bool attr = false;
+        if (!attr) {
+            QVK_CUDA_CHECK(cudaFuncSetAttribute(snapkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(kSnapSmem)));
+            attr = true;
+        }
+        SnapParams sp;
+        sp.tok_off = g->tok_off_d;
+        sp.n_groups = g->n_groups;
+        sp.n_kv = n_kv;
+        sp.gq = gq;
+        sp.window = window;
+        sp.rows = gq * window;
+        sp.rows_pad = (sp.rows + 31) / 32 * 32;
+        sp.sl2 = sl2;
+        sp.raw = raw;
+        int dev = 0, sms = 0;
+        QVK_CUDA_CHECK(cudaGetDevice(&dev));
+        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(static_cast<int64_t>(g->n_groups) * n_kv, sms));
+        snapkv_tc_kernel<<<grid, kSnapThreads, kSnapSmem, stream>>>(mq, mk, sp);
+        QVK_LAUNCH_CHECK();
+    } else {
     QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&stats),
                                    sizeof(float2) * g->n_groups * n_q * static_cast<size_t>(window), stream));
-    QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
     snap_stats_kernel<<<dim3(g->n_groups, n_q), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), g->tok_off_d, n_q, n_kv, window,
         sl2, stats);
@@ -170,10 +447,11 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), g->tok_off_d, n_q, n_kv, window,
         sl2, stats, raw);
     QVK_LAUNCH_CHECK();
+    QVK_CUDA_CHECK(cudaFreeAsync(stats, stream));
+    }
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, kNumSms * 16));
     snap_pool_kernel<<<blocks, 256, 0, stream>>>(raw, g->tok_off_d, g->n_groups, n_kv, total, pool, scores);
     QVK_LAUNCH_CHECK();
-    QVK_CUDA_CHECK(cudaFreeAsync(stats, stream));
     QVK_CUDA_CHECK(cudaFreeAsync(raw, stream));
     return QVK_OK;
 }
