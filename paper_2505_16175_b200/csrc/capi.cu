@@ -16,7 +16,7 @@ int launch_score(cudaStream_t, const qvk_groups*, int64_t, const void*, const vo
                  const float*, int64_t, int, double*);
 int launch_select(cudaStream_t, const qvk_groups*, const double*, int, uint32_t*);
 int launch_gather(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const uint32_t*, void*,
-                  void*, uint64_t*);
+                  void*, uint64_t*, int64_t);
 int launch_attention(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, int, float,
                      void*);
 int launch_snapkv(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, int, int, float,
@@ -174,13 +174,20 @@ int qvk_select(qvk_stream_t s, const qvk_groups* g, const double* scores, int32_
     return launch_select(s, g, scores, heads, idx);
 }
 
-int qvk_gather(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
-               int32_t width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin) {
+namespace {
+int gather_checked(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
+                   int32_t width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin, int64_t keep_stride) {
     QVK_TRY(check_groups(g));
     if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
     if (dtype != QVK_F32 && dtype != QVK_BF16) QVK_INVALID("gather: unsupported dtype");
     if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
-    return launch_gather(s, g, k, v, dtype, heads, width, idx, kc, vc, origin);
+    return launch_gather(s, g, k, v, dtype, heads, width, idx, kc, vc, origin, keep_stride);
+}
+}  // namespace
+
+int qvk_gather(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
+               int32_t width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin) {
+    return gather_checked(s, g, k, v, dtype, heads, width, idx, kc, vc, origin, 0);
 }
 
 int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
@@ -188,8 +195,9 @@ int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v,
               double* scores_ws, uint32_t* idx_ws, void* kc, void* vc, uint64_t* origin) {
     QVK_TRY(check_rho(rho));  // prefill.cpp:258, validated before anything else
     QVK_TRY(check_groups(g));
+    const int64_t keep_full = static_cast<int64_t>(retained(rho, static_cast<size_t>(g->max_tokens)));
     if (rho == 1.0)  // prefill.cpp:263-270: identity, no scoring, no shape check
-        return qvk_gather(s, g, k, v, dtype, heads, width, nullptr, kc, vc, origin);
+        return gather_checked(s, g, k, v, dtype, heads, width, nullptr, kc, vc, origin, keep_full);
     double* sc = scores_ws;
     uint32_t* ix = idx_ws;
     if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
@@ -198,7 +206,7 @@ int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v,
                                             sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
     int rc = qvk_score(s, g, k, v, dtype, heads, width, scorer, tq, text_count, n_h, sc);
     if (rc == QVK_OK) rc = qvk_select(s, g, sc, heads, ix);
-    if (rc == QVK_OK) rc = qvk_gather(s, g, k, v, dtype, heads, width, ix, kc, vc, origin);
+    if (rc == QVK_OK) rc = gather_checked(s, g, k, v, dtype, heads, width, ix, kc, vc, origin, keep_full);
     if (!scores_ws) cudaFreeAsync(sc, s);
     if (!idx_ws) cudaFreeAsync(ix, s);
     return rc;
@@ -219,7 +227,8 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
     QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
     const int heads = p->per_head ? p->n_kv : 1;
     const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
-    if (p->rho == 1.0) return launch_gather(s, g, k, v, QVK_BF16, heads, width, nullptr, kc, vc, origin);
+    const int64_t keep_full = static_cast<int64_t>(retained(p->rho, static_cast<size_t>(g->max_tokens)));
+    if (p->rho == 1.0) return launch_gather(s, g, k, v, QVK_BF16, heads, width, nullptr, kc, vc, origin, keep_full);
     double* sc = scores_ws;
     uint32_t* ix = idx_ws;
     if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
@@ -236,7 +245,7 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
         rc = qvk_score(s, g, k, v, QVK_BF16, heads, width, p->scorer, nullptr, 0, p->n_kv, sc);
     }
     if (rc == QVK_OK) rc = launch_select(s, g, sc, heads, ix);
-    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin);
+    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, keep_full);
     if (!scores_ws) cudaFreeAsync(sc, s);
     if (!idx_ws) cudaFreeAsync(ix, s);
     return rc;

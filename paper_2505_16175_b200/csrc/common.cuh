@@ -35,6 +35,18 @@ __device__ __forceinline__ int find_group(const int64_t* __restrict__ off, int n
     return lo;
 }
 
+// Same, for the usual case of equal group sizes: guess g = t / stride (stride = the largest group's size) and verify
+// with two independent loads; fall back to the search for ragged plans.  32-bit division when t, stride fit.
+__device__ __forceinline__ int find_group_fast(const int64_t* __restrict__ off, int n_groups, int64_t t,
+                                               int64_t stride) {
+    if (stride > 0 && t < 0x7fffffff && stride < 0x7fffffff) {
+        uint32_t g = static_cast<uint32_t>(t) / static_cast<uint32_t>(stride);
+        if (g > static_cast<uint32_t>(n_groups - 1)) g = n_groups - 1;
+        if (__ldg(off + g) <= t && t < __ldg(off + g + 1)) return static_cast<int>(g);
+    }
+    return find_group(off, n_groups, t);
+}
+
 __device__ __forceinline__ uint64_t splitmix64_at(uint64_t state0, uint64_t i) {
     // Draw i (0-based) of splitmix64 seeded with state0 (synthetic.cpp:5-10): state advances by gamma per draw.
     uint64_t z = state0 + (i + 1) * 0x9e3779b97f4a7c15ull;

@@ -16,6 +16,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
                                                      const int64_t* __restrict__ row_off,
                                                      const uint64_t* __restrict__ first_token,
                                                      const uint32_t* __restrict__ idx, int64_t total_units,
+                                                     int64_t keep_stride,
                                                      uint8_t* __restrict__ kc, uint8_t* __restrict__ vc,
                                                      uint64_t* __restrict__ origin) {
     const int vec_per_unit = row_bytes / static_cast<int>(sizeof(V));
@@ -26,7 +27,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         const int part = static_cast<int>(w - cu * vec_per_unit);
         const int64_t row = cu / heads;
         const int h = static_cast<int>(cu - row * heads);
-        const int g = find_group(row_off, n_groups, row);
+        const int g = find_group_fast(row_off, n_groups, row, keep_stride);
         const int64_t r = row - __ldg(row_off + g);
         const int64_t src_tok = idx ? static_cast<int64_t>(__ldg(idx + cu)) : r;
         const int64_t src_unit = (__ldg(tok_off + g) + src_tok) * heads + h;
@@ -42,8 +43,11 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
 
 }  // namespace
 
+// keep_stride: cache rows of a full-size group when known (rho given), else 0 = derive / binary search.
 int launch_gather(cudaStream_t stream, const qvk_groups* g, const void* k, const void* v, int dtype, int heads,
-                  int width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin) {
+                  int width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin, int64_t keep_stride) {
+    if (keep_stride <= 0 && g->n_groups > 0 && g->total_rows % g->n_groups == 0)
+        keep_stride = g->total_rows / g->n_groups;  // equal groups
     const int elem = dtype == QVK_F32 ? 4 : 2;
     const int row_bytes = width * elem;
     const int64_t units = g->total_rows * heads;
@@ -59,7 +63,8 @@ int launch_gather(cudaStream_t stream, const qvk_groups* g, const void* k, const
     auto args = [&](auto* kern) {
         kern<<<blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v), row_bytes,
                                          heads, g->n_groups, g->tok_off_d, g->row_off_d, g->first_token_d, idx,
-                                         units, static_cast<uint8_t*>(kc), static_cast<uint8_t*>(vc), origin);
+                                         units, keep_stride, static_cast<uint8_t*>(kc), static_cast<uint8_t*>(vc),
+                                         origin);
     };
     if (vec == 16) args(gather_kernel<uint4>);
     else if (vec == 4) args(gather_kernel<uint32_t>);

@@ -6,7 +6,10 @@
 // near-tie band.  The rows a CTA owns are contiguous in HBM, so the CTA stages them through shared memory with
 // coalesced 16-byte loads in width chunks of 64 elements; each thread then reads its own padded smem row.
 // Algorithmic bytes per (token, head): width*sizeof(T) read + 8 written.
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace qvk {
 namespace {
@@ -132,6 +135,188 @@ __global__ void __launch_bounds__(kSeqThreads) score_norm_bf16_kernel(const __nv
     }
 }
 
+// TMA-fed variant for per-head rows of 64 or 128 bf16 (every GQA configuration): 128-row tiles (16 or 32 KB,
+// contiguous in HBM) stream into a 3-stage shared-memory ring through cp.async.bulk.tensor with the 128-byte
+// swizzle, so each thread reads ITS row's 16-byte chunks bank-conflict-free (chunk c of row r sits at
+// r*128 + ((c ^ (r & 7)) * 16)) while HBM sees fully coalesced bulk reads.  One producer warp, 4 consumer warps,
+// 2 CTAs per SM, persistent over tiles; the per-row double sum is the reference's sequential order (exact, see
+// score_norm_bf16_kernel).
+constexpr int kTmaStages = 3;
+constexpr int kTmaRows = 128;
+constexpr int kTmaConsumers = 4 * kTmaRows;  // four threads per row
+
+struct ScoreTmaShared {
+    uint64_t full[kTmaStages], empty[kTmaStages];
+};
+
+// Reference-order (prefill.cpp:207) sum of squares of row r of a swizzled smem tile of NB 64-column boxes.
+template <int NB>
+__device__ double seq_sumsq_smem(uint32_t row_s, int r) {
+    double acc = 0.0;
+    for (int b = 0; b < NB; ++b)
+        for (int c = 0; c < 8; ++c) {
+            uint32_t w[4];
+            ptx::lds128(w, row_s + b * kTmaRows * 128 + ((c ^ (r & 7)) << 4));
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t bits = (e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16);
+                const double d = static_cast<double>(__uint_as_float(bits));
+                acc = __fma_rn(d, d, acc);
+            }
+        }
+    return acc;
+}
+
+__device__ __forceinline__ void store_score(double* __restrict__ out, int64_t u, int heads, int g,
+                                            const int64_t* __restrict__ tok_off, double sumsq, int negate) {
+    const double norm = __dsqrt_rn(sumsq);
+    const double sc = negate ? -norm : norm;  // zero row -> -0.0 exactly like the reference
+    if (heads == 1) {
+        out[u] = sc;
+    } else {
+        const int64_t tok = static_cast<uint32_t>(u) / heads;  // units < 2^31 on this path
+        const int hh = static_cast<int>(u - tok * heads);
+        const int64_t t0 = __ldg(tok_off + g);
+        const int64_t n = __ldg(tok_off + g + 1) - t0;
+        out[heads * t0 + hh * n + (tok - t0)] = sc;
+    }
+}
+
+template <int NB>  // 64-element boxes per row (row width = 64 * NB)
+__global__ void __launch_bounds__(kTmaConsumers + 32) score_norm_tma_kernel(
+    const __grid_constant__ CUtensorMap tm, int64_t units, int heads, const int64_t* __restrict__ tok_off,
+    int n_groups, int64_t max_tokens, int negate, double* __restrict__ out) {
+    constexpr uint32_t kBox = kTmaRows * 128;        // bytes of one 64-column box
+    constexpr uint32_t kTile = NB * kBox;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    ScoreTmaShared* sh = reinterpret_cast<ScoreTmaShared*>(smem + kTmaStages * kTile);
+    const int warp = threadIdx.x >> 5;
+    const int64_t tiles = (units + kTmaRows - 1) / kTmaRows;
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kTmaStages; ++st) {
+            ptx::mbar_init(&sh->full[st], 1);
+            ptx::mbar_init(&sh->empty[st], kTmaConsumers);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kTmaConsumers / 32) {
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tm);
+            uint32_t k = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
+                const uint32_t st = k % kTmaStages;
+                ptx::mbar_wait(&sh->empty[st], ((k / kTmaStages) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&sh->full[st], kTile);
+#pragma unroll
+                for (int b = 0; b < NB; ++b)
+                    ptx::tma_load_2d(smem + st * kTile + b * kBox, &tm, &sh->full[st], 64 * b,
+                                     static_cast<int>(t * kTmaRows));
+            }
+        }
+        return;
+    }
+    // Four adjacent lanes share a row: lane quarter q reads the 16-byte chunks {2q, 2q+1} of every box (the
+    // 8 lanes of a shared-memory phase then hit 8 distinct bank groups under the swizzle).
+    const int r = threadIdx.x >> 2, q = threadIdx.x & 3;
+    uint32_t k = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
+        const uint32_t st = k % kTmaStages;
+        ptx::mbar_wait(&sh->full[st], (k / kTmaStages) & 1);
+        const uint8_t* row = smem + st * kTile + r * 128;
+        // Partial sums in any order and, per row, the min / max 15-bit magnitude over the nonzero elements
+        // (16x2 SIMD): if the row total S is below 2^(q_min + 53), q_min = 2 (E_min - 134) the exponent of a unit
+        // dividing every bf16 square, every partial sum of ANY order is exact, so the result equals the
+        // reference's sequential sum bit for bit.  Rows that fail the test (huge dynamic range, inf / nan) are
+        // recomputed sequentially.
+        double acc[2] = {0.0, 0.0};
+        uint32_t lo = 0xffffffffu, hi = 0u;  // min(|x| - 1) (zero wraps to max: ignored), max |x|, fp32 bits
+        const uint32_t row_s = ptx::smem_u32(row);
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                const int c = 2 * q + cc;
+                uint32_t w[4];
+                ptx::lds128(w, row_s + b * kBox + ((c ^ (r & 7)) << 4));
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t bits = (e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16);
+                    const uint32_t mag = bits & 0x7fffffffu;
+                    lo = min(lo, mag - 1u);
+                    hi = max(hi, mag);
+                    const double d = static_cast<double>(__uint_as_float(bits));
+                    acc[e & 1] = __fma_rn(d, d, acc[e & 1]);
+                }
+            }
+        double sum = __dadd_rn(acc[0], acc[1]);
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        // Exactness test: every bf16 square is a multiple of 2^q, q = 2 (E - 134) with E the bf16 exponent
+        // (E >= 1; (|x|-1) >> 23 underestimates it by at most one, which only makes the test conservative).
+        bool exact = hi < 0x7f800000u;  // no inf / nan
+        if (exact && hi != 0u) {
+            const int qmin = 2 * (static_cast<int>(lo >> 23) - 134);
+            const int es = static_cast<int>((__double_as_longlong(sum) >> 52) & 0x7ff) - 1023;
+            exact = es <= qmin + 52;
+        }
+        if (!exact && q == 0) sum = seq_sumsq_smem<NB>(row_s, r);  // rare: prefill.cpp:207's sequential order
+        ptx::mbar_arrive(&sh->empty[st]);
+        const int64_t u = t * kTmaRows + r;
+        if (q == 0 && u < units)
+            store_score(out, u, heads,
+                        heads == 1 ? 0 : find_group_fast(tok_off, n_groups, static_cast<uint32_t>(u) / heads, max_tokens),
+                        tok_off, sum, negate);
+    }
+}
+
+bool score_map(CUtensorMap* m, const void* base, int64_t units, int width) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(units)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(kTmaRows)};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NB>
+int launch_score_tma(cudaStream_t stream, const CUtensorMap& tm, int64_t units, int heads, const qvk_groups* g,
+                     int negate, double* scores) {
+    constexpr size_t smem = 1024 + kTmaStages * NB * kTmaRows * 128 + sizeof(ScoreTmaShared);
+    static bool attr = false;
+    if (!attr) {
+        QVK_CUDA_CHECK(cudaFuncSetAttribute(score_norm_tma_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem)));
+        attr = true;
+    }
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        QVK_CUDA_CHECK(cudaGetDevice(&dev));
+        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t tiles = (units + kTmaRows - 1) / kTmaRows;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, 2 * static_cast<int64_t>(sms)));
+    score_norm_tma_kernel<NB><<<grid, kTmaConsumers + 32, smem, stream>>>(tm, units, heads, g->tok_off_d,
+                                                                          g->n_groups, g->max_tokens, negate, scores);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
 // attention_score (prefill.cpp:213-230): s_i = (sum_t sum_j double(k_ij) * q_tj) / (T * n_h), t-outer, j-inner,
 // one running double — reproduced in the same order.  q rows are read by every thread at the same time (broadcast);
 // each thread walks its own key row (L1-resident across the t loop).
@@ -163,6 +348,11 @@ int launch_score(cudaStream_t stream, const qvk_groups* g, int64_t total_tokens,
         const unsigned blocks = static_cast<unsigned>((units + kScoreThreads - 1) / kScoreThreads);
         const int negate = scorer == QVK_KEY_NORM_SMALL;
         const bool fast = dtype == QVK_BF16 && width % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+        CUtensorMap tm;
+        if (fast && (width == 64 || width == 128) && units < (int64_t(1) << 31) && score_map(&tm, x, units, width)) {
+            return width == 64 ? launch_score_tma<1>(stream, tm, units, heads, g, negate, scores)
+                               : launch_score_tma<2>(stream, tm, units, heads, g, negate, scores);
+        }
         if (fast) {
             const unsigned grid = static_cast<unsigned>((units + kSeqThreads - 1) / kSeqThreads);
             const auto* xb = static_cast<const __nv_bfloat16*>(x);
