@@ -35,7 +35,8 @@ namespace {
 
 constexpr int kBM = 128;                      // query rows per tile
 constexpr int kBN = 128;                      // kv rows per tile
-constexpr int kStages = 4;                    // K/V ring depth
+constexpr int kStages = 3;                    // K/V ring depth
+constexpr int kQBufs = 2;                     // Q double buffer: the next unit's Q loads during the current one
 constexpr uint32_t kChunkBytes = kBM * 64 * 2; // one 128-row x 128-byte SW128 chunk (64 head-dim columns)
 // Head dim D in {64, 128}: a 128-row Q/K/V tile is D/64 chunks.
 template <int D>
@@ -79,8 +80,8 @@ struct AttnParams {
 };
 
 struct Barriers {
-    uint64_t q_full;
-    uint64_t q_empty;
+    uint64_t q_full[kQBufs];
+    uint64_t q_empty[kQBufs];
     uint64_t kv_full[kStages];
     uint64_t kv_empty[kStages];
     uint64_t s_full[2];
@@ -93,7 +94,7 @@ struct Barriers {
 };
 
 template <int D>
-constexpr size_t smem_bytes() { return 1024 /*align slack*/ + (2 + kStages) * tile_bytes<D>() + sizeof(Barriers); }
+constexpr size_t smem_bytes() { return (2 * kQBufs + kStages) * tile_bytes<D>() + sizeof(Barriers); }
 
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_addr, int kk) {
     // k-step kk (16 elements) of a K-major SW128 tile: chunk kk/4, +32 B per step inside the 128-byte row.
@@ -135,18 +136,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
     constexpr uint32_t kTileBytes = tile_bytes<D>();
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                       // Q0, Q1
-    uint8_t* sKV = smem + 2 * kTileBytes;     // ring
-    Barriers* bar = reinterpret_cast<Barriers*>(smem + (2 + kStages) * kTileBytes);
+    // 228 KB of tiles + barriers leave no room for alignment slack: the dynamic window must be 1024-aligned
+    // (SWIZZLE_128B atoms); checked below.
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sQ = smem;                                   // [Q buffer][tile 0 | tile 1]
+    uint8_t* sKV = smem + 2 * kQBufs * kTileBytes;        // ring
+    Barriers* bar = reinterpret_cast<Barriers*>(smem + (2 * kQBufs + kStages) * kTileBytes);
+    if (ptx::smem_u32(smem) & 1023) __trap();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int unit_iter = 0;  // per-role count of valid units processed (barrier phases; trace)
     if (threadIdx.x == 0) QVK_TRACE(1022);
 
     if (threadIdx.x == 0) {
-        ptx::mbar_init(&bar->q_full, 1);
-        ptx::mbar_init(&bar->q_empty, 1);
+        for (int b = 0; b < kQBufs; ++b) {
+            ptx::mbar_init(&bar->q_full[b], 1);
+            ptx::mbar_init(&bar->q_empty[b], 1);
+        }
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&bar->kv_full[s], 1);
             ptx::mbar_init(&bar->kv_empty[s], 1);
@@ -175,32 +180,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::prefetch_tmap(&tm_q);
             ptx::prefetch_tmap(&tm_k);
             ptx::prefetch_tmap(&tm_v);
-            uint32_t item = 0;
-            for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
-                const Unit w = decode_unit(p, u);
-                if (!w.valid) continue;
-                ptx::mbar_wait(&bar->q_empty, (unit_iter & 1) ^ 1);  // previous unit's S MMAs retired
-                ptx::mbar_arrive_expect_tx(&bar->q_full, w.n1 ? 2 * kTileBytes : kTileBytes);
+            // Q of unit i goes to buffer i & 1 and is issued early in unit i-1 (after its first K/V tiles, by
+            // which time unit i-2's S MMAs — the previous users of that buffer — have retired).
+            auto next_valid = [&](int u) -> int {
+                for (; u < p.total_units; u += gridDim.x)
+                    if (decode_unit(p, u).valid) return u;
+                return p.total_units;
+            };
+            auto load_q = [&](const Unit& w, int qi) {
+                const int qb = qi & 1;
+                uint8_t* q_dst = sQ + qb * 2 * kTileBytes;
+                ptx::mbar_wait(&bar->q_empty[qb], ((qi >> 1) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&bar->q_full[qb], w.n1 ? 2 * kTileBytes : kTileBytes);
                 const int r0 = static_cast<int>(w.tok0) + w.mt0 * kBM;
 #pragma unroll
                 for (int c = 0; c < D / 64; ++c) {
-                    ptx::tma_load_3d(sQ + c * kChunkBytes, &tm_q, &bar->q_full, 64 * c, w.hq, r0);
+                    ptx::tma_load_3d(q_dst + c * kChunkBytes, &tm_q, &bar->q_full[qb], 64 * c, w.hq, r0);
                     if (w.n1)
-                        ptx::tma_load_3d(sQ + kTileBytes + c * kChunkBytes, &tm_q, &bar->q_full, 64 * c, w.hq,
+                        ptx::tma_load_3d(q_dst + kTileBytes + c * kChunkBytes, &tm_q, &bar->q_full[qb], 64 * c, w.hq,
                                          r0 + kBM);
                 }
-                // Warm L2 with the CTA's next unit's Q (its load is issued only once this unit's S MMAs retire).
-                for (int un = u + static_cast<int>(gridDim.x); un < p.total_units; un += gridDim.x) {
-                    const Unit nx = decode_unit(p, un);
-                    if (!nx.valid) continue;
-                    const int nr0 = static_cast<int>(nx.tok0) + nx.mt0 * kBM;
-#pragma unroll
-                    for (int c = 0; c < D / 64; ++c) {
-                        ptx::tma_prefetch_3d(&tm_q, 64 * c, nx.hq, nr0);
-                        if (nx.n1) ptx::tma_prefetch_3d(&tm_q, 64 * c, nx.hq, nr0 + kBM);
-                    }
-                    break;
-                }
+            };
+            uint32_t item = 0;
+            int u = next_valid(blockIdx.x);
+            if (u < p.total_units) load_q(decode_unit(p, u), 0);
+            for (; u < p.total_units; ++unit_iter) {
+                const Unit w = decode_unit(p, u);
+                const int un = next_valid(u + gridDim.x);
+                const int q_at = min(2, 2 * w.nkv - 1);  // K/V item after which the next unit's Q is issued
                 for (int it = 0; it < 2 * w.nkv; ++it, ++item) {
                     const uint32_t st = item % kStages;
                     ptx::mbar_wait(&bar->kv_empty[st], ((item / kStages) & 1) ^ 1);
@@ -211,14 +218,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < D / 64; ++c)
                         ptx::tma_load_3d(dst + c * kChunkBytes, map, &bar->kv_full[st], 64 * c, w.hk, row);
+                    if (it == q_at && un < p.total_units) load_q(decode_unit(p, un), unit_iter + 1);
                 }
-                ++unit_iter;
+                u = un;
             }
         } else if (warp == kMmaWarp && ptx::elect_one()) {
             // ===================== MMA issuer =====================
             constexpr uint32_t kIdS = ptx::idesc_bf16_f32(kBM, kBN, false, false);
             constexpr uint32_t kIdPV = ptx::idesc_bf16_f32(kBM, D, false, true);
-            const uint32_t q_addr = ptx::smem_u32(sQ);
+            const uint32_t q_base = ptx::smem_u32(sQ);
             const uint32_t ring = ptx::smem_u32(sKV);
             uint32_t item = 0;
             uint32_t pv_step[2] = {0, 0};  // P publications consumed per tile (p_full phases)
@@ -227,7 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const Unit w = decode_unit(p, u);
                 if (!w.valid) continue;
                 const int nt[2] = {w.n0, w.n1};
-                ptx::mbar_wait(&bar->q_full, unit_iter & 1);
+                const int qb = unit_iter & 1;
+                const uint32_t q_addr = q_base + qb * 2 * kTileBytes;
+                ptx::mbar_wait(&bar->q_full[qb], (unit_iter >> 1) & 1);
                 ptx::tc_fence_after();
                 // S_t(j) into TMEM columns [128 t, 128 t + 128)
                 auto issue_s = [&](int t, uint32_t k_addr) {
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     issue_s(1, k0);
                     ptx::mma_commit(&bar->s_full[1]);
                 }
-                if (w.nkv == 1) ptx::mma_commit(&bar->q_empty);  // every S of the unit issued
+                if (w.nkv == 1) ptx::mma_commit(&bar->q_empty[qb]);  // every S of the unit issued
                 ptx::mma_commit(&bar->kv_empty[item % kStages]);
                 for (int j = 0; j < w.nkv; ++j) {
                     const uint32_t v_item = item + 2 * j + 1;
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mma_commit(&bar->s_full[1]);
                         QVK_TRACE(j * 8 + 6);
                     }
-                    if (j + 2 == w.nkv) ptx::mma_commit(&bar->q_empty);  // the unit's last S was just issued
+                    if (j + 2 == w.nkv) ptx::mma_commit(&bar->q_empty[qb]);  // the unit's last S was just issued
                     if (more) ptx::mma_commit(&bar->kv_empty[(v_item + 1) % kStages]);
                 }
                 item += 2 * w.nkv;
