@@ -269,17 +269,14 @@ def main():
         out_k = torch.empty(buf.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
         out_v = torch.empty_like(out_k).pin_memory()
         out_o = torch.empty(buf.origin.numel(), dtype=torch.int64).pin_memory()
+        # public host-buffer API: group-chunked, copies overlapped with the kernels (paper_2505_16175_b200/pipeline.py)
+        hp = qp.HostPrefill(local_plan, n_q, n_kv, d, rho, dev, chunks=4, cache_rows=plan.total_rows,
+                            row_base=row_base)
+        gather = (lambda: allgather_cache([hp.k_cache, hp.v_cache, hp.origin], bounds, [unit, unit, n_kv])) \
+            if world > 1 else None
 
         def e2e_step():
-            q.copy_(hq, non_blocking=True)
-            k.copy_(hk, non_blocking=True)
-            v.copy_(hv, non_blocking=True)
-            qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, buffers=buf, cache_row_offset=row_base)
-            if world > 1:
-                allgather_cache([buf.k_cache, buf.v_cache, buf.origin], bounds, [unit, unit, n_kv])
-            out_k.copy_(buf.k_cache, non_blocking=True)
-            out_v.copy_(buf.v_cache, non_blocking=True)
-            out_o.copy_(buf.origin, non_blocking=True)
+            hp.run(hq, hk, hv, out_k, out_v, out_o, after_compute=gather)
 
         for _ in range(max(1, args.warmup)):
             e2e_step()
@@ -299,7 +296,8 @@ def main():
         d2h = sum(x.numel() * x.element_size() for x in (out_k, out_v, out_o))
         e2e = {"value": total_tokens * args.steps / (t.item() / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "qvk_prefill_layer (C ABI) with pinned host Q/K/V in, pruned cache out"}
+               "path": "HostPrefill: qvk_prefill_layer (C ABI) per 4-group chunk, pinned host Q/K/V in and pruned "
+                       "cache out on two copy streams overlapped with the kernels"}
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
     fl = flops_attention(sizes, n_q, d)

@@ -28,4 +28,6 @@ from .prefill import (  # noqa: F401
     top_k_indices,
 )
 
+from .pipeline import HostPrefill  # noqa: F401,E402
+
 __all__ = [n for n in dir() if not n.startswith("_")]

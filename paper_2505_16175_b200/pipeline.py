@@ -1,0 +1,108 @@
+"""Host-buffer prefill: group-chunked pipelining of the host<->device copies with the kernels.
+
+The north-star path consumes Q/K/V that a user may hold in (pinned) host memory.  `HostPrefill.run` streams them in
+contiguous chunks of groups: the H2D copy of chunk c+1 (copy stream) and the D2H copy of chunk c-1's pruned cache
+(a second copy stream) overlap the kernels of chunk c (the caller's stream), so a step costs about
+max(copies, kernels) instead of their sum.  Groups are independent and every chunk writes its pruned
+rows at their static global cache offsets (prefill.cpp:235-238), so chunking changes nothing in the result.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check, lib
+from .prefill import GroupPlan, Scorer
+
+
+class HostPrefill:
+    def __init__(self, plan: GroupPlan, n_q: int, n_kv: int, d_h: int, rho: float, device,
+                 scorer: Scorer = Scorer.key_norm_small, chunks: int = 4, cache_rows: int | None = None,
+                 row_base: int = 0):
+        self.plan, self.n_q, self.n_kv, self.d, self.rho = plan, n_q, n_kv, d_h, rho
+        self.dev = torch.device(device)
+        G = plan.n_groups
+        chunks = max(1, min(chunks, G))
+        bounds = np.linspace(0, G, chunks + 1).round().astype(int)
+        self.parts = []
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            if b <= a:
+                continue
+            t0, r0 = int(plan.tok_off[a]), int(plan.row_off[a])
+            sub = GroupPlan((plan.tok_off[a:b + 1] - t0).astype(np.int64), plan.keep[a:b].copy(),
+                            (plan.row_off[a:b + 1] - r0).astype(np.int64), plan.first_token[a:b].copy())
+            self.parts.append((t0, int(plan.tok_off[b]), r0, int(plan.row_off[b]), sub.to(self.dev)))
+        T, R = plan.total_tokens, plan.total_rows
+        bf = torch.bfloat16
+        self.q = torch.empty(T, n_q, d_h, dtype=bf, device=self.dev)
+        self.k = torch.empty(T, n_kv, d_h, dtype=bf, device=self.dev)
+        self.v = torch.empty(T, n_kv, d_h, dtype=bf, device=self.dev)
+        self.o = torch.empty(T, n_q, d_h, dtype=bf, device=self.dev)
+        self.scores = torch.empty(max(1, T * n_kv), dtype=torch.float64, device=self.dev)
+        self.idx = torch.empty(max(1, R * n_kv), dtype=torch.int32, device=self.dev)
+        rows = R if cache_rows is None else cache_rows
+        self.k_cache = torch.empty(rows * n_kv * d_h, dtype=bf, device=self.dev)
+        self.v_cache = torch.empty_like(self.k_cache)
+        self.origin = torch.empty(rows * n_kv, dtype=torch.int64, device=self.dev)
+        self.row_base = row_base
+        self.prm = L.QvkLayerParams(n_q, n_kv, d_h, int(scorer), 1, rho, 1.0 / math.sqrt(d_h), 32, 1)
+        self.h2d = torch.cuda.Stream(self.dev)
+        self.d2h = torch.cuda.Stream(self.dev)
+
+    def _layer(self, part, stream):
+        t0, t1, r0, r1, g = part
+        unit = self.n_kv * self.d
+        cr = self.row_base + r0
+        check(lib.qvk_prefill_layer(stream.cuda_stream, g.ref, C.byref(self.prm), self.q[t0:t1].data_ptr(),
+                                    self.k[t0:t1].data_ptr(), self.v[t0:t1].data_ptr(), self.o[t0:t1].data_ptr(),
+                                    self.scores[t0 * self.n_kv:].data_ptr(), self.idx[r0 * self.n_kv:].data_ptr(),
+                                    self.k_cache[cr * unit:].data_ptr(), self.v_cache[cr * unit:].data_ptr(),
+                                    self.origin[cr * self.n_kv:].data_ptr()))
+
+    def run(self, hq, hk, hv, out_k=None, out_v=None, out_o=None, after_compute=None):
+        """One pruned-prefill layer from host Q/K/V (pinned, (T, heads, d) bf16) into the device cache; optional
+        pinned host outputs receive this rank's pruned rows (or the whole cache when `after_compute` — e.g. the
+        multi-GPU all-gather — runs between the kernels and the readback)."""
+        main = torch.cuda.current_stream(self.dev)
+        start = torch.cuda.Event()
+        start.record(main)
+        self.h2d.wait_event(start)
+        self.d2h.wait_event(start)
+        unit = self.n_kv * self.d
+        per_chunk_out = out_k is not None and after_compute is None
+        for part in self.parts:
+            t0, t1, r0, r1, _ = part
+            e_in = torch.cuda.Event()
+            with torch.cuda.stream(self.h2d):
+                self.q[t0:t1].copy_(hq[t0:t1], non_blocking=True)
+                self.k[t0:t1].copy_(hk[t0:t1], non_blocking=True)
+                self.v[t0:t1].copy_(hv[t0:t1], non_blocking=True)
+                e_in.record(self.h2d)
+            main.wait_event(e_in)
+            self._layer(part, main)
+            if per_chunk_out:
+                e_out = torch.cuda.Event()
+                e_out.record(main)
+                self.d2h.wait_event(e_out)
+                a, b = self.row_base + r0, self.row_base + r1
+                with torch.cuda.stream(self.d2h):
+                    out_k[a * unit:b * unit].copy_(self.k_cache[a * unit:b * unit], non_blocking=True)
+                    out_v[a * unit:b * unit].copy_(self.v_cache[a * unit:b * unit], non_blocking=True)
+                    out_o[a * self.n_kv:b * self.n_kv].copy_(self.origin[a * self.n_kv:b * self.n_kv],
+                                                             non_blocking=True)
+        if after_compute is not None:
+            after_compute()
+            if out_k is not None:
+                out_k.copy_(self.k_cache, non_blocking=True)
+                out_v.copy_(self.v_cache, non_blocking=True)
+                out_o.copy_(self.origin, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self.d2h)
+        main.wait_event(done)
+        done_h2d = torch.cuda.Event()
+        done_h2d.record(self.h2d)
+        main.wait_event(done_h2d)

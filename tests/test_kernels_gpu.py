@@ -337,3 +337,25 @@ def test_prefill_layer(cuda, scorer, per_head):
     kc, vc, origin = qp.gather(k, v, g, heads, width, idx)
     assert torch.equal(buf.idx[: idx.numel()], idx)
     assert torch.equal(buf.k_cache, kc) and torch.equal(buf.v_cache, vc) and torch.equal(buf.origin, origin)
+
+
+def test_host_prefill_pipeline_matches_device_layer(cuda):
+    """Chunked host-buffer pipeline (copies overlapped with kernels) == one device-resident prefill_layer call."""
+    sizes, n_q, n_kv, rho = [1024, 1024, 1024, 777, 1024], 28, 4, 0.5
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, 128, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, 128, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, 128, 2, False, cuda)
+    buf = qp.prefill_layer(q, k, v, g, n_q, n_kv, rho)
+    hp = qp.HostPrefill(plan, n_q, n_kv, 128, rho, cuda, chunks=3)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    out_k = torch.empty(hp.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+    out_v = torch.empty_like(out_k).pin_memory()
+    out_o = torch.empty(hp.origin.numel(), dtype=torch.int64).pin_memory()
+    for _ in range(2):
+        hp.run(hq, hk, hv, out_k, out_v, out_o)
+    torch.cuda.synchronize()
+    assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
+    assert torch.equal(out_o, buf.origin.cpu())
+    assert torch.equal(hp.o, buf.o)
