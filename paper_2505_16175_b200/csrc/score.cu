@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32) score_norm_tma_kernel(
         // reference's sequential sum bit for bit.  Rows that fail the test (huge dynamic range, inf / nan) are
         // recomputed sequentially.
         double acc[2] = {0.0, 0.0};
-        uint32_t lo = 0xffffffffu, hi = 0u;  // min(|x| - 1) (zero wraps to max: ignored), max |x|, fp32 bits
+        uint32_t lo = 0xffffffffu;  // min(|x| - 1) over the row (zero wraps to the max: ignored), fp32 bits
         const uint32_t row_s = ptx::smem_u32(row);
 #pragma unroll
         for (int b = 0; b < NB; ++b)
@@ -242,9 +242,7 @@ __global__ void __launch_bounds__(kTmaConsumers + 32) score_norm_tma_kernel(
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const uint32_t bits = (e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16);
-                    const uint32_t mag = bits & 0x7fffffffu;
-                    lo = min(lo, mag - 1u);
-                    hi = max(hi, mag);
+                    lo = min(lo, (bits & 0x7fffffffu) - 1u);
                     const double d = static_cast<double>(__uint_as_float(bits));
                     acc[e & 1] = __fma_rn(d, d, acc[e & 1]);
                 }
@@ -254,12 +252,13 @@ __global__ void __launch_bounds__(kTmaConsumers + 32) score_norm_tma_kernel(
         for (int o = 1; o < 4; o <<= 1) {
             sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
             lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
         }
         // Exactness test: every bf16 square is a multiple of 2^q, q = 2 (E - 134) with E the bf16 exponent
         // (E >= 1; (|x|-1) >> 23 underestimates it by at most one, which only makes the test conservative).
-        bool exact = hi < 0x7f800000u;  // no inf / nan
-        if (exact && hi != 0u) {
+        // inf / nan elements make the sum non-finite: recomputed sequentially too (payload and sign included).
+        const uint64_t sum_bits = static_cast<uint64_t>(__double_as_longlong(sum));
+        bool exact = ((sum_bits >> 52) & 0x7ff) != 0x7ff;
+        if (exact && lo != 0xffffffffu) {
             const int qmin = 2 * (static_cast<int>(lo >> 23) - 134);
             const int es = static_cast<int>((__double_as_longlong(sum) >> 52) & 0x7ff) - 1023;
             exact = es <= qmin + 52;
