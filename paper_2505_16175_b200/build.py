@@ -29,7 +29,7 @@ REF_INCLUDE = Path(os.environ.get("QV_REF_INCLUDE", "/root/reference/proj/includ
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-                     f"-I{INCLUDE}", f"-I{CSRC}", "-ccbin", "g++"]
+                     f"-I{INCLUDE}", f"-I{CSRC}", "-ccbin", "g++"] + os.environ.get("QVK_EXTRA_NVFLAGS", "").split()
 CXX = "g++"  # /usr/bin/g++ (the image's CXX variable points at a toolchain without libgomp)
 
 

@@ -73,7 +73,7 @@ struct AttnParams {
     int n_groups;
     int n_q;
     int n_kv;
-    int pairs_max;
+    int tiles_max;
     int total_units;
     float scale_log2;
     __nv_bfloat16* o;
@@ -89,8 +89,10 @@ struct Barriers {
     uint64_t o_done[2];     // last PV of the tile retired (MMA commit)
     uint64_t o_free[2];     // epilogue has O_t in registers: TMEM columns reusable (128 arrivals)
     uint64_t l_full[2];     // softmax published the row sums of the tile (128 arrivals)
+    uint64_t l_free[2];     // epilogue has read them (128 arrivals).  Keeps the softmax at most one unit ahead of
+                            // the epilogue: with 1-step units nothing else does, and l_full's phase parity would alias
     uint32_t tmem_base;
-    float row_sum[2][2][kBM];  // [unit parity][tile][row]
+    float row_sum[2][kBM];  // [tile][row]
 };
 
 template <int D>
@@ -105,29 +107,59 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t tile_addr, int kk) {
     return ptx::umma_desc_sw128(tile_addr + kk * 16 * 128, kChunkBytes, 1024);
 }
 
-// Work unit u (heaviest first: query-tile pairs from the last one down, then group, then q head fastest so the
-// CTAs that run concurrently share K/V tiles through L2).
+// Work units, heaviest first.  A unit is two 128-row query tiles that share one K/V stream of a KV head:
+//   * head pair: the same query tile t of two query heads of the KV head (both need K/V tiles 0..t, so the
+//     ping-pong never runs a step with one tile only);
+//   * tile pair: tiles 2p, 2p+1 of one head (the odd head left over when n_q/n_kv is odd; tile 2p+1 needs one extra
+//     step).
+// Units are ordered by length L (= K/V steps) descending; within a length band the KV head's slots vary fastest, so
+// CTAs running concurrently share K/V tiles through L2.
 struct Unit {
-    int g, hq, hk, mt0, mt1, n, n0, n1, nkv;
+    int g, hk, hq0, hq1, mt0, mt1, n, n0, n1, nkv;
     int64_t tok0;
     bool valid;
 };
+__host__ __device__ __forceinline__ int unit_lmax(int gq, int tiles) {
+    return (gq & 1) ? ((tiles + 1) & ~1) : tiles;
+}
+__host__ __device__ __forceinline__ int unit_slots(int gq, int tiles, int L) {
+    return (L <= tiles ? gq >> 1 : 0) + (((gq & 1) && !(L & 1)) ? 1 : 0);
+}
 __device__ __forceinline__ Unit decode_unit(const AttnParams& p, int u) {
     Unit w;
-    const int per_pair = p.n_groups * p.n_q;
-    const int pair = p.pairs_max - 1 - u / per_pair;
-    const int rem = u % per_pair;
-    w.g = rem / p.n_q;
-    w.hq = rem - w.g * p.n_q;
-    w.hk = w.hq / (p.n_q / p.n_kv);
-    w.tok0 = __ldg(p.tok_off + w.g);
-    w.n = static_cast<int>(__ldg(p.tok_off + w.g + 1) - w.tok0);
-    w.mt0 = 2 * pair;
-    w.mt1 = 2 * pair + 1;
-    w.valid = w.mt0 * kBM < w.n;
-    w.n0 = w.mt0 + 1;                           // K/V tiles of query tile 0 (last one is diagonal)
-    w.n1 = w.mt1 * kBM < w.n ? w.mt1 + 1 : 0;   // K/V tiles of query tile 1 (0: tile absent)
-    w.nkv = w.n1 ? w.n1 : w.n0;
+    w.valid = false;
+    const int gq = p.n_q / p.n_kv, hp = gq >> 1;
+    const int gk_count = p.n_groups * p.n_kv;
+    int rem = u;
+    for (int L = unit_lmax(gq, p.tiles_max); L >= 1; --L) {
+        const int S = unit_slots(gq, p.tiles_max, L);
+        if (S == 0) continue;
+        const int band = gk_count * S;
+        if (rem >= band) {
+            rem -= band;
+            continue;
+        }
+        const int gk = rem / S, slot = rem - gk * S;
+        w.g = gk / p.n_kv;
+        w.hk = gk - w.g * p.n_kv;
+        const int hp_here = L <= p.tiles_max ? hp : 0;
+        if (slot < hp_here) {
+            w.hq0 = w.hk * gq + 2 * slot;
+            w.hq1 = w.hq0 + 1;
+            w.mt0 = w.mt1 = L - 1;
+        } else {
+            w.hq0 = w.hq1 = w.hk * gq + gq - 1;
+            w.mt0 = L - 2;
+            w.mt1 = L - 1;
+        }
+        w.tok0 = __ldg(p.tok_off + w.g);
+        w.n = static_cast<int>(__ldg(p.tok_off + w.g + 1) - w.tok0);
+        w.valid = w.mt0 * kBM < w.n;
+        w.n0 = w.mt0 + 1;                           // K/V tiles of query tile 0 (last one is diagonal)
+        w.n1 = w.mt1 * kBM < w.n ? w.mt1 + 1 : 0;   // K/V tiles of query tile 1 (0: tile absent)
+        w.nkv = w.n1 > w.n0 ? w.n1 : w.n0;
+        break;
+    }
     return w;
 }
 
@@ -163,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&bar->o_done[t], 1);
             ptx::mbar_init(&bar->o_free[t], 128);
             ptx::mbar_init(&bar->l_full[t], 128);
+            ptx::mbar_init(&bar->l_free[t], 128);
         }
         ptx::fence_mbar_init();
     }
@@ -193,12 +226,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(&bar->q_empty[qb], ((qi >> 1) & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(&bar->q_full[qb], w.n1 ? 2 * kTileBytes : kTileBytes);
                 const int r0 = static_cast<int>(w.tok0) + w.mt0 * kBM;
+                const int r1 = static_cast<int>(w.tok0) + w.mt1 * kBM;
 #pragma unroll
                 for (int c = 0; c < D / 64; ++c) {
-                    ptx::tma_load_3d(q_dst + c * kChunkBytes, &tm_q, &bar->q_full[qb], 64 * c, w.hq, r0);
+                    ptx::tma_load_3d(q_dst + c * kChunkBytes, &tm_q, &bar->q_full[qb], 64 * c, w.hq0, r0);
                     if (w.n1)
-                        ptx::tma_load_3d(q_dst + kTileBytes + c * kChunkBytes, &tm_q, &bar->q_full[qb], 64 * c, w.hq,
-                                         r0 + kBM);
+                        ptx::tma_load_3d(q_dst + kTileBytes + c * kChunkBytes, &tm_q, &bar->q_full[qb], 64 * c, w.hq1,
+                                         r1);
                 }
             };
             uint32_t item = 0;
@@ -321,12 +355,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (t == 1 && !w.n1) continue;
                 const uint32_t ph = t_units[t] & 1;
                 ptx::mbar_wait(&bar->l_full[t], ph);
-                const float inv = 1.f / bar->row_sum[ph][t][row];
+                const float inv = 1.f / bar->row_sum[t][row];
+                ptx::mbar_arrive(&bar->l_free[t]);
                 ptx::mbar_wait(&bar->o_done[t], ph);
                 ptx::tc_fence_after();
                 const uint32_t o_col = tmem + lane_off + 256 + t * 128;
                 const int qrow = (t ? w.mt1 : w.mt0) * kBM + row;
-                __nv_bfloat16* dst = p.o + ((w.tok0 + qrow) * p.n_q + w.hq) * static_cast<int64_t>(D);
+                __nv_bfloat16* dst = p.o + ((w.tok0 + qrow) * p.n_q + (t ? w.hq1 : w.hq0)) * static_cast<int64_t>(D);
 #pragma unroll
                 for (int c = 0; c < D / 16; ++c) {
                     uint32_t o[16];
@@ -454,7 +489,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::f2_split(acc1, s2, s3);
                 l += (s0 + s1) + (s2 + s3);
             }
-            bar->row_sum[units & 1][t][row] = l;
+            if (units) ptx::mbar_wait(&bar->l_free[t], (units - 1) & 1);  // previous unit's sums consumed
+            bar->row_sum[t][row] = l;
             ptx::mbar_arrive(&bar->l_full[t]);
             ++units;
             ++unit_iter;
@@ -535,10 +571,14 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     prm.n_q = n_q;
     prm.n_kv = n_kv;
     const int64_t tiles = (g->max_tokens + kBM - 1) / kBM;
-    prm.pairs_max = static_cast<int>((tiles + 1) / 2);
+    if (tiles > 0x3fffffff) QVK_INVALID("attention: group too long");
+    prm.tiles_max = static_cast<int>(tiles);
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.o = static_cast<__nv_bfloat16*>(o);
-    const int64_t units = static_cast<int64_t>(prm.pairs_max) * g->n_groups * n_q;
+    const int gq = n_q / n_kv;
+    int64_t units = 0;
+    for (int L = unit_lmax(gq, prm.tiles_max); L >= 1; --L)
+        units += static_cast<int64_t>(g->n_groups) * n_kv * unit_slots(gq, prm.tiles_max, L);
     if (units > 0x7fffffff) QVK_INVALID("attention: too many work units");
     prm.total_units = static_cast<int>(units);
     static int sms = 0;

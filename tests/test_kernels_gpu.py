@@ -258,6 +258,22 @@ def test_attention_vs_torch_fp32(cuda, sizes, n_q, n_kv, d):
     check_tol(o, want, f"attention {sizes} d={d}")
 
 
+def test_attention_one_step_units_no_deadlock(cuda):
+    """C3 shape (1024-token groups): thousands of 1-step head-pair units per launch.  The softmax warps must not run
+    two units ahead of the epilogue (mbarrier phase aliasing deadlocked this shape once)."""
+    sizes, n_q, n_kv = [1024] * 40, 28, 4
+    plan = qp.GroupPlan.from_sizes(sizes, 0.25)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, 128, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, 128, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, 128, 2, False, cuda)
+    for _ in range(3):
+        o = qp.attention(q, k, v, g, n_q, n_kv)
+    torch.cuda.synchronize()
+    check_tol(o[:4096], torch_attention(q[:4096], k[:4096], v[:4096], sizes[:4], n_q, n_kv, 1 / math.sqrt(128)),
+              "1-step units")
+
+
 def test_attention_persistent_many_units(cuda):
     """More work units than SMs with ragged groups: every CTA runs several units back to back (TMEM / barrier
     phases carried across units), including units whose second query tile is absent."""
