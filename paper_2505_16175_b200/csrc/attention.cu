@@ -151,6 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int unit_iter = 0;  // per-role count of valid units processed (barrier phases; trace)
     if (threadIdx.x == 0) QVK_TRACE(1022);
+    // PDL: a dependent launched with programmatic stream serialization (the fused prune of qvk_prefill_layer, which
+    // does not read O) may be scheduled now; its CTAs take the SMs this persistent grid releases in its tail.
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < kQBufs; ++b) {

@@ -26,6 +26,9 @@ int launch_project_exact(cudaStream_t, const float*, int64_t, int, const float*,
 int launch_tokenize(cudaStream_t, const uint8_t*, int64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
                     const float*, int, float*);
 int launch_synth_bf16(cudaStream_t, uint64_t, uint32_t, uint32_t, uint64_t, int64_t, int, int, int, void*);
+bool prune_fused_supported(const qvk_groups*, int, int, const void*, const void*, const void*, const void*);
+int launch_prune_fused(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const double*,
+                       double*, uint32_t*, void*, void*, uint64_t*, int);
 
 namespace {
 
@@ -198,6 +201,12 @@ int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v,
     const int64_t keep_full = static_cast<int64_t>(retained(rho, static_cast<size_t>(g->max_tokens)));
     if (rho == 1.0)  // prefill.cpp:263-270: identity, no scoring, no shape check
         return gather_checked(s, g, k, v, dtype, heads, width, nullptr, kc, vc, origin, keep_full);
+    if ((scorer == QVK_KEY_NORM_SMALL || scorer == QVK_VALUE_NORM) && heads > 0 && width > 0 &&
+        prune_fused_supported(g, dtype, width, k, v, kc, vc)) {
+        if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
+        // score -> select -> gather in one cluster launch (prune_fused.cu); workspaces receive scores / idx
+        return launch_prune_fused(s, g, k, v, heads, width, scorer, nullptr, scores_ws, idx_ws, kc, vc, origin, 0);
+    }
     double* sc = scores_ws;
     uint32_t* ix = idx_ws;
     if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
@@ -229,6 +238,11 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
     const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
     const int64_t keep_full = static_cast<int64_t>(retained(p->rho, static_cast<size_t>(g->max_tokens)));
     if (p->rho == 1.0) return launch_gather(s, g, k, v, QVK_BF16, heads, width, nullptr, kc, vc, origin, keep_full);
+    const bool fused = prune_fused_supported(g, QVK_BF16, width, k, v, kc, vc);
+    if (fused && (p->scorer == QVK_KEY_NORM_SMALL || p->scorer == QVK_VALUE_NORM))
+        // overlap_prev = 1: the prune only reads K / V, so its CTAs may take the SMs the attention grid releases
+        return launch_prune_fused(s, g, k, v, heads, width, p->scorer, nullptr, scores_ws, idx_ws, kc, vc, origin,
+                                  1);
     double* sc = scores_ws;
     uint32_t* ix = idx_ws;
     if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
@@ -244,8 +258,12 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
     } else {
         rc = qvk_score(s, g, k, v, QVK_BF16, heads, width, p->scorer, nullptr, 0, p->n_kv, sc);
     }
-    if (rc == QVK_OK) rc = launch_select(s, g, sc, heads, ix);
-    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, keep_full);
+    if (rc == QVK_OK && fused && p->scorer == QVK_SNAPKV)  // select + gather fused, scores from snapkv.cu
+        rc = launch_prune_fused(s, g, k, v, heads, width, p->scorer, sc, nullptr, idx_ws, kc, vc, origin, 0);
+    else if (rc == QVK_OK) {
+        rc = launch_select(s, g, sc, heads, ix);
+        if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, keep_full);
+    }
     if (!scores_ws) cudaFreeAsync(sc, s);
     if (!idx_ws) cudaFreeAsync(ix, s);
     return rc;

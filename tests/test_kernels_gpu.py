@@ -375,3 +375,68 @@ def test_host_prefill_pipeline_matches_device_layer(cuda):
     assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
     assert torch.equal(out_o, buf.origin.cpu())
     assert torch.equal(hp.o, buf.o)
+
+
+# ------------------------------------------------------------------------------------------------ fused prune
+def _separate_prune(k, v, g, heads, width, scorer):
+    """score -> select -> gather as three launches (score.cu, select.cu, gather.cu): the fused kernel's check."""
+    sc = qp.score(k, v, g, heads, width, scorer)
+    idx = qp.select(sc, g, heads)
+    kc, vc, origin = qp.gather(k, v, g, heads, width, idx)
+    return sc, idx, kc, vc, origin
+
+
+def _tie_rows(sizes, heads, width, device, seed):
+    """Integer-valued bf16 rows from {-1, 0, 1}: norms collide massively (exact ties straddle every k boundary);
+    some rows all-zero (score -0.0 == +0.0)."""
+    gen = torch.Generator().manual_seed(seed)
+    x = torch.randint(-1, 2, (sum(sizes), heads, width), generator=gen).float()
+    x[::7] = 0.0
+    return x.to(torch.bfloat16).to(device)
+
+
+@pytest.mark.parametrize("sizes,heads,width,rho,kind", [
+    ([4096] * 3, 4, 128, 0.5, "synth"),
+    ([4096, 100, 1, 777, 3, 16384, 2], 4, 128, 0.25, "synth"),
+    ([256] * 4, 2, 64, 0.5, "synth"),
+    ([300, 5, 1000], 1, 512, 0.5, "synth"),
+    ([1000, 999, 8], 2, 256, 0.125, "synth"),
+    ([2048, 513, 64], 4, 128, 0.5, "ties"),
+    ([777, 31], 1, 512, 0.25, "ties"),
+    ([1500, 40000], 2, 64, 0.3, "synth"),
+])
+def test_prune_fused_matches_separate_kernels(cuda, sizes, heads, width, rho, kind):
+    """qvk_prune's one-launch cluster kernel (prune_fused.cu) == the three separate kernels, bit for bit: scores,
+    retained indices, cache rows, origins — ragged groups, 1-token groups (k == N), massive exact ties."""
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    if kind == "ties":
+        k, v = _tie_rows(sizes, heads, width, cuda, 1), _tie_rows(sizes, heads, width, cuda, 2)
+    else:
+        k = synth_groups(sizes, heads, width, 1, True, cuda)
+        v = synth_groups(sizes, heads, width, 2, False, cuda)
+    for scorer in (qp.Scorer.key_norm_small, qp.Scorer.value_norm):
+        kc, vc, origin, idx = qp.prune(k, v, g, heads, width, scorer, rho)
+        sc, idx2, kc2, vc2, origin2 = _separate_prune(k, v, g, heads, width, scorer)
+        torch.cuda.synchronize()
+        R = plan.total_rows * heads
+        assert torch.equal(idx[:R], idx2[:R]), scorer
+        assert torch.equal(kc, kc2) and torch.equal(vc, vc2) and torch.equal(origin, origin2), scorer
+
+
+def test_prune_fused_extreme_values(cuda):
+    """Arbitrary finite bf16 bit patterns (subnormals, +-huge, mixed scales): the fused kernel's order-free sums
+    take the sequential fallback where needed and still match the separate kernels bit for bit."""
+    sizes, heads, width = [2000, 333], 4, 128
+    gen = torch.Generator().manual_seed(7)
+    bits = torch.randint(0, 0x7f80, (sum(sizes), heads, width), generator=gen, dtype=torch.int32)
+    sign = torch.randint(0, 2, bits.shape, generator=gen, dtype=torch.int32) << 15
+    k = (bits | sign).to(torch.int16).view(torch.bfloat16).to(cuda)
+    v = synth_groups(sizes, heads, width, 2, False, cuda)
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    kc, vc, origin, idx = qp.prune(k, v, g, heads, width, qp.Scorer.key_norm_small, 0.5)
+    sc, idx2, kc2, vc2, origin2 = _separate_prune(k, v, g, heads, width, qp.Scorer.key_norm_small)
+    R = plan.total_rows * heads
+    assert torch.equal(idx[:R], idx2[:R])
+    assert torch.equal(kc, kc2) and torch.equal(origin, origin2)
