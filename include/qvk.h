@@ -120,6 +120,13 @@ int qvk_prune(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, co
               int64_t text_count, int32_t n_h, double* scores_ws_d, uint32_t* idx_ws_d, void* k_cache_d,
               void* v_cache_d, uint64_t* origin_d);
 
+/* select -> gather from precomputed scores (any scorer, e.g. qvk_snapkv_score's), one cluster launch per batch
+ * (prune_fused.cu): bf16 rows of 64/128/256/512 elements, groups of at most 65536 tokens; other shapes run the
+ * separate qvk_select + qvk_gather kernels.  Same outputs as qvk_select followed by qvk_gather; idx_d may be NULL. */
+int qvk_select_gather(qvk_stream_t stream, const qvk_groups* groups, const double* scores_d, const void* k_d,
+                      const void* v_d, int dtype, int32_t heads, int32_t width, uint32_t* idx_d, void* k_cache_d,
+                      void* v_cache_d, uint64_t* origin_d);
+
 /* ---- (a4) per-group causal GQA attention ------------------------------------------------------------------------ */
 /* O[i, h, :] = sum_{j <= i, same group} softmax_j(scale * Q[i,h].K[j,h/(n_q/n_kv)]) V[j, ...]; bf16 in/out, fp32
  * accumulate.  tcgen05/TMEM/TMA kernel; d_h == 128 only (QVK_E_UNSUPPORTED otherwise). */

@@ -23,6 +23,7 @@ from .prefill import (  # noqa: F401
     score_tokens,
     scorer_from_name,
     select,
+    select_gather,
     snapkv_scores,
     synth_bf16,
     top_k_indices,

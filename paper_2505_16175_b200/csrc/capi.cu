@@ -193,6 +193,23 @@ int qvk_gather(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v
     return gather_checked(s, g, k, v, dtype, heads, width, idx, kc, vc, origin, 0);
 }
 
+int qvk_select_gather(qvk_stream_t s, const qvk_groups* g, const double* scores, const void* k, const void* v,
+                      int dtype, int32_t heads, int32_t width, uint32_t* idx, void* kc, void* vc, uint64_t* origin) {
+    QVK_TRY(check_groups(g));
+    if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
+    if (dtype != QVK_F32 && dtype != QVK_BF16) QVK_INVALID("gather: unsupported dtype");
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
+    if (prune_fused_supported(g, dtype, width, k, v, kc, vc))
+        return launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores, nullptr, idx, kc, vc, origin, 0);
+    uint32_t* ix = idx;
+    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+                                            sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
+    int rc = launch_select(s, g, scores, heads, ix);
+    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, dtype, heads, width, ix, kc, vc, origin, 0);
+    if (!idx) cudaFreeAsync(ix, s);
+    return rc;
+}
+
 int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
               int32_t width, int32_t scorer, double rho, const float* tq, int64_t text_count, int32_t n_h,
               double* scores_ws, uint32_t* idx_ws, void* kc, void* vc, uint64_t* origin) {

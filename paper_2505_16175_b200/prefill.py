@@ -193,6 +193,20 @@ def gather(k, v, groups: DeviceGroups, heads: int, width: int, idx=None, k_cache
     return k_cache, v_cache, origin
 
 
+def select_gather(scores, k, v, groups: DeviceGroups, heads: int, width: int, idx=None, k_cache=None,
+                  v_cache=None, origin=None):
+    """select -> gather from precomputed scores in one launch (qvk_select_gather; e.g. SnapKV scores)."""
+    R = groups.plan.total_rows
+    dev = k.device
+    k_cache = k_cache if k_cache is not None else torch.empty(R * heads * width, dtype=k.dtype, device=dev)
+    v_cache = v_cache if v_cache is not None else torch.empty(R * heads * width, dtype=v.dtype, device=dev)
+    origin = origin if origin is not None else torch.empty(R * heads, dtype=torch.int64, device=dev)
+    idx = idx if idx is not None else torch.empty(max(1, R * heads), dtype=torch.int32, device=dev)
+    check(lib.qvk_select_gather(_stream(), groups.ref, _ptr(scores), _ptr(k), _ptr(v), _dtype_code(k), heads, width,
+                                _ptr(idx), _ptr(k_cache), _ptr(v_cache), _ptr(origin)))
+    return k_cache, v_cache, origin, idx
+
+
 def prune(k, v, groups: DeviceGroups, heads: int, width: int, scorer: Scorer, rho: float, text_query=None,
           n_h: int = 1):
     """score -> select -> gather for every group (prune_group batched; prefill.cpp:255-282)."""

@@ -440,3 +440,21 @@ def test_prune_fused_extreme_values(cuda):
     R = plan.total_rows * heads
     assert torch.equal(idx[:R], idx2[:R])
     assert torch.equal(kc, kc2) and torch.equal(origin, origin2)
+
+
+@pytest.mark.parametrize("sizes,window", [([1024, 1024, 300], 32), ([4096, 77], 16)])
+def test_select_gather_snapkv_matches_separate(cuda, sizes, window):
+    """qvk_select_gather (one cluster launch from precomputed SnapKV scores) == qvk_select + qvk_gather."""
+    n_q, n_kv, D, rho = 28, 4, 128, 0.25
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, D, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, D, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, D, 2, False, cuda)
+    sc = qp.snapkv_scores(q, k, g, n_q, n_kv, window)
+    kc, vc, origin, idx = qp.select_gather(sc, k, v, g, n_kv, D)
+    idx2 = qp.select(sc, g, n_kv)
+    kc2, vc2, origin2 = qp.gather(k, v, g, n_kv, D, idx2)
+    R = plan.total_rows * n_kv
+    assert torch.equal(idx[:R], idx2[:R])
+    assert torch.equal(kc, kc2) and torch.equal(vc, vc2) and torch.equal(origin, origin2)

@@ -21,7 +21,7 @@ ncu)
      python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > "$OUT/ncu_bench.log" 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:attention -c 1 -f -o "$OUT/attn" \
      python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_attn.log" 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'score|select|gather' -c 3 -f -o "$OUT/prune" \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:prune_fused -c 1 -f -o "$OUT/prune" \
      python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > "$OUT/ncu_prune.log" 2>&1 ;;
 esac; done
 ls -la "$OUT"

@@ -10,8 +10,8 @@ bench.py keeps the driver contract on the headline config (C2); this tool covers
   C3b  same with 256 tok/frame (64 groups x 4096)
   C4   1 h @ 1 FPS: 3600 frames x 256 tok (225 groups x 4096), key-norm rho 0.5, 28 layers (1 GPU holds all groups)
   C5   256 frames x 256 tok, group {4,8,16,32,64} frames x rho {0.125,0.25,0.5,1.0}, 1 layer
-Per layer: attention -> score (key-norm or SnapKV) -> select -> gather into that layer's cache, every kernel timed
-with CUDA events on the launch stream.  Layers use two alternating synthetic Q/K/V sets (each larger than L2, the
+Per layer: one qvk_prefill_layer call (attention, then the prune: fused key-norm score+select+gather, or SnapKV
+score + fused select+gather) into that layer's cache; a second, serialised pass times every kernel with CUDA events.  Layers use two alternating synthetic Q/K/V sets (each larger than L2, the
 stand-in model has no residual stream: prefill.cpp:185-190), so timing is per-layer work on cold data.
 tokens/s = tokens x layers-through / wall (a token counts once when it has gone through every layer).
 """
@@ -70,58 +70,68 @@ def run(name, c, steps, warmup, dev):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     snap = c["scorer"] == "snapkv"
-    times = {"attention": [], "score": [], "select": [], "gather": []}
+    scorer = qp.Scorer.snapkv if snap else qp.Scorer.key_norm_small
+    times = {"attention": [], "score": [], "prune": []}
 
-    def layer(l, rec):
+    def layer(l):
+        """The production path: one qvk_prefill_layer call (attention, then the prune overlapping its tail)."""
         q, k, v = sets[l % len(sets)]
-        e = [ev() for _ in range(5)]
+        buf = qp.LayerBuffers(o, scores, idx, kc[l], vc[l], org[l])
+        qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, scorer, True, buffers=buf)
+
+    def layer_kernels(l):
+        """Same layer with the kernels serialised and event-timed one by one (the roofline figures)."""
+        q, k, v = sets[l % len(sets)]
+        e = [ev() for _ in range(4)]
         e[0].record(stream)
         qp.attention(q, k, v, g, n_q, n_kv, out=o)
         e[1].record(stream)
-        if rho != 1.0:
-            if snap:
-                qp.snapkv_scores(q, k, g, n_q, n_kv, 32, 1, out=scores)
-            else:
-                qp.score(k, v, g, n_kv, d, qp.Scorer.key_norm_small, out=scores)
+        if rho == 1.0:  # identity path: no scoring (prefill.cpp:263-270)
             e[2].record(stream)
-            qp.select(scores, g, n_kv, out=idx)
-            e[3].record(stream)
-            qp.gather(k, v, g, n_kv, d, idx, kc[l], vc[l], org[l])
-        else:  # identity path: no scoring (prefill.cpp:263-270)
-            e[2].record(stream)
-            e[3].record(stream)
             qp.gather(k, v, g, n_kv, d, None, kc[l], vc[l], org[l])
-        e[4].record(stream)
-        if rec is not None:
-            rec.append(e)
+        elif snap:
+            qp.snapkv_scores(q, k, g, n_q, n_kv, 32, 1, out=scores)
+            e[2].record(stream)
+            qp.select_gather(scores, k, v, g, n_kv, d, idx, kc[l], vc[l], org[l])
+        else:
+            e[2].record(stream)
+            qp.lib.qvk_prune(stream.cuda_stream, g.ref, k.data_ptr(), v.data_ptr(), qp._lib.QVK_BF16, n_kv, d,
+                             int(qp.Scorer.key_norm_small), rho, None, 0, n_kv, scores.data_ptr(), idx.data_ptr(),
+                             kc[l].data_ptr(), vc[l].data_ptr(), org[l].data_ptr())
+        e[3].record(stream)
+        return e
 
     for _ in range(warmup):
         for l in range(L):
-            layer(l, None)
+            layer(l)
     torch.cuda.synchronize()
     t0, t1 = ev(), ev()
-    recs = []
     t0.record(stream)
     for _ in range(steps):
         for l in range(L):
-            layer(l, recs)
+            layer(l)
     t1.record(stream)
     torch.cuda.synchronize()
     wall_ms = t0.elapsed_time(t1)
+    recs = [layer_kernels(l) for _ in range(max(1, steps // 2)) for l in range(min(L, 4))]
+    torch.cuda.synchronize()
     for e in recs:
         times["attention"].append(e[0].elapsed_time(e[1]))
         times["score"].append(e[1].elapsed_time(e[2]))
-        times["select"].append(e[2].elapsed_time(e[3]))
-        times["gather"].append(e[3].elapsed_time(e[4]))
+        times["prune"].append(e[2].elapsed_time(e[3]))
     avg = {k_: statistics.mean(v_) for k_, v_ in times.items()}
     hbm, tf_burst, _, src = peaks()
     fl = flops_attention(sizes, n_q, d)
     T, Rr = plan.total_tokens, plan.total_rows
-    b_score = snapkv_bytes(plan, n_q, n_kv, d, 32) if snap else float(T * n_kv * (d * 2 + 8))
-    b_select = float(T * n_kv * 8 + Rr * n_kv * 4)
-    b_gather = float(Rr * n_kv * (4 * d * 2 + 8 + (4 if rho != 1.0 else 0)))
-    if rho == 1.0:
-        b_score = b_select = 0.0
+    if rho == 1.0:  # identity copy: K, V rows read and written, origin written
+        b_prune = float(Rr * n_kv * (4 * d * 2 + 8))
+        b_score = 0.0
+    elif snap:  # snapkv.cu reads K and the window queries; the fused select/gather reads the scores
+        b_score = snapkv_bytes(plan, n_q, n_kv, d, 32)
+        b_prune = float(T * n_kv * 8 + Rr * n_kv * (4 * d * 2 + 8 + 4))
+    else:  # fused prune (prune_fused.cu): K read once, scores written, retained V read, K/V/idx/origin written
+        b_score = 0.0
+        b_prune = bytes_prune(plan, n_kv, d)
 
     def gbs(b, ms):
         return None if ms <= 0 or b == 0 else b / (ms / 1e3) / 1e9
@@ -130,19 +140,21 @@ def run(name, c, steps, warmup, dev):
         "config": name, **{k_: v_ for k_, v_ in c.items()}, "groups": plan.n_groups, "group_tokens": sizes[0],
         "tokens": T, "retained_rows": Rr, "steps": steps,
         "tokens_per_s": T * steps / (wall_ms / 1e3), "ms_per_step": wall_ms / steps,
+        "path": "qvk_prefill_layer per layer (prune launched with PDL, overlapping the attention tail)",
         "attention": {"ms": avg["attention"], "tflops": fl / (avg["attention"] / 1e3) / 1e12,
                       "frac": fl / (avg["attention"] / 1e3) / 1e12 / tf_burst},
-        "score": {"kernel": "snapkv" if snap else "key_norm", "ms": avg["score"], "bytes": b_score,
-                  "gbs": gbs(b_score, avg["score"]),
-                  "frac": (gbs(b_score, avg["score"]) or 0) / hbm},
-        "select": {"ms": avg["select"], "bytes": b_select, "gbs": gbs(b_select, avg["select"])},
-        "gather": {"ms": avg["gather"], "bytes": b_gather, "gbs": gbs(b_gather, avg["gather"]),
-                   "frac": (gbs(b_gather, avg["gather"]) or 0) / hbm},
-        "prune": {"ms": avg["score"] + avg["select"] + avg["gather"],
-                  "frac": ((b_score + b_select + b_gather) /
-                           max(1e-9, (avg["score"] + avg["select"] + avg["gather"]) / 1e3) / 1e9) / hbm},
+        "prune": {"kernels": "identity gather" if rho == 1.0 else
+                  ("snapkv score, then fused select+gather" if snap else "fused score+select+gather"),
+                  "ms": avg["score"] + avg["prune"], "bytes": b_score + b_prune,
+                  "gbs": gbs(b_score + b_prune, avg["score"] + avg["prune"]),
+                  "frac": (gbs(b_score + b_prune, avg["score"] + avg["prune"]) or 0) / hbm},
         "peaks": {"tflops": tf_burst, "hbm_gbs": hbm, "source": src},
     }
+    if snap:
+        out["snapkv_score"] = {"ms": avg["score"], "bytes": b_score, "gbs": gbs(b_score, avg["score"]),
+                               "frac": (gbs(b_score, avg["score"]) or 0) / hbm}
+        out["select_gather"] = {"ms": avg["prune"], "bytes": b_prune, "gbs": gbs(b_prune, avg["prune"]),
+                                "frac": (gbs(b_prune, avg["prune"]) or 0) / hbm}
     return out
 
 
