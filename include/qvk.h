@@ -149,6 +149,26 @@ int qvk_prefill_layer(qvk_stream_t stream, const qvk_groups* groups, const qvk_l
                       const void* k_d, const void* v_d, void* o_d, double* scores_ws_d, uint32_t* idx_ws_d,
                       void* k_cache_d, void* v_cache_d, uint64_t* origin_d);
 
+/* ---- §8f-1: QKV projection (tcgen05 GEMM) with the key-norm score fused into its epilogue ------------------------ */
+/* [Q | K | V] = X . W^T: x_d (tokens, d_model) bf16, w_d ((n_q + 2 n_kv) d_h, d_model) bf16 row-major (the
+ * nn.Linear layout of the stacked q/k/v projection weights); outputs q_d (tokens, n_q, d_h), k_d / v_d
+ * (tokens, n_kv, d_h) bf16, fp32 accumulation.  The stand-in of the reference is prefill.cpp:185-190 (K, V only).
+ * When scores_d is not NULL the epilogue also writes the key_norm_small score of every (token, KV head) of the
+ * stored bf16 K (prefill.cpp:200-212 order, bit-identical to qvk_score with heads = n_kv, width = d_h) in the
+ * qvk_score layout of `groups` (which must cover the tokens).  Needs d_model % 64 == 0, 256 % d_h == 0 and
+ * (n_q + 2 n_kv) d_h % 256 == 0 (QVK_E_UNSUPPORTED otherwise). */
+int qvk_project_qkv(qvk_stream_t stream, const void* x_d, int64_t tokens, int32_t d_model, const void* w_d,
+                    int32_t n_q, int32_t n_kv, int32_t d_h, void* q_d, void* k_d, void* v_d,
+                    const qvk_groups* groups, double* scores_d);
+
+/* One pruned-prefill layer from hidden states: qvk_project_qkv (key-norm fused when p->scorer is key_norm_small and
+ * p->per_head) -> attention -> select + gather into the cache (other scorers: their score kernel first).
+ * q_ws_d / k_ws_d / v_ws_d receive the projections; scores_ws_d: n_kv * tokens doubles (required). */
+int qvk_prefill_layer_x(qvk_stream_t stream, const qvk_groups* groups, const qvk_layer_params* p, const void* x_d,
+                        int32_t d_model, const void* w_d, void* q_ws_d, void* k_ws_d, void* v_ws_d, void* o_d,
+                        double* scores_ws_d, uint32_t* idx_ws_d, void* k_cache_d, void* v_cache_d,
+                        uint64_t* origin_d);
+
 /* ---- stand-in model pieces of the reference API (exact, for the drop-in shim) ----------------------------------- */
 /* prefill.cpp:21-30 seeded_matrix generated on the device, bit-identical (counter-based splitmix64). */
 int qvk_seeded_matrix(qvk_stream_t stream, uint64_t seed, uint32_t tag, uint32_t layer, size_t count, double scale,

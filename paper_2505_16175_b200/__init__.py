@@ -16,6 +16,8 @@ from .prefill import (  # noqa: F401
     gather,
     group_count,
     prefill_layer,
+    prefill_layer_x,
+    project_qkv,
     prune,
     prune_group,
     retained_count,

@@ -26,6 +26,8 @@ int launch_project_exact(cudaStream_t, const float*, int64_t, int, const float*,
 int launch_tokenize(cudaStream_t, const uint8_t*, int64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
                     const float*, int, float*);
 int launch_synth_bf16(cudaStream_t, uint64_t, uint32_t, uint32_t, uint64_t, int64_t, int, int, int, void*);
+int launch_project_qkv(cudaStream_t, const void*, int64_t, int, const void*, int, int, int, void*, void*, void*,
+                       const qvk_groups*, double*);
 bool prune_fused_supported(const qvk_groups*, int, int, const void*, const void*, const void*, const void*);
 int launch_prune_fused(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const double*,
                        double*, uint32_t*, void*, void*, uint64_t*, int);
@@ -282,6 +284,38 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
         if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, keep_full);
     }
     if (!scores_ws) cudaFreeAsync(sc, s);
+    if (!idx_ws) cudaFreeAsync(ix, s);
+    return rc;
+}
+
+int qvk_project_qkv(qvk_stream_t s, const void* x, int64_t tokens, int32_t d_model, const void* w, int32_t n_q,
+                    int32_t n_kv, int32_t d_h, void* q, void* k, void* v, const qvk_groups* g, double* scores) {
+    if (g) QVK_TRY(check_groups(g));
+    if (n_q > 0 && n_kv > 0 && n_q % n_kv != 0) QVK_INVALID("project: n_q must be a multiple of n_kv");
+    return launch_project_qkv(s, x, tokens, d_model, w, n_q, n_kv, d_h, q, k, v, g, scores);
+}
+
+int qvk_prefill_layer_x(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* x,
+                        int32_t d_model, const void* w, void* q, void* k, void* v, void* o, double* scores_ws,
+                        uint32_t* idx_ws, void* kc, void* vc, uint64_t* origin) {
+    if (!p) QVK_INVALID("prefill_layer: null params");
+    QVK_TRY(check_rho(p->rho));
+    QVK_TRY(check_groups(g));
+    if (!scores_ws) QVK_INVALID("prefill_layer_x: scores workspace required");
+    const bool fused_norm = p->scorer == QVK_KEY_NORM_SMALL && p->per_head && p->rho != 1.0;
+    QVK_TRY(launch_project_qkv(s, x, g->total_tokens, d_model, w, p->n_q, p->n_kv, p->d_h, q, k, v, g,
+                               fused_norm ? scores_ws : nullptr));
+    if (!fused_norm) return qvk_prefill_layer(s, g, p, q, k, v, o, scores_ws, idx_ws, kc, vc, origin);
+    QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
+    const int heads = p->n_kv, width = p->d_h;
+    if (prune_fused_supported(g, QVK_BF16, width, k, v, kc, vc))  // scores came from the projection epilogue
+        return launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores_ws, nullptr, idx_ws, kc, vc, origin,
+                                  1);
+    uint32_t* ix = idx_ws;
+    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+                                            sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
+    int rc = launch_select(s, g, scores_ws, heads, ix);
+    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, 0);
     if (!idx_ws) cudaFreeAsync(ix, s);
     return rc;
 }

@@ -1,0 +1,275 @@
+// §8f-1: the QKV projection of a prefill layer as a tcgen05 GEMM with the key-norm score fused into its epilogue.
+//
+// The reference's stand-in model projects every layer's tokens with two naive fp32 x fp32 -> double GEMMs
+// (prefill.cpp:38-54 `matmul`, called by `project`, prefill.cpp:185-190) — >= 97 % of its CPU prefill time
+// (SURVEY.md §0.7).  The GQA layer this framework prefills needs Q, K and V:
+//     [Q | K | V] (T x (n_q + 2 n_kv) d_h) = X (T x d_model) . W^T,   W: ((n_q + 2 n_kv) d_h) x d_model (row-major)
+// bf16 operands, fp32 accumulation in TMEM, bf16 outputs written straight into the three (tokens, heads, d_h) tensors
+// the attention / prune kernels consume.  For the columns of K the epilogue also computes the key-norm score of
+// every (token, KV head) — -sqrt(sum of squares) of the bf16-rounded row in the reference's sequential double order
+// (prefill.cpp:200-212), bit-identical to qvk_score on the stored K — so the prune never re-reads K from HBM.
+//
+// Kernel: persistent (one CTA per SM), 128 x 256 output tiles (n fastest, so co-resident CTAs share the X row
+// block through L2), BK = 64, 4-stage TMA ring (16 KB X + 32 KB W per stage, SWIZZLE_128B, both K-major),
+// tcgen05.mma.cta_group::1.kind::f16 M = 128, N = 256, K = 16 issued by one elected thread into one of two
+// 256-column TMEM accumulators, so the epilogue of tile i overlaps the main loop of tile i + 1.
+// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2-5 epilogue (TMEM lane quarter = warp % 4, one output row
+// per thread).  Algorithmic FLOPs: 2 T d_model (n_q + 2 n_kv) d_h.
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace qvk {
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kBK = 64;
+constexpr int kStages = 4;
+constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
+constexpr uint32_t kBBytes = kBN * kBK * 2;   // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;
+constexpr int kTmaWarp = 0, kMmaWarp = 1;
+
+struct ProjParams {
+    int64_t m;          // tokens
+    int n, k;           // output columns, d_model
+    int q_cols, kv_cols, d_h, n_kv;
+    __nv_bfloat16 *q, *k_out, *v;
+    // fused key-norm (optional)
+    double* scores;
+    const int64_t* tok_off;
+    int n_groups;
+    int64_t max_tokens;
+};
+
+struct ProjBarriers {
+    uint64_t full[kStages], empty[kStages];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem_base;
+};
+
+constexpr size_t kSmem = 1024 + kStages * kStageBytes + sizeof(ProjBarriers);
+
+__device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk) {
+    return ptx::umma_desc_sw128(tile + kk * 32, 16, 1024);  // k-step kk: +32 B inside the 128-byte SW128 rows
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    project_qkv_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                       const ProjParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    ProjBarriers* bar = reinterpret_cast<ProjBarriers*>(smem + kStages * kStageBytes);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m_tiles = static_cast<int>((p.m + kBM - 1) / kBM);
+    const int n_tiles = p.n / kBN;
+    const int tiles = m_tiles * n_tiles;
+    const int kb_count = p.k / kBK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&bar->full[s], 1);
+            ptx::mbar_init(&bar->empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bar->acc_full[b], 1);
+            ptx::mbar_init(&bar->acc_empty[b], 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == kMmaWarp) ptx::tmem_alloc<512>(&bar->tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = bar->tmem_base;
+
+    if (warp == kTmaWarp) {
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tm_x);
+            ptx::prefetch_tmap(&tm_w);
+            uint32_t it = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int mt = tile / n_tiles, nt = tile - mt * n_tiles;
+                for (int kb = 0; kb < kb_count; ++kb, ++it) {
+                    const uint32_t s = it % kStages;
+                    ptx::mbar_wait(&bar->empty[s], ((it / kStages) & 1) ^ 1);
+                    uint8_t* st = smem + s * kStageBytes;
+                    ptx::mbar_arrive_expect_tx(&bar->full[s], kStageBytes);
+                    ptx::tma_load_2d(st, &tm_x, &bar->full[s], kb * kBK, mt * kBM);
+                    ptx::tma_load_2d(st + kABytes, &tm_w, &bar->full[s], kb * kBK, nt * kBN);
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (ptx::elect_one()) {
+            constexpr uint32_t kId = ptx::idesc_bf16_f32(kBM, kBN, false, false);
+            const uint32_t base = ptx::smem_u32(smem);
+            uint32_t it = 0, n_acc = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++n_acc) {
+                const uint32_t b = n_acc & 1;
+                ptx::mbar_wait(&bar->acc_empty[b], ((n_acc >> 1) & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + b * kBN;
+                for (int kb = 0; kb < kb_count; ++kb, ++it) {
+                    const uint32_t s = it % kStages;
+                    ptx::mbar_wait(&bar->full[s], (it / kStages) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = base + s * kStageBytes, b_addr = a_addr + kABytes;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk)
+                        ptx::mma_ss(d, kdesc(a_addr, kk), kdesc(b_addr, kk), kId, (kb | kk) != 0);
+                    ptx::mma_commit(&bar->empty[s]);
+                }
+                ptx::mma_commit(&bar->acc_full[b]);
+            }
+        }
+    } else {
+        // ===================== epilogue: TMEM -> bf16 -> Q / K / V (+ key-norm of the K heads) =====================
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        uint32_t n_acc = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++n_acc) {
+            const int mt = tile / n_tiles, nt = tile - mt * n_tiles;
+            const uint32_t b = n_acc & 1;
+            ptx::mbar_wait(&bar->acc_full[b], (n_acc >> 1) & 1);
+            ptx::tc_fence_after();
+            const int64_t m = static_cast<int64_t>(mt) * kBM + row;
+            const bool live = m < p.m;
+            double acc = 0.0;  // key-norm: running sum of squares of the current K head (reference order)
+#pragma unroll 1
+            for (int c = 0; c < kBN / 32; ++c) {
+                float x[32];
+                QVK_TMEM_LD32F(tmem + lane_off + b * kBN + 32 * c, x);
+                ptx::tmem_ld_wait();
+                if (c == kBN / 32 - 1) {  // accumulator fully read: the MMA warp may reuse it
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&bar->acc_empty[b]);
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pk[e] = ptx::pack_bf16(x[2 * e], x[2 * e + 1]);
+                const int col = nt * kBN + 32 * c;  // global output column of this 32-column chunk
+                __nv_bfloat16* dst;
+                bool is_k = false;
+                int kcol = 0;
+                if (col < p.q_cols) {
+                    dst = p.q + m * p.q_cols + col;
+                } else if (col < p.q_cols + p.kv_cols) {
+                    kcol = col - p.q_cols;
+                    dst = p.k_out + m * p.kv_cols + kcol;
+                    is_k = true;
+                } else {
+                    dst = p.v + m * p.kv_cols + (col - p.q_cols - p.kv_cols);
+                }
+                if (live) {
+                    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                }
+                if (is_k && p.scores && live) {
+                    // prefill.cpp:207: sum over the head's columns in order of double(bf16 value)^2 (exact squares)
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const double lo = static_cast<double>(__uint_as_float(pk[e] << 16));
+                        const double hi = static_cast<double>(__uint_as_float(pk[e] & 0xffff0000u));
+                        acc = __fma_rn(lo, lo, acc);
+                        acc = __fma_rn(hi, hi, acc);
+                    }
+                    if ((kcol + 32) % p.d_h == 0) {  // last chunk of this KV head
+                        const int h = kcol / p.d_h;
+                        const int g = find_group_fast(p.tok_off, p.n_groups, m, p.max_tokens);
+                        const int64_t t0 = __ldg(p.tok_off + g);
+                        const int64_t n = __ldg(p.tok_off + g + 1) - t0;
+                        p.scores[p.n_kv * t0 + h * n + (m - t0)] = -__dsqrt_rn(acc);  // key_norm_small
+                        acc = 0.0;
+                    }
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d_model, const void* w, int n_q,
+                       int n_kv, int d_h, void* q, void* k, void* v, const qvk_groups* g, double* scores) {
+    const int n = (n_q + 2 * n_kv) * d_h;
+    if (tokens < 0 || d_model <= 0 || n_q <= 0 || n_kv <= 0 || d_h <= 0)
+        QVK_INVALID("model config: dimensions must be positive");
+    if (d_h % 32 != 0 || kBN % d_h != 0 || d_model % kBK != 0 || n % kBN != 0) {
+        set_error("project: needs d_h % 32 == 0, d_model % 64 == 0 and (n_q + 2 n_kv) d_h % 256 == 0");
+        return QVK_E_UNSUPPORTED;
+    }
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(q) |
+         reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15)
+        QVK_INVALID("project: tensors must be 16-byte aligned");
+    if (scores && (!g || g->total_tokens != tokens)) QVK_INVALID("project: scores need the token groups");
+    if (tokens == 0) return QVK_OK;
+    CUtensorMap mx, mw;
+    if (!make_map_2d(&mx, x, tokens, d_model, kBM) || !make_map_2d(&mw, w, n, d_model, kBN)) {
+        set_error("project: cuTensorMapEncodeTiled failed");
+        return QVK_E_CUDA;
+    }
+    ProjParams p;
+    p.m = tokens;
+    p.n = n;
+    p.k = d_model;
+    p.q_cols = n_q * d_h;
+    p.kv_cols = n_kv * d_h;
+    p.d_h = d_h;
+    p.n_kv = n_kv;
+    p.q = static_cast<__nv_bfloat16*>(q);
+    p.k_out = static_cast<__nv_bfloat16*>(k);
+    p.v = static_cast<__nv_bfloat16*>(v);
+    p.scores = scores;
+    p.tok_off = g ? g->tok_off_d : nullptr;
+    p.n_groups = g ? g->n_groups : 0;
+    p.max_tokens = g ? g->max_tokens : 0;
+    static bool attr = false;
+    if (!attr) {
+        QVK_CUDA_CHECK(cudaFuncSetAttribute(project_qkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(kSmem)));
+        attr = true;
+    }
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        QVK_CUDA_CHECK(cudaGetDevice(&dev));
+        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t tiles = ((tokens + kBM - 1) / kBM) * (n / kBN);
+    if (tiles > 0x7fffffff) QVK_INVALID("project: too many tiles");
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, sms));
+    project_qkv_kernel<<<grid, kThreads, kSmem, stream>>>(mx, mw, p);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
+}  // namespace qvk

@@ -503,7 +503,7 @@ bool prune_fused_supported(const qvk_groups* g, int dtype, int width, const void
 }
 
 // scorer: QVK_KEY_NORM_SMALL / QVK_VALUE_NORM (scores computed here; written to scores_out when non-null) or
-// QVK_SNAPKV (scores_in precomputed).
+// QVK_SNAPKV = any precomputed scores in scores_in (SnapKV, or the key-norm fused into the projection).
 // overlap_prev: the previous kernel on `stream` does not produce k / v (see the kernel's PDL note).
 int launch_prune_fused(cudaStream_t stream, const qvk_groups* g, const void* k, const void* v, int heads, int width,
                        int scorer, const double* scores_in, double* scores_out, uint32_t* idx, void* kc, void* vc,

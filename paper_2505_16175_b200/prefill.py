@@ -288,6 +288,47 @@ def prefill_layer(q, k, v, groups: DeviceGroups, n_q: int, n_kv: int, rho: float
     return buf
 
 
+def project_qkv(x, w, n_q: int, n_kv: int, d_h: int, groups: DeviceGroups | None = None, with_scores: bool = False,
+                q=None, k=None, v=None, scores=None):
+    """[Q | K | V] = X W^T on the tensor cores (qvk_project_qkv); with_scores: key-norm per (token, KV head) fused
+    into the epilogue (needs groups).  Returns q, k, v (and scores)."""
+    T, d_model = x.shape[0], x.shape[-1]
+    dev = x.device
+    q = q if q is not None else torch.empty(T, n_q, d_h, dtype=torch.bfloat16, device=dev)
+    k = k if k is not None else torch.empty(T, n_kv, d_h, dtype=torch.bfloat16, device=dev)
+    v = v if v is not None else torch.empty(T, n_kv, d_h, dtype=torch.bfloat16, device=dev)
+    if with_scores and scores is None:
+        scores = torch.empty(max(1, T * n_kv), dtype=torch.float64, device=dev)
+    check(lib.qvk_project_qkv(_stream(), _ptr(x), T, d_model, _ptr(w), n_q, n_kv, d_h, _ptr(q), _ptr(k), _ptr(v),
+                              groups.ref if groups is not None else None, _ptr(scores) if with_scores else None))
+    return (q, k, v, scores) if with_scores else (q, k, v)
+
+
+def prefill_layer_x(x, w, groups: DeviceGroups, n_q: int, n_kv: int, d_h: int, rho: float,
+                    scorer: Scorer = Scorer.key_norm_small, per_head: bool = True, scale: float | None = None,
+                    snap_window: int = 32, snap_pool: int = 1, buffers: LayerBuffers | None = None,
+                    qkv=None, cache_row_offset: int = 0):
+    """Projection -> attention -> prune for one layer from hidden states X (qvk_prefill_layer_x)."""
+    T, d_model = x.shape[0], x.shape[-1]
+    dev = x.device
+    buf = buffers or LayerBuffers.allocate(groups.plan, n_q, n_kv, d_h, per_head, dev)
+    if qkv is None:
+        qkv = (torch.empty(T, n_q, d_h, dtype=torch.bfloat16, device=dev),
+               torch.empty(T, n_kv, d_h, dtype=torch.bfloat16, device=dev),
+               torch.empty(T, n_kv, d_h, dtype=torch.bfloat16, device=dev))
+    heads = n_kv if per_head else 1
+    width = d_h if per_head else n_kv * d_h
+    prm = L.QvkLayerParams(n_q, n_kv, d_h, int(scorer), int(per_head), rho,
+                           1.0 / math.sqrt(d_h) if scale is None else scale, snap_window, snap_pool)
+    off = cache_row_offset * heads
+    kc = buf.k_cache.data_ptr() + off * width * 2
+    vc = buf.v_cache.data_ptr() + off * width * 2
+    og = buf.origin.data_ptr() + off * 8
+    check(lib.qvk_prefill_layer_x(_stream(), groups.ref, C.byref(prm), _ptr(x), d_model, _ptr(w), _ptr(qkv[0]),
+                                  _ptr(qkv[1]), _ptr(qkv[2]), _ptr(buf.o), _ptr(buf.scores), _ptr(buf.idx), kc, vc, og))
+    return buf, qkv
+
+
 def synth_bf16(seed: int, tag: int, layer: int, group: int, rows: int, heads: int, width: int,
                head_scale: bool, device="cuda") -> torch.Tensor:
     """Synthetic activations generated in HBM (same bits as oracle qvo_synth_bf16)."""

@@ -458,3 +458,51 @@ def test_select_gather_snapkv_matches_separate(cuda, sizes, window):
     R = plan.total_rows * n_kv
     assert torch.equal(idx[:R], idx2[:R])
     assert torch.equal(kc, kc2) and torch.equal(vc, vc2) and torch.equal(origin, origin2)
+
+
+# ------------------------------------------------------------------------------------------------ projection (§8f-1)
+def _proj_inputs(T, d_model, n_q, n_kv, d_h, device, seed=5):
+    x = qp.synth_bf16(seed, 7, 0, 0, T, 1, d_model, False, device).view(T, d_model)
+    w = (qp.synth_bf16(seed, 8, 0, 0, (n_q + 2 * n_kv) * d_h, 1, d_model, False, device).float()
+         * (1.0 / math.sqrt(d_model))).to(torch.bfloat16).view(-1, d_model)
+    return x, w
+
+
+@pytest.mark.parametrize("sizes,d_model,n_q,n_kv,d_h", [([4096, 1000], 3584, 28, 4, 128), ([256] * 4, 256, 4, 2, 64),
+                                                        ([77, 300], 512, 8, 4, 64), ([128], 1024, 4, 2, 128)])
+def test_project_qkv_vs_torch_and_fused_keynorm(cuda, sizes, d_model, n_q, n_kv, d_h):
+    """tcgen05 QKV GEMM vs a torch fp32 matmul of the same bf16 operands (|err| <= 1e-2 + 1e-2 |ref|: bf16 output
+    rounding + accumulation order), and the key-norm fused into its epilogue == qvk_score on the stored K, bit for
+    bit (prefill.cpp:200-212 order)."""
+    T = sum(sizes)
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    x, w = _proj_inputs(T, d_model, n_q, n_kv, d_h, cuda)
+    q, k, v, sc = qp.project_qkv(x, w, n_q, n_kv, d_h, g, with_scores=True)
+    ref = x.float() @ w.float().t()
+    qc, kc = n_q * d_h, n_kv * d_h
+    check_tol(q.view(T, -1), ref[:, :qc], "Q")
+    check_tol(k.view(T, -1), ref[:, qc:qc + kc], "K")
+    check_tol(v.view(T, -1), ref[:, qc + kc:], "V")
+    want = qp.score(k, v, g, n_kv, d_h, qp.Scorer.key_norm_small)
+    assert sc.cpu().numpy().tobytes() == want.cpu().numpy().tobytes()
+
+
+def test_prefill_layer_x_matches_projection_then_layer(cuda):
+    """qvk_prefill_layer_x (projection with fused key-norm -> attention -> fused select/gather) == qvk_project_qkv
+    followed by qvk_prefill_layer on its outputs, bit for bit."""
+    sizes, d_model, n_q, n_kv, d_h, rho = [2048, 2048, 640], 3584, 28, 4, 128, 0.5
+    T = sum(sizes)
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    x, w = _proj_inputs(T, d_model, n_q, n_kv, d_h, cuda, seed=9)
+    buf, (q, k, v) = qp.prefill_layer_x(x, w, g, n_q, n_kv, d_h, rho)
+    q2, k2, v2 = qp.project_qkv(x, w, n_q, n_kv, d_h)
+    assert torch.equal(q, q2) and torch.equal(k, k2) and torch.equal(v, v2)
+    buf2 = qp.prefill_layer(q2, k2, v2, g, n_q, n_kv, rho)
+    torch.cuda.synchronize()
+    R = plan.total_rows * n_kv
+    assert torch.equal(buf.o, buf2.o)
+    assert torch.equal(buf.idx[:R], buf2.idx[:R])
+    assert torch.equal(buf.k_cache, buf2.k_cache) and torch.equal(buf.v_cache, buf2.v_cache)
+    assert torch.equal(buf.origin, buf2.origin)
