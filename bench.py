@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-layer", action="store_true", help="skip the from-hidden-states layer (projection)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     return ap.parse_args()
 
@@ -272,6 +273,54 @@ def main():
     total_tokens = plan.total_tokens
     value = total_tokens * args.steps / (elapsed_ms / 1e3)
 
+    # ---- the same layer from hidden states: QKV projection GEMM (key-norm fused) -> attention -> select+gather ----
+    full = None
+    if not args.no_full_layer:
+        d_model = n_q * d
+        x = torch.cat([qp.synth_bf16(1, 7, 0, gidx0 + i, n, 1, d_model, False, dev) for i, n in enumerate(sizes)])
+        x = x.view(-1, d_model)
+        wqkv = (qp.synth_bf16(1, 8, 0, 0, (n_q + 2 * n_kv) * d, 1, d_model, False, dev).float()
+                * (1.0 / math.sqrt(d_model))).to(torch.bfloat16).view(-1, d_model)
+        qkv = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
+
+        def full_step():
+            qp.prefill_layer_x(x, wqkv, g, n_q, n_kv, d, rho, buffers=buf, qkv=qkv, cache_row_offset=row_base)
+            if world > 1:
+                allgather_cache([buf.k_cache, buf.v_cache, buf.origin], bounds, [unit, unit, n_kv])
+
+        for _ in range(args.warmup):
+            full_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = ev(), ev()
+        f0.record(stream)
+        for _ in range(args.steps):
+            full_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        pj = []
+        for _ in range(max(3, args.steps)):
+            a0, a1 = ev(), ev()
+            a0.record(stream)
+            qp.project_qkv(x, wqkv, n_q, n_kv, d, g, True, *qkv, buf.scores)
+            a1.record(stream)
+            pj.append((a0, a1))
+        torch.cuda.synchronize()
+        t = torch.tensor([f0.elapsed_time(f1), statistics.mean(a.elapsed_time(b) for a, b in pj)], device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        full_ms, proj_ms = t.tolist()
+        proj_fl = 2.0 * plan.total_tokens / world * d_model * (n_q + 2 * n_kv) * d
+        full = {"value": plan.total_tokens * args.steps / (full_ms / 1e3), "unit": "tokens/s",
+                "ms_per_step": full_ms / args.steps,
+                "path": "qvk_prefill_layer_x: hidden states X (T x 3584) -> tcgen05 QKV projection GEMM with the "
+                        "key-norm fused into its epilogue -> attention -> fused select+gather (PDL)",
+                "projection": {"kernel": "project_qkv_kernel (tcgen05)", "avg_launch_ms": proj_ms,
+                               "flop_per_launch": proj_fl, "achieved_tflops": proj_fl / (proj_ms / 1e3) / 1e12},
+                "data": "synthetic X ~ N(0,1), W ~ N(0, 1/d_model), bf16"}
+        del x, wqkv, qkv
+
     # ---- e2e through the C ABI with host buffers (H2D of this step's Q/K/V, D2H of the pruned cache) ----
     e2e = None
     if not args.no_e2e:
@@ -319,6 +368,8 @@ def main():
     pb = bytes_prune(local_plan, n_kv, d)
     prof_p = ROOT / "profiles" / "ncu_prune_summary.json"
     traffic_p = json.loads(prof_p.read_text()).get("dram_bytes_per_launch") if prof_p.exists() else None
+    if full is not None:
+        full["projection"]["frac_of_peak"] = full["projection"]["achieved_tflops"] / tf_burst
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -339,7 +390,7 @@ def main():
             "secondary": {"kernels": "prune_fused_kernel: score+select+gather in one cluster launch (qvk_prune)", "avg_ms": prune_avg,
                           "algorithmic_bytes": pb, "achieved_gbs": pb / (prune_avg / 1e3) / 1e9,
                           "hbm_peak_gbs": hbm, "frac": pb / (prune_avg / 1e3) / 1e9 / hbm, "traffic": traffic_p},
-            "clocks": clocks, "e2e": e2e, "gpu_launches": 2 * args.steps,
+            "clocks": clocks, "e2e": e2e, "gpu_launches": 2 * args.steps, "full_layer": full,
         }
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1
