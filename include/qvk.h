@@ -169,6 +169,17 @@ int qvk_prefill_layer_x(qvk_stream_t stream, const qvk_groups* groups, const qvk
                         double* scores_ws_d, uint32_t* idx_ws_d, void* k_cache_d, void* v_cache_d,
                         uint64_t* origin_d);
 
+/* ---- §8f-4: decode-step consumer of the pruned cache ------------------------------------------------------------- */
+/* O[t, h] = softmax_r(scale * q[t, h] . K[r, h / (n_q/n_kv)]) V[r, ...] over every cache row r (non-causal: the video
+ * tokens precede the queries) and lse[t, h] = ln sum_r exp(scale * q . K[r]) (may be NULL) so the caller can merge it
+ * with its own text-token attention.  q_d / o_d (n_tq, n_q, d_h) bf16; k_cache_d / v_cache_d (rows, n_kv, d_h) bf16 —
+ * one layer of the per-head pruned cache (qvk_prefill_layer's layout).  d_h == 128.  Split-KV: ws_d must hold
+ * qvk_decode_workspace(...) bytes. */
+int qvk_decode_workspace(int32_t n_tq, int32_t n_q, int32_t n_kv, int32_t d_h, int64_t rows, size_t* bytes);
+int qvk_decode_attention(qvk_stream_t stream, const void* q_d, int32_t n_tq, int32_t n_q, int32_t n_kv, int32_t d_h,
+                         const void* k_cache_d, const void* v_cache_d, int64_t rows, float scale, void* o_d,
+                         float* lse_d, void* ws_d, size_t ws_bytes);
+
 /* ---- stand-in model pieces of the reference API (exact, for the drop-in shim) ----------------------------------- */
 /* prefill.cpp:21-30 seeded_matrix generated on the device, bit-identical (counter-based splitmix64). */
 int qvk_seeded_matrix(qvk_stream_t stream, uint64_t seed, uint32_t tag, uint32_t layer, size_t count, double scale,

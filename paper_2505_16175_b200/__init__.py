@@ -13,6 +13,7 @@ from .prefill import (  # noqa: F401
     PruneConfig,
     Scorer,
     attention,
+    decode_attention,
     gather,
     group_count,
     prefill_layer,

@@ -28,6 +28,8 @@ int launch_tokenize(cudaStream_t, const uint8_t*, int64_t, uint32_t, uint32_t, u
 int launch_synth_bf16(cudaStream_t, uint64_t, uint32_t, uint32_t, uint64_t, int64_t, int, int, int, void*);
 int launch_project_qkv(cudaStream_t, const void*, int64_t, int, const void*, int, int, int, void*, void*, void*,
                        const qvk_groups*, double*);
+int launch_decode_attention(cudaStream_t, const void*, int, int, int, int, const void*, const void*, int64_t, float,
+                            void*, float*, void*, size_t, size_t*);
 bool prune_fused_supported(const qvk_groups*, int, int, const void*, const void*, const void*, const void*);
 int launch_prune_fused(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const double*,
                        double*, uint32_t*, void*, void*, uint64_t*, int);
@@ -318,6 +320,21 @@ int qvk_prefill_layer_x(qvk_stream_t s, const qvk_groups* g, const qvk_layer_par
     if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, 0);
     if (!idx_ws) cudaFreeAsync(ix, s);
     return rc;
+}
+
+int qvk_decode_workspace(int32_t n_tq, int32_t n_q, int32_t n_kv, int32_t d_h, int64_t rows, size_t* bytes) {
+    if (!bytes) QVK_INVALID("decode_workspace: null output");
+    // size query: no tensors are touched (aligned dummy pointers pass the checks)
+    void* const dummy = reinterpret_cast<void*>(uintptr_t(256));
+    return launch_decode_attention(nullptr, dummy, n_tq, n_q, n_kv, d_h, dummy, dummy, rows, 1.f, dummy, nullptr,
+                                   nullptr, 0, bytes);
+}
+
+int qvk_decode_attention(qvk_stream_t s, const void* q, int32_t n_tq, int32_t n_q, int32_t n_kv, int32_t d_h,
+                         const void* kc, const void* vc, int64_t rows, float scale, void* o, float* lse, void* ws,
+                         size_t ws_bytes) {
+    if (!ws) QVK_INVALID("decode_attention: workspace required");
+    return launch_decode_attention(s, q, n_tq, n_q, n_kv, d_h, kc, vc, rows, scale, o, lse, ws, ws_bytes, nullptr);
 }
 
 // ---- stand-in model pieces --------------------------------------------------------------------------------------

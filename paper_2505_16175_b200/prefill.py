@@ -329,6 +329,24 @@ def prefill_layer_x(x, w, groups: DeviceGroups, n_q: int, n_kv: int, d_h: int, r
     return buf, qkv
 
 
+def decode_attention(q, k_cache, v_cache, n_q: int, n_kv: int, scale: float | None = None, with_lse: bool = False,
+                     out=None, workspace=None):
+    """Attention of query tokens q (n_tq, n_q, d) over one layer's pruned cache (rows, n_kv, d) — the decode-step
+    consumer (qvk_decode_attention).  Returns o (and the natural-log LSE per (token, head))."""
+    n_tq, d = q.shape[0], q.shape[-1]
+    rows = k_cache.numel() // (n_kv * d)
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    need = C.c_size_t(0)
+    check(lib.qvk_decode_workspace(n_tq, n_q, n_kv, d, rows, C.byref(need)))
+    ws = workspace if workspace is not None and workspace.numel() >= need.value else \
+        torch.empty(max(1, need.value), dtype=torch.uint8, device=q.device)
+    out = out if out is not None else torch.empty(n_tq, n_q, d, dtype=torch.bfloat16, device=q.device)
+    lse = torch.empty(n_tq, n_q, dtype=torch.float32, device=q.device) if with_lse else None
+    check(lib.qvk_decode_attention(_stream(), _ptr(q), n_tq, n_q, n_kv, d, _ptr(k_cache), _ptr(v_cache), rows, scale,
+                                   _ptr(out), _ptr(lse), _ptr(ws), ws.numel()))
+    return (out, lse) if with_lse else out
+
+
 def synth_bf16(seed: int, tag: int, layer: int, group: int, rows: int, heads: int, width: int,
                head_scale: bool, device="cuda") -> torch.Tensor:
     """Synthetic activations generated in HBM (same bits as oracle qvo_synth_bf16)."""

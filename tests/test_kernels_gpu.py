@@ -506,3 +506,25 @@ def test_prefill_layer_x_matches_projection_then_layer(cuda):
     assert torch.equal(buf.idx[:R], buf2.idx[:R])
     assert torch.equal(buf.k_cache, buf2.k_cache) and torch.equal(buf.v_cache, buf2.v_cache)
     assert torch.equal(buf.origin, buf2.origin)
+
+
+# ------------------------------------------------------------------------------------------------ decode consumer (§8f-4)
+@pytest.mark.parametrize("n_tq,rows,n_q,n_kv", [(1, 32768, 28, 4), (3, 100, 28, 4), (64, 5000, 28, 4), (1, 1, 4, 2),
+                                                (10, 70001, 8, 8)])
+def test_decode_attention_vs_torch(cuda, n_tq, rows, n_q, n_kv):
+    """Query tokens attending over a pruned cache (non-causal, GQA) vs a torch fp32 reference: O within
+    1e-2 + 1e-2 |ref| (bf16 output), natural-log LSE within 1e-3 absolute."""
+    d = 128
+    gen = torch.Generator(device=cuda).manual_seed(rows + n_tq)
+    q = torch.randn(n_tq, n_q, d, device=cuda, generator=gen).to(torch.bfloat16)
+    kc = torch.randn(rows, n_kv, d, device=cuda, generator=gen).to(torch.bfloat16)
+    vc = torch.randn(rows, n_kv, d, device=cuda, generator=gen).to(torch.bfloat16)
+    o, lse = qp.decode_attention(q, kc, vc, n_q, n_kv, with_lse=True)
+    g = n_q // n_kv
+    kf = kc.float().repeat_interleave(g, 1).permute(1, 0, 2)   # (n_q, rows, d)
+    vf = vc.float().repeat_interleave(g, 1).permute(1, 0, 2)
+    s = torch.einsum("thd,hrd->htr", q.float(), kf) / math.sqrt(d)
+    ref = torch.einsum("htr,hrd->thd", torch.softmax(s, -1), vf)
+    check_tol(o, ref, "decode O")
+    lse_ref = torch.logsumexp(s, -1).t()
+    assert (lse - lse_ref).abs().max().item() <= 1e-3
