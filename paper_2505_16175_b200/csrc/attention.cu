@@ -77,6 +77,7 @@ struct AttnParams {
     int total_units;
     float scale_log2;
     __nv_bfloat16* o;
+    int pre_issue;  // issue the next unit's S0(0) during tile 1's lone last step (QVK_ATTN_PRE=0 disables)
 };
 
 struct Barriers {
@@ -241,6 +242,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t item = 0;
             uint32_t pv_step[2] = {0, 0};  // P publications consumed per tile (p_full phases)
             uint32_t o_units[2] = {0, 0};  // units per tile (o_free phases)
+            bool s0_pre = false;           // S0(0) of this unit was issued ahead, during the previous unit's last step
+            auto wait_item = [&](uint32_t it) -> uint32_t {
+                const uint32_t st = it % kStages;
+                ptx::mbar_wait(&bar->kv_full[st], (it / kStages) & 1);
+                ptx::tc_fence_after();
+                return ring + st * kTileBytes;
+            };
+            // S_t(j) = Q_t K(j)^T into TMEM columns [128 t, 128 t + 128)
+            auto issue_s_at = [&](int t, uint32_t qa, uint32_t k_addr) {
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk)
+                    ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
+            };
             for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
                 const Unit w = decode_unit(p, u);
                 if (!w.valid) continue;
@@ -249,13 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t q_addr = q_base + qb * 2 * kTileBytes;
                 ptx::mbar_wait(&bar->q_full[qb], (unit_iter >> 1) & 1);
                 ptx::tc_fence_after();
-                // S_t(j) into TMEM columns [128 t, 128 t + 128)
-                auto issue_s = [&](int t, uint32_t k_addr) {
-                    const uint32_t qa = q_addr + t * kTileBytes;
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
-                };
+                auto issue_s = [&](int t, uint32_t k_addr) { issue_s_at(t, q_addr + t * kTileBytes, k_addr); };
                 // O_t += P_t(j) V(j), in two halves as the softmax publishes P (p_full[t][0], p_full[t][1]).
                 auto issue_pv = [&](int t, uint32_t v_addr, int j) {
                     if (j == 0) ptx::mbar_wait(&bar->o_free[t], (o_units[t] & 1) ^ 1);
@@ -275,21 +283,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ++o_units[t];
                     }
                 };
-                auto wait_item = [&](uint32_t it) -> uint32_t {
-                    const uint32_t st = it % kStages;
-                    ptx::mbar_wait(&bar->kv_full[st], (it / kStages) & 1);
-                    ptx::tc_fence_after();
-                    return ring + st * kTileBytes;
-                };
                 const uint32_t k0 = wait_item(item);
-                issue_s(0, k0);
-                ptx::mma_commit(&bar->s_full[0]);
+                if (!s0_pre) {
+                    issue_s(0, k0);
+                    ptx::mma_commit(&bar->s_full[0]);
+                }
                 if (w.n1) {
                     issue_s(1, k0);
                     ptx::mma_commit(&bar->s_full[1]);
                 }
                 if (w.nkv == 1) ptx::mma_commit(&bar->q_empty[qb]);  // every S of the unit issued
                 ptx::mma_commit(&bar->kv_empty[item % kStages]);
+                bool next_pre = false;
                 for (int j = 0; j < w.nkv; ++j) {
                     const uint32_t v_item = item + 2 * j + 1;
                     const uint32_t v_addr = wait_item(v_item);
@@ -312,9 +317,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (j + 2 == w.nkv) ptx::mma_commit(&bar->q_empty[qb]);  // the unit's last S was just issued
                     if (more) ptx::mma_commit(&bar->kv_empty[(v_item + 1) % kStages]);
+                    // Tile 1 has one more (diagonal) step than tile 0: while its softmax runs that last step alone,
+                    // start the next unit — its S0(0) goes into tile 0's free S columns (P0's last PV was issued
+                    // above), so the next unit's tile-0 softmax overlaps this unit's tail.  K(0) of the next unit
+                    // is the ring item after this unit's last V; the two slots released above let it load.
+                    if (p.pre_issue && j + 2 == w.nkv && w.n1 == w.n0 + 1) {
+                        int un = u + gridDim.x;
+                        while (un < p.total_units && !decode_unit(p, un).valid) un += gridDim.x;
+                        if (un < p.total_units) {
+                            const int qbn = (unit_iter + 1) & 1;
+                            ptx::mbar_wait(&bar->q_full[qbn], ((unit_iter + 1) >> 1) & 1);
+                            ptx::tc_fence_after();
+                            const uint32_t kn0 = wait_item(item + 2 * w.nkv);
+                            issue_s_at(0, q_base + qbn * 2 * kTileBytes, kn0);
+                            ptx::mma_commit(&bar->s_full[0]);
+                            next_pre = true;
+                        }
+                    }
                 }
                 item += 2 * w.nkv;
                 ++unit_iter;
+                s0_pre = next_pre;
             }
         }
     } else if (warp >= kEpiWarp0) {
@@ -551,6 +574,12 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     prm.tiles_max = static_cast<int>(tiles);
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.o = static_cast<__nv_bfloat16*>(o);
+    static int pre = -1;
+    if (pre < 0) {
+        const char* e = getenv("QVK_ATTN_PRE");
+        pre = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    prm.pre_issue = pre;
     const int64_t units = static_cast<int64_t>((prm.tiles_max + 1) / 2) * g->n_groups * n_q;
     if (units > 0x7fffffff) QVK_INVALID("attention: too many work units");
     prm.total_units = static_cast<int>(units);

@@ -12,6 +12,22 @@ namespace qvk {
 thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {
+    static bool pooled[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64 && !pooled[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pooled[dev] = true;
+    }
+    return cudaMallocAsync(p, bytes, stream);
+}
+
 int launch_score(cudaStream_t, const qvk_groups*, int64_t, const void*, const void*, int, int, int, int,
                  const float*, int64_t, int, double*);
 int launch_select(cudaStream_t, const qvk_groups*, const double*, int, uint32_t*);
@@ -206,7 +222,7 @@ int qvk_select_gather(qvk_stream_t s, const qvk_groups* g, const double* scores,
     if (prune_fused_supported(g, dtype, width, k, v, kc, vc))
         return launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores, nullptr, idx, kc, vc, origin, 0);
     uint32_t* ix = idx;
-    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+    if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
                                             sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
     int rc = launch_select(s, g, scores, heads, ix);
     if (rc == QVK_OK) rc = launch_gather(s, g, k, v, dtype, heads, width, ix, kc, vc, origin, 0);
@@ -230,9 +246,9 @@ int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v,
     }
     double* sc = scores_ws;
     uint32_t* ix = idx_ws;
-    if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
+    if (!sc) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&sc),
                                             sizeof(double) * std::max<int64_t>(1, g->total_tokens * heads), s));
-    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+    if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
                                             sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
     int rc = qvk_score(s, g, k, v, dtype, heads, width, scorer, tq, text_count, n_h, sc);
     if (rc == QVK_OK) rc = qvk_select(s, g, sc, heads, ix);
@@ -266,9 +282,9 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
                                   1);
     double* sc = scores_ws;
     uint32_t* ix = idx_ws;
-    if (!sc) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sc),
+    if (!sc) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&sc),
                                             sizeof(double) * std::max<int64_t>(1, g->total_tokens * heads), s));
-    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+    if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
                                             sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
     int rc;
     if (p->scorer == QVK_SNAPKV) {
@@ -314,7 +330,7 @@ int qvk_prefill_layer_x(qvk_stream_t s, const qvk_groups* g, const qvk_layer_par
         return launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores_ws, nullptr, idx_ws, kc, vc, origin,
                                   1);
     uint32_t* ix = idx_ws;
-    if (!ix) QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&ix),
+    if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
                                             sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
     int rc = launch_select(s, g, scores_ws, heads, ix);
     if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, 0);

@@ -15,6 +15,11 @@ namespace qvk {
 // Thread-local error text returned by qvk_last_error() (capi.cu).
 void set_error(const std::string& msg);
 
+// Stream-ordered scratch allocation (cudaMallocAsync) from the device's default memory pool, whose release threshold
+// is raised once per device so freed scratch stays pooled across stream synchronisations (with the default
+// threshold of 0 every synchronise returns it to the driver and the next call pays a real allocation, ~0.4 ms).
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
+
 constexpr int kNumSms = 148;
 
 // Order-preserving map of a double score onto uint64: larger score <=> larger key.  -0.0 is canonicalised to +0.0

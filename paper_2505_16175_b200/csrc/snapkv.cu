@@ -318,13 +318,16 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                         for (int c = 0; c < 128; ++c)
                             if (j0 + c > my_pos) x[c] = -INFINITY;
                     }
-                    float mx = x[0];
+                    // four independent max / sum chains (the serial FMNMX / FADD chains were latency-bound)
+                    float mx4[4] = {x[0], x[1], x[2], x[3]};
 #pragma unroll
-                    for (int c = 1; c < 128; ++c) mx = fmaxf(mx, x[c]);
+                    for (int c = 4; c < 128; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], x[c]);
+                    const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
                     const float mn = fmaxf(m, mx * sl2);
-                    float sum = 0.f;
+                    float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int c = 0; c < 128; ++c) sum += ptx::ex2(fmaf(x[c], sl2, -mn));
+                    for (int c = 0; c < 128; ++c) s4[c & 3] += ptx::ex2(fmaf(x[c], sl2, -mn));
+                    const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     l = (m == -INFINITY ? 0.f : l * ptx::ex2(m - mn)) + sum;
                     m = mn;
                 }
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 ptx::tc_fence_after();
                 const int j = jt * 128 + i;
                 const bool edge = jt * 128 + 127 > n - p.window;  // some window rows precede some keys
-                float acc = 0.f;
+                float a4[4] = {0.f, 0.f, 0.f, 0.f};
                 for (int ch = c_lo; ch < c_hi; ++ch) {
                     float x[32];
                     QVK_TMEM_LD32F(tmem + lane_off + 256 + 32 * ch, x);
@@ -348,9 +351,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                         const int c = 32 * ch + e;
                         float y = fmaf(x[e], sl2, -sh->bias[c]);
                         if (edge && j > sh->pos[c]) y = -INFINITY;
-                        acc += ptx::ex2(y);
+                        a4[e & 3] += ptx::ex2(y);
                     }
                 }
+                const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&sh->acc_empty);
                 if (set) sh->part[jt & 1][i] = acc;
@@ -403,7 +407,7 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
     float2* stats = nullptr;
     float* raw = nullptr;
     const int64_t total = g->total_tokens * n_kv;
-    QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
+    QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
     const int gq = n_q / n_kv;
     if (gq * window <= 256 && window <= 256 && !getenv("QVK_SNAPKV_SIMT")) {
         CUtensorMap mq, mk;
@@ -436,7 +440,7 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         snapkv_tc_kernel<<<grid, kSnapThreads, kSnapSmem, stream>>>(mq, mk, sp);
         QVK_LAUNCH_CHECK();
     } else {
-    QVK_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&stats),
+    QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&stats),
                                    sizeof(float2) * g->n_groups * n_q * static_cast<size_t>(window), stream));
     snap_stats_kernel<<<dim3(g->n_groups, n_q), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k), g->tok_off_d, n_q, n_kv, window,

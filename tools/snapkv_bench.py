@@ -1,0 +1,34 @@
+#!/usr/bin/env python
+"""SnapKV scorer microbenchmark (GPU): qvk_snapkv_score on the C3 shape (64 groups x 1024 tokens, 28 / 4 heads,
+window 32) and C3b (64 x 4096), CUDA-event timed per launch after an L2 flush; one JSON line per shape."""
+import json
+import statistics
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2505_16175_b200 as qp  # noqa: E402
+
+dev = torch.device("cuda:0")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+for G, N in ((64, 1024), (64, 4096)):
+    plan = qp.GroupPlan.from_sizes([N] * G, 0.25)
+    g = plan.to(dev)
+    q = torch.randn(G * N, 28, 128, device=dev).to(torch.bfloat16)
+    k = torch.randn(G * N, 4, 128, device=dev).to(torch.bfloat16)
+    sc = torch.empty(G * N * 4, dtype=torch.float64, device=dev)
+    qp.snapkv_scores(q, k, g, 28, 4, 32, out=sc)
+    ts = []
+    for _ in range(20):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        qp.snapkv_scores(q, k, g, 28, 4, 32, out=sc)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    byt = G * N * 4 * 128 * 2 + G * 32 * 28 * 128 * 2 + G * N * 4 * 8
+    print(json.dumps({"groups": G, "tokens": N, "ms": ms, "bytes": byt, "gbs": byt / ms / 1e6}), flush=True)
