@@ -322,41 +322,66 @@ def main():
         del x, wqkv, qkv
 
     # ---- e2e through the C ABI with host buffers (H2D of this step's Q/K/V, D2H of the pruned cache) ----
-    e2e = None
+    e2e = e2e_qkv = None
     if not args.no_e2e:
-        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
         out_k = torch.empty(buf.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
         out_v = torch.empty_like(out_k).pin_memory()
         out_o = torch.empty(buf.origin.numel(), dtype=torch.int64).pin_memory()
-        # public host-buffer API: group-chunked, copies overlapped with the kernels (paper_2505_16175_b200/pipeline.py)
+
+        def timed_steps(fn):
+            for _ in range(max(1, args.warmup)):
+                fn()
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.item()
+
+        d2h = sum(x.numel() * x.element_size() for x in (out_k, out_v, out_o))
+        # (1) the user's call from video frames (the reference's prefill(model, tokenize(frames), prune) scope):
+        #     pinned host uint8 frames -> GPU tokenizer -> QKV projection (key-norm fused) -> attention -> select +
+        #     gather -> pruned cache back to pinned host, per 4-group chunk with both copies overlapped
+        side = 28 * int(round(math.sqrt(c["tokens_per_frame"])))  # 448 x 448 frames: 16 x 16 patches of 28 px
+        n_frames = local_plan.total_tokens // c["tokens_per_frame"]
+        hframes = torch.randint(0, 256, (n_frames, 3, side, side), dtype=torch.uint8,
+                                generator=torch.Generator().manual_seed(rank)).pin_memory()
+        d_model = n_q * d
+        embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(11)) * 2 - 1) / 255).to(dev)
+        wqkv = (qp.synth_bf16(1, 8, 0, 0, (n_q + 2 * n_kv) * d, 1, d_model, False, dev).float()
+                * (1.0 / math.sqrt(d_model))).to(torch.bfloat16).view(-1, d_model)
+        fp = qp.FramePrefill(local_plan, c["tokens_per_frame"], side, side, embed, wqkv, n_q, n_kv, d, rho, dev,
+                             chunks=8, cache_rows=plan.total_rows, row_base=row_base)
+        gather_f = (lambda: allgather_cache([fp.k_cache, fp.v_cache, fp.origin], bounds, [unit, unit, n_kv])) \
+            if world > 1 else None
+        t_f = timed_steps(lambda: fp.run(hframes, out_k, out_v, out_o, after_compute=gather_f))
+        e2e = {"value": total_tokens * args.steps / (t_f / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": hframes.numel() * hframes.element_size(), "d2h_bytes_per_step": d2h,
+               "path": "FramePrefill (public API, pipeline.py): pinned host video frames (%d x 3 x %d x %d uint8) -> "
+                       "qvk_tokenize_bf16 -> qvk_prefill_layer_x (QKV projection GEMM with fused key-norm, attention, "
+                       "select+gather) -> pruned cache to pinned host; 8 group chunks, copies on two streams "
+                       "overlapped with the kernels" % (n_frames, side, side),
+               "includes": "frames upload, tokenizer, projection GEMM (not in `value`), attention, prune, readback"}
+        del fp, hframes, wqkv, embed
+        # (2) the same step from host Q/K/V (the `value` step's inputs in pinned host memory; PCIe-bound)
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
         hp = qp.HostPrefill(local_plan, n_q, n_kv, d, rho, dev, chunks=4, cache_rows=plan.total_rows,
                             row_base=row_base)
         gather = (lambda: allgather_cache([hp.k_cache, hp.v_cache, hp.origin], bounds, [unit, unit, n_kv])) \
             if world > 1 else None
-
-        def e2e_step():
-            hp.run(hq, hk, hv, out_k, out_v, out_o, after_compute=gather)
-
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = ev(), ev()
-        e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        h2d = sum(x.numel() * x.element_size() for x in (hq, hk, hv))
-        d2h = sum(x.numel() * x.element_size() for x in (out_k, out_v, out_o))
-        e2e = {"value": total_tokens * args.steps / (t.item() / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "HostPrefill: qvk_prefill_layer (C ABI) per 4-group chunk, pinned host Q/K/V in and pruned "
-                       "cache out on two copy streams overlapped with the kernels"}
+        t_q = timed_steps(lambda: hp.run(hq, hk, hv, out_k, out_v, out_o, after_compute=gather))
+        e2e_qkv = {"value": total_tokens * args.steps / (t_q / 1e3), "unit": "tokens/s",
+                   "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in (hq, hk, hv)),
+                   "d2h_bytes_per_step": d2h,
+                   "path": "HostPrefill: qvk_prefill_layer (C ABI) per 4-group chunk, pinned host Q/K/V in and pruned "
+                           "cache out on two copy streams overlapped with the kernels"}
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
     fl = flops_attention(sizes, n_q, d)
@@ -390,7 +415,8 @@ def main():
             "secondary": {"kernels": "prune_fused_kernel: score+select+gather in one cluster launch (qvk_prune)", "avg_ms": prune_avg,
                           "algorithmic_bytes": pb, "achieved_gbs": pb / (prune_avg / 1e3) / 1e9,
                           "hbm_peak_gbs": hbm, "frac": pb / (prune_avg / 1e3) / 1e9 / hbm, "traffic": traffic_p},
-            "clocks": clocks, "e2e": e2e, "gpu_launches": 2 * args.steps, "full_layer": full,
+            "clocks": clocks, "e2e": e2e, "e2e_qkv": e2e_qkv, "gpu_launches": 2 * args.steps,
+            "full_layer": full,
         }
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1

@@ -193,6 +193,9 @@ int qvk_project_exact(qvk_stream_t stream, const float* x_d, int64_t rows, int32
  * the patch grid" on a bad size. */
 int qvk_tokenize(qvk_stream_t stream, const uint8_t* frames_d, int64_t n_frames, uint32_t width, uint32_t height,
                  uint32_t tokens_per_frame, const float* embed_d, int32_t d_model, float* tokens_d);
+/* Same tokens rounded to bf16 (RNE): the activations X of qvk_project_qkv (video frames -> pruned cache). */
+int qvk_tokenize_bf16(qvk_stream_t stream, const uint8_t* frames_d, int64_t n_frames, uint32_t width, uint32_t height,
+                      uint32_t tokens_per_frame, const float* embed_d, int32_t d_model, void* tokens_d);
 /* prefill.cpp:116-121 */
 void qvk_patch_grid(uint32_t tokens_per_frame, uint32_t* rows, uint32_t* cols);
 

@@ -29,9 +29,10 @@ from .prefill import (  # noqa: F401
     select_gather,
     snapkv_scores,
     synth_bf16,
+    tokenize,
     top_k_indices,
 )
 
-from .pipeline import HostPrefill  # noqa: F401,E402
+from .pipeline import FramePrefill, HostPrefill  # noqa: F401,E402
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -76,6 +76,7 @@ _SIGS = {
     "qvk_seeded_matrix": (C.c_int, [P, U64, U32, U32, SZ, F64, P]),
     "qvk_project_exact": (C.c_int, [P, P, I64, I32, P, I32, P]),
     "qvk_tokenize": (C.c_int, [P, P, I64, U32, U32, U32, P, I32, P]),
+    "qvk_tokenize_bf16": (C.c_int, [P, P, I64, U32, U32, U32, P, I32, P]),
     "qvk_patch_grid": (None, [U32, C.POINTER(U32), C.POINTER(U32)]),
     "qvk_synth_bf16": (C.c_int, [P, U64, U32, U32, U64, I64, I32, I32, I32, P]),
 }

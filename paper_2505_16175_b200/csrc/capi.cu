@@ -40,7 +40,7 @@ int launch_snapkv(cudaStream_t, const qvk_groups*, const void*, const void*, int
 int launch_seeded_matrix(cudaStream_t, uint64_t, uint32_t, uint32_t, size_t, double, float*);
 int launch_project_exact(cudaStream_t, const float*, int64_t, int, const float*, int, float*);
 int launch_tokenize(cudaStream_t, const uint8_t*, int64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
-                    const float*, int, float*);
+                    const float*, int, void*, int);
 int launch_synth_bf16(cudaStream_t, uint64_t, uint32_t, uint32_t, uint64_t, int64_t, int, int, int, void*);
 int launch_project_qkv(cudaStream_t, const void*, int64_t, int, const void*, int, int, int, void*, void*, void*,
                        const qvk_groups*, double*);
@@ -380,7 +380,17 @@ int qvk_tokenize(qvk_stream_t s, const uint8_t* frames, int64_t n_frames, uint32
     qvk_patch_grid(tpf, &gr, &gc);
     if (height % gr != 0 || width % gc != 0)  // prefill.cpp:128-129
         QVK_INVALID("tokenize: frame size not divisible into the patch grid");
-    return launch_tokenize(s, frames, n_frames, width, height, tpf, gr, gc, embed, d_model, tokens);
+    return launch_tokenize(s, frames, n_frames, width, height, tpf, gr, gc, embed, d_model, tokens, 0);
+}
+
+int qvk_tokenize_bf16(qvk_stream_t s, const uint8_t* frames, int64_t n_frames, uint32_t width, uint32_t height,
+                      uint32_t tpf, const float* embed, int32_t d_model, void* tokens) {
+    if (tpf == 0 || d_model <= 0) QVK_INVALID("model config: dimensions must be positive");
+    uint32_t gr, gc;
+    qvk_patch_grid(tpf, &gr, &gc);
+    if (height % gr != 0 || width % gc != 0)  // prefill.cpp:128-129
+        QVK_INVALID("tokenize: frame size not divisible into the patch grid");
+    return launch_tokenize(s, frames, n_frames, width, height, tpf, gr, gc, embed, d_model, tokens, 1);
 }
 
 int qvk_synth_bf16(qvk_stream_t s, uint64_t seed, uint32_t tag, uint32_t layer, uint64_t group, int64_t rows,

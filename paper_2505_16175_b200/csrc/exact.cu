@@ -52,10 +52,13 @@ __global__ void __launch_bounds__(kPT * kPR) project_exact_kernel(const float* _
 // One CTA per token (frame slot f, patch gr, gc).  Integer channel sums are exact in any order (the reference
 // accumulates uint8 into a double, exact below 2^53), then mean = sum / (double(ph) * pw) and
 // out[o] = float(e0*m0 + e1*m1 + e2*m2) evaluated left to right in double.
+// OutT float: the reference's fp32 tokens bit for bit; __nv_bfloat16: the same fp32 value rounded to bf16 (RNE), the
+// activations of the bf16 projection GEMM (frames -> pruned cache path, pipeline.py FramePrefill).
+template <typename OutT>
 __global__ void __launch_bounds__(256) tokenize_kernel(const uint8_t* __restrict__ frames, uint32_t width,
                                                        uint32_t height, uint32_t tpf, uint32_t grid_cols,
                                                        uint32_t ph, uint32_t pw, const float* __restrict__ embed,
-                                                       int d, float* __restrict__ tokens) {
+                                                       int d, OutT* __restrict__ tokens) {
     __shared__ unsigned long long sums[3];
     __shared__ double mean[3];
     const int64_t token = blockIdx.x;
@@ -82,7 +85,71 @@ __global__ void __launch_bounds__(256) tokenize_kernel(const uint8_t* __restrict
     for (int o = threadIdx.x; o < d; o += blockDim.x) {
         const double e0 = embed[o * 3 + 0], e1 = embed[o * 3 + 1], e2 = embed[o * 3 + 2];
         const double s = __dadd_rn(__dadd_rn(__dmul_rn(e0, mean[0]), __dmul_rn(e1, mean[1])), __dmul_rn(e2, mean[2]));
-        tokens[token * d + o] = __double2float_rn(s);
+        const float f = __double2float_rn(s);
+        if constexpr (sizeof(OutT) == 4) tokens[token * d + o] = f;
+        else tokens[token * d + o] = __float2bfloat16_rn(f);
+    }
+}
+
+// Throughput variant of the same tokenizer (identical values): a CTA takes kTokCta consecutive tokens (patches) of one
+// frame.  Patch sums: 4 threads per patch, 4 bytes per load (__dp4a), exact integer sums reduced by shuffles, then
+// the reference's double mean.  Embed: each thread owns the outputs o = tid (mod 256) and converts their 3 embed
+// weights to double ONCE for all kTokCta tokens (the per-token kernel above reconverts them for every token), then
+// writes o for every token of the CTA (coalesced across the warp).
+constexpr int kTokCta = 64;
+template <typename OutT>
+__global__ void __launch_bounds__(256) tokenize_fast_kernel(const uint8_t* __restrict__ frames, uint32_t width,
+                                                            uint32_t height, uint32_t tpf, uint32_t grid_cols,
+                                                            uint32_t ph, uint32_t pw, const float* __restrict__ embed,
+                                                            int d, OutT* __restrict__ tokens) {
+    __shared__ double mean[kTokCta][3];
+    const int64_t f = blockIdx.x;
+    const uint32_t p0 = blockIdx.y * kTokCta;
+    const uint32_t np = min(static_cast<uint32_t>(kTokCta), tpf - p0);
+    const size_t plane = static_cast<size_t>(width) * height;
+    const uint8_t* px = frames + f * 3 * plane;
+    {
+        const uint32_t pl = threadIdx.x >> 2, part = threadIdx.x & 3;
+        uint32_t acc[3] = {0u, 0u, 0u};
+        if (pl < np) {
+            const uint32_t p = p0 + pl, gr = p / grid_cols, gc = p % grid_cols;
+            const bool vec = (pw % 4 == 0) && (width % 4 == 0);
+            for (uint32_t y = part; y < ph; y += 4) {
+                const size_t row = static_cast<size_t>(gr * ph + y) * width + gc * pw;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const uint8_t* r = px + c * plane + row;
+                    if (vec) {
+                        for (uint32_t x = 0; x < pw; x += 4)
+                            acc[c] = __dp4a(*reinterpret_cast<const uint32_t*>(r + x), 0x01010101u, acc[c]);
+                    } else {
+                        for (uint32_t x = 0; x < pw; ++x) acc[c] += r[x];
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
+            acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
+        }
+        if (pl < np && part == 0) {
+            const double cnt = __dmul_rn(static_cast<double>(ph), static_cast<double>(pw));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) mean[pl][c] = __ddiv_rn(static_cast<double>(acc[c]), cnt);
+        }
+    }
+    __syncthreads();
+    OutT* out = tokens + (f * tpf + p0) * static_cast<int64_t>(d);
+    for (int o = threadIdx.x; o < d; o += blockDim.x) {
+        const double e0 = embed[o * 3 + 0], e1 = embed[o * 3 + 1], e2 = embed[o * 3 + 2];
+        for (uint32_t t = 0; t < np; ++t) {
+            const double s =
+                __dadd_rn(__dadd_rn(__dmul_rn(e0, mean[t][0]), __dmul_rn(e1, mean[t][1])), __dmul_rn(e2, mean[t][2]));
+            const float v = __double2float_rn(s);
+            if constexpr (sizeof(OutT) == 4) out[t * static_cast<int64_t>(d) + o] = v;
+            else out[t * static_cast<int64_t>(d) + o] = __float2bfloat16_rn(v);
+        }
     }
 }
 
@@ -134,13 +201,27 @@ int launch_project_exact(cudaStream_t s, const float* x, int64_t rows, int d_in,
 }
 
 int launch_tokenize(cudaStream_t s, const uint8_t* frames, int64_t n_frames, uint32_t width, uint32_t height,
-                    uint32_t tpf, uint32_t grid_rows, uint32_t grid_cols, const float* embed, int d, float* tokens) {
+                    uint32_t tpf, uint32_t grid_rows, uint32_t grid_cols, const float* embed, int d, void* tokens,
+                    int bf16_out) {
     const int64_t n_tok = n_frames * tpf;
     if (n_tok == 0) return QVK_OK;
     if (n_tok > 0x7fffffff) QVK_INVALID("tokenize: too many tokens for one launch");
-    tokenize_kernel<<<static_cast<unsigned>(n_tok), 256, 0, s>>>(frames, width, height, tpf, grid_cols,
-                                                                  height / grid_rows, width / grid_cols, embed, d,
-                                                                  tokens);
+    const uint32_t ph = height / grid_rows, pw = width / grid_cols;
+    if (n_frames <= 0x7fffffff && ph * pw <= (1u << 24)) {  // u32 patch sums: at most 2^24 pixels of <= 255
+        const dim3 grid(static_cast<unsigned>(n_frames), (tpf + kTokCta - 1) / kTokCta);
+        if (bf16_out)
+            tokenize_fast_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(frames, width, height, tpf, grid_cols, ph, pw,
+                                                                     embed, d, static_cast<__nv_bfloat16*>(tokens));
+        else
+            tokenize_fast_kernel<float><<<grid, 256, 0, s>>>(frames, width, height, tpf, grid_cols, ph, pw, embed, d,
+                                                             static_cast<float*>(tokens));
+    } else if (bf16_out) {
+        tokenize_kernel<__nv_bfloat16><<<static_cast<unsigned>(n_tok), 256, 0, s>>>(
+            frames, width, height, tpf, grid_cols, ph, pw, embed, d, static_cast<__nv_bfloat16*>(tokens));
+    } else {
+        tokenize_kernel<float><<<static_cast<unsigned>(n_tok), 256, 0, s>>>(
+            frames, width, height, tpf, grid_cols, ph, pw, embed, d, static_cast<float*>(tokens));
+    }
     QVK_LAUNCH_CHECK();
     return QVK_OK;
 }

@@ -106,3 +106,110 @@ class HostPrefill:
         done_h2d = torch.cuda.Event()
         done_h2d.record(self.h2d)
         main.wait_event(done_h2d)
+
+
+class FramePrefill:
+    """Video frames in host memory -> one layer's pruned KV cache: the end-to-end path of the reference's
+    `prefill(model, tokenize(frames), prune)` (prefill.hpp:86-87, 137-138; prefill.cpp:170-183, 293-323) on the GPU.
+
+    Per chunk of groups (contiguous frames): pinned host frames -> HBM on a copy stream; GPU tokenizer (bf16 tokens,
+    qvk_tokenize_bf16); QKV projection with the key-norm fused (qvk_project_qkv); attention; fused select + gather
+    (qvk_prefill_layer_x); the chunk's pruned cache rows -> pinned host on a second copy stream.  Chunk c+1's frames
+    upload and chunk c-1's cache readback overlap chunk c's kernels.  Frames are (F, 3, H, W) uint8 (decode.hpp:27-55
+    FrameBuffer slots), H and W divisible by the patch grid of tokens_per_frame (prefill.cpp:116-121)."""
+
+    def __init__(self, plan: GroupPlan, tokens_per_frame: int, height: int, width: int, embed, w_qkv, n_q: int,
+                 n_kv: int, d_h: int, rho: float, device, chunks: int = 4, cache_rows: int | None = None,
+                 row_base: int = 0):
+        self.plan, self.tpf, self.n_q, self.n_kv, self.d, self.rho = plan, tokens_per_frame, n_q, n_kv, d_h, rho
+        self.dev = torch.device(device)
+        self.embed, self.w = embed, w_qkv
+        self.d_model = int(embed.shape[0])
+        G = plan.n_groups
+        chunks = max(1, min(chunks, G))
+        bounds = np.linspace(0, G, chunks + 1).round().astype(int)
+        self.parts = []
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            if b <= a:
+                continue
+            t0, r0 = int(plan.tok_off[a]), int(plan.row_off[a])
+            sub = GroupPlan((plan.tok_off[a:b + 1] - t0).astype(np.int64), plan.keep[a:b].copy(),
+                            (plan.row_off[a:b + 1] - r0).astype(np.int64), plan.first_token[a:b].copy())
+            self.parts.append((t0, int(plan.tok_off[b]), r0, int(plan.row_off[b]), sub.to(self.dev)))
+        T, R = plan.total_tokens, plan.total_rows
+        if T % tokens_per_frame:
+            raise ValueError("plan tokens are not whole frames")
+        bf = torch.bfloat16
+        self.frames = torch.empty(T // tokens_per_frame, 3, height, width, dtype=torch.uint8, device=self.dev)
+        self.x = torch.empty(T, self.d_model, dtype=bf, device=self.dev)
+        self.q = torch.empty(T, n_q, d_h, dtype=bf, device=self.dev)
+        self.k = torch.empty(T, n_kv, d_h, dtype=bf, device=self.dev)
+        self.v = torch.empty(T, n_kv, d_h, dtype=bf, device=self.dev)
+        self.o = torch.empty(T, n_q, d_h, dtype=bf, device=self.dev)
+        self.scores = torch.empty(max(1, T * n_kv), dtype=torch.float64, device=self.dev)
+        self.idx = torch.empty(max(1, R * n_kv), dtype=torch.int32, device=self.dev)
+        rows = R if cache_rows is None else cache_rows
+        self.k_cache = torch.empty(rows * n_kv * d_h, dtype=bf, device=self.dev)
+        self.v_cache = torch.empty_like(self.k_cache)
+        self.origin = torch.empty(rows * n_kv, dtype=torch.int64, device=self.dev)
+        self.row_base = row_base
+        self.prm = L.QvkLayerParams(n_q, n_kv, d_h, int(Scorer.key_norm_small), 1, rho, 1.0 / math.sqrt(d_h), 32, 1)
+        self.h2d = torch.cuda.Stream(self.dev)
+        self.d2h = torch.cuda.Stream(self.dev)
+
+    def _layer(self, part, stream):
+        t0, t1, r0, r1, g = part
+        f0, f1 = t0 // self.tpf, t1 // self.tpf
+        fr = self.frames[f0:f1]
+        check(lib.qvk_tokenize_bf16(stream.cuda_stream, fr.data_ptr(), f1 - f0, fr.shape[3], fr.shape[2], self.tpf,
+                                    self.embed.data_ptr(), self.d_model, self.x[t0:t1].data_ptr()))
+        unit = self.n_kv * self.d
+        cr = self.row_base + r0
+        check(lib.qvk_prefill_layer_x(stream.cuda_stream, g.ref, C.byref(self.prm), self.x[t0:t1].data_ptr(),
+                                      self.d_model, self.w.data_ptr(), self.q[t0:t1].data_ptr(),
+                                      self.k[t0:t1].data_ptr(), self.v[t0:t1].data_ptr(), self.o[t0:t1].data_ptr(),
+                                      self.scores[t0 * self.n_kv:].data_ptr(), self.idx[r0 * self.n_kv:].data_ptr(),
+                                      self.k_cache[cr * unit:].data_ptr(), self.v_cache[cr * unit:].data_ptr(),
+                                      self.origin[cr * self.n_kv:].data_ptr()))
+
+    def run(self, hframes, out_k=None, out_v=None, out_o=None, after_compute=None):
+        """One layer from pinned host frames (F, 3, H, W) uint8 into the device cache (and optional pinned host
+        outputs, per chunk — or the whole cache after `after_compute`, e.g. the multi-GPU all-gather)."""
+        main = torch.cuda.current_stream(self.dev)
+        start = torch.cuda.Event()
+        start.record(main)
+        self.h2d.wait_event(start)
+        self.d2h.wait_event(start)
+        unit = self.n_kv * self.d
+        per_chunk_out = out_k is not None and after_compute is None
+        for part in self.parts:
+            t0, t1, r0, r1, _ = part
+            f0, f1 = t0 // self.tpf, t1 // self.tpf
+            e_in = torch.cuda.Event()
+            with torch.cuda.stream(self.h2d):
+                self.frames[f0:f1].copy_(hframes[f0:f1], non_blocking=True)
+                e_in.record(self.h2d)
+            main.wait_event(e_in)
+            self._layer(part, main)
+            if per_chunk_out:
+                e_out = torch.cuda.Event()
+                e_out.record(main)
+                self.d2h.wait_event(e_out)
+                a, b = self.row_base + r0, self.row_base + r1
+                with torch.cuda.stream(self.d2h):
+                    out_k[a * unit:b * unit].copy_(self.k_cache[a * unit:b * unit], non_blocking=True)
+                    out_v[a * unit:b * unit].copy_(self.v_cache[a * unit:b * unit], non_blocking=True)
+                    out_o[a * self.n_kv:b * self.n_kv].copy_(self.origin[a * self.n_kv:b * self.n_kv],
+                                                             non_blocking=True)
+        if after_compute is not None:
+            after_compute()
+            if out_k is not None:
+                out_k.copy_(self.k_cache, non_blocking=True)
+                out_v.copy_(self.v_cache, non_blocking=True)
+                out_o.copy_(self.origin, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self.d2h)
+        main.wait_event(done)
+        done_h2d = torch.cuda.Event()
+        done_h2d.record(self.h2d)
+        main.wait_event(done_h2d)

@@ -347,6 +347,19 @@ def decode_attention(q, k_cache, v_cache, n_q: int, n_kv: int, scale: float | No
     return (out, lse) if with_lse else out
 
 
+def tokenize(frames, tokens_per_frame: int, embed, bf16: bool = False, out=None):
+    """Stand-in tokenizer on the GPU (prefill.cpp:116-168): frames (F, 3, H, W) uint8, embed (d_model, 3) fp32 ->
+    tokens (F * tpf, d_model), fp32 bit-identical to the reference, or those values rounded to bf16."""
+    F, _, H, W = frames.shape
+    d_model = embed.shape[0]
+    out = out if out is not None else torch.empty(F * tokens_per_frame, d_model,
+                                                  dtype=torch.bfloat16 if bf16 else torch.float32,
+                                                  device=frames.device)
+    fn = lib.qvk_tokenize_bf16 if bf16 else lib.qvk_tokenize
+    check(fn(_stream(), _ptr(frames), F, W, H, tokens_per_frame, _ptr(embed), d_model, _ptr(out)))
+    return out
+
+
 def synth_bf16(seed: int, tag: int, layer: int, group: int, rows: int, heads: int, width: int,
                head_scale: bool, device="cuda") -> torch.Tensor:
     """Synthetic activations generated in HBM (same bits as oracle qvo_synth_bf16)."""

@@ -528,3 +528,44 @@ def test_decode_attention_vs_torch(cuda, n_tq, rows, n_q, n_kv):
     check_tol(o, ref, "decode O")
     lse_ref = torch.logsumexp(s, -1).t()
     assert (lse - lse_ref).abs().max().item() <= 1e-3
+
+
+# ------------------------------------------------------------------------------------------------ frames -> pruned cache
+def _frames(F, H, W, device, seed=3):
+    gen = torch.Generator().manual_seed(seed)
+    return torch.randint(0, 256, (F, 3, H, W), generator=gen, dtype=torch.uint8).to(device)
+
+
+def test_tokenize_bf16_is_rounded_reference_tokens(cuda):
+    """GPU stand-in tokenizer: the bf16 variant is exactly the fp32 reference tokens rounded to nearest even."""
+    fr = _frames(4, 60, 64, cuda)  # tpf 48: 6 x 8 patch grid
+    embed = ((torch.rand(256, 3, generator=torch.Generator().manual_seed(1)) * 2 - 1) / 255).to(cuda)
+    t32 = qp.tokenize(fr, 48, embed)
+    t16 = qp.tokenize(fr, 48, embed, bf16=True)
+    assert torch.equal(t16, t32.to(torch.bfloat16))
+
+
+def test_frame_prefill_matches_device_layer(cuda):
+    """FramePrefill (host frames -> chunked upload, tokenize, projection, attention, prune, readback) == the same
+    kernels on device-resident data in one call, bit for bit."""
+    F, fpg, tpf, H, W = 24, 4, 64, 64, 64
+    n_q, n_kv, d_h, d_model, rho = 8, 2, 128, 512, 0.5
+    plan = qp.GroupPlan.plan(F, fpg, tpf, rho, 1)
+    g = plan.to(cuda)
+    fr = _frames(F, H, W, cuda)
+    embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(2)) * 2 - 1) / 255).to(cuda)
+    w = (torch.randn((n_q + 2 * n_kv) * d_h, d_model, generator=torch.Generator().manual_seed(4)) /
+         math.sqrt(d_model)).to(torch.bfloat16).to(cuda)
+    x = qp.tokenize(fr, tpf, embed, bf16=True)
+    buf, _ = qp.prefill_layer_x(x, w, g, n_q, n_kv, d_h, rho)
+    fp = qp.FramePrefill(plan, tpf, H, W, embed, w, n_q, n_kv, d_h, rho, cuda, chunks=3)
+    hf = fr.cpu().pin_memory()
+    out_k = torch.empty(fp.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+    out_v = torch.empty_like(out_k).pin_memory()
+    out_o = torch.empty(fp.origin.numel(), dtype=torch.int64).pin_memory()
+    for _ in range(2):
+        fp.run(hf, out_k, out_v, out_o)
+    torch.cuda.synchronize()
+    assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
+    assert torch.equal(out_o, buf.origin.cpu())
+    assert torch.equal(fp.o, buf.o)
