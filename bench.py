@@ -188,10 +188,19 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook (not used by the driver): QVK_BENCH_SHARE_GPU=1 runs every rank on the visible GPU(s) round-robin
+    # over gloo, so the multi-rank path (sharding, cache all-gather, max-over-ranks timing) can be exercised on a
+    # 1-GPU box; NCCL refuses two ranks on one device.
+    share = os.environ.get("QVK_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2505_16175_b200.distributed import allgather_cache, segment_bounds
 
     c = CFG
