@@ -282,6 +282,40 @@ def main():
     total_tokens = plan.total_tokens
     value = total_tokens * args.steps / (elapsed_ms / 1e3)
 
+    # ---- N > 1: the same step with the all-gather fused into the compaction (PeerCache: every rank's prune kernel
+    #      stores its retained rows into all ranks' caches over NVLink peer memory; one barrier per step) ----
+    fused_ag = None
+    if world > 1:
+        try:
+            from paper_2505_16175_b200.distributed import PeerCache
+
+            peers = PeerCache([buf.k_cache, buf.v_cache, buf.origin])
+
+            def fused_step():
+                qp.prefill_layer_dests(q, k, v, g, n_q, n_kv, rho, peers, buf, cache_row_offset=row_base)
+                peers.fence(dev)
+
+            for _ in range(args.warmup):
+                fused_step()
+            dist.barrier()
+            torch.cuda.synchronize()
+            f0, f1 = ev(), ev()
+            f0.record(stream)
+            for _ in range(args.steps):
+                fused_step()
+            f1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([f0.elapsed_time(f1)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            fused_ag = {"value": plan.total_tokens * args.steps / (t.item() / 1e3), "unit": "tokens/s",
+                        "ms_per_step": t.item() / args.steps,
+                        "path": "qvk_prefill_layer_dests: attention + fused prune whose compaction stores every "
+                                "retained row into all %d ranks' caches (CUDA IPC peer pointers over NVLink), then one "
+                                "cross-rank barrier; no separate all-gather" % world}
+            peers.close()
+        except Exception as e:  # noqa: BLE001 — reported, never fatal for the bench line
+            fused_ag = {"error": repr(e)[:300]}
+
     # ---- the same layer from hidden states: QKV projection GEMM (key-norm fused) -> attention -> select+gather ----
     full = None
     if not args.no_full_layer:
@@ -425,7 +459,7 @@ def main():
                           "algorithmic_bytes": pb, "achieved_gbs": pb / (prune_avg / 1e3) / 1e9,
                           "hbm_peak_gbs": hbm, "frac": pb / (prune_avg / 1e3) / 1e9 / hbm, "traffic": traffic_p},
             "clocks": clocks, "e2e": e2e, "e2e_qkv": e2e_qkv, "gpu_launches": 2 * args.steps,
-            "full_layer": full,
+            "full_layer": full, "fused_allgather": fused_ag,
         }
         if world == 1 and not args.no_cpu_baseline:
             cores = os.cpu_count() or 1

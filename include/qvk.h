@@ -169,6 +169,25 @@ int qvk_prefill_layer_x(qvk_stream_t stream, const qvk_groups* groups, const qvk
                         double* scores_ws_d, uint32_t* idx_ws_d, void* k_cache_d, void* v_cache_d,
                         uint64_t* origin_d);
 
+/* ---- multi-GPU: the cache all-gather fused into the compaction (peer memory over NVLink) ----------------------- */
+/* CUDA IPC export / import of a device buffer (e.g. a rank's cache) so other ranks can store into it directly:
+ * handle_out receives 64 bytes, offset_out the buffer's offset inside its allocation.  qvk_ipc_open maps the
+ * allocation of another process (base_out) — the buffer is base_out + offset; qvk_ipc_close unmaps it. */
+int qvk_ipc_get_handle(const void* ptr_d, void* handle_out, uint64_t* offset_out);
+int qvk_ipc_open(const void* handle, void** base_out);
+int qvk_ipc_close(void* base_d);
+/* qvk_prune / qvk_prefill_layer whose compaction stores every retained row into n_dest caches (<= 8): dest 0 is this
+ * GPU's cache, the others the same cache buffers of the other ranks (qvk_ipc_open pointers), so after every rank's
+ * call (and a cross-rank barrier) each GPU holds the whole pruned cache — no separate all-gather.  kc_d / vc_d /
+ * origin_d are HOST arrays of n_dest device pointers (origin_d may be NULL).  bf16 rows of 64/128/256/512 with the
+ * key_norm_small / value_norm scorers (QVK_E_UNSUPPORTED otherwise). */
+int qvk_prune_dests(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, const void* v_d, int32_t heads,
+                    int32_t width, int32_t scorer, double rho, double* scores_ws_d, uint32_t* idx_ws_d, int32_t n_dest,
+                    void* const* kc_d, void* const* vc_d, uint64_t* const* origin_d);
+int qvk_prefill_layer_dests(qvk_stream_t stream, const qvk_groups* groups, const qvk_layer_params* p, const void* q_d,
+                            const void* k_d, const void* v_d, void* o_d, double* scores_ws_d, uint32_t* idx_ws_d,
+                            int32_t n_dest, void* const* kc_d, void* const* vc_d, uint64_t* const* origin_d);
+
 /* ---- §8f-4: decode-step consumer of the pruned cache ------------------------------------------------------------- */
 /* O[t, h] = softmax_r(scale * q[t, h] . K[r, h / (n_q/n_kv)]) V[r, ...] over every cache row r (non-causal: the video
  * tokens precede the queries) and lse[t, h] = ln sum_r exp(scale * q . K[r]) (may be NULL) so the caller can merge it

@@ -17,6 +17,7 @@ from .prefill import (  # noqa: F401
     gather,
     group_count,
     prefill_layer,
+    prefill_layer_dests,
     prefill_layer_x,
     project_qkv,
     prune,

@@ -71,6 +71,11 @@ _SIGS = {
     "qvk_prefill_layer": (C.c_int, [P, GP, C.POINTER(QvkLayerParams), P, P, P, P, P, P, P, P, P]),
     "qvk_project_qkv": (C.c_int, [P, P, I64, I32, P, I32, I32, I32, P, P, P, GP, P]),
     "qvk_prefill_layer_x": (C.c_int, [P, GP, C.POINTER(QvkLayerParams), P, I32, P, P, P, P, P, P, P, P, P, P]),
+    "qvk_ipc_get_handle": (C.c_int, [P, P, C.POINTER(U64)]),
+    "qvk_ipc_open": (C.c_int, [P, C.POINTER(P)]),
+    "qvk_ipc_close": (C.c_int, [P]),
+    "qvk_prune_dests": (C.c_int, [P, GP, P, P, I32, I32, I32, F64, P, P, I32, P, P, P]),
+    "qvk_prefill_layer_dests": (C.c_int, [P, GP, C.POINTER(QvkLayerParams), P, P, P, P, P, P, I32, P, P, P]),
     "qvk_decode_workspace": (C.c_int, [I32, I32, I32, I32, I64, C.POINTER(SZ)]),
     "qvk_decode_attention": (C.c_int, [P, P, I32, I32, I32, I32, P, P, I64, F32, P, P, P, SZ]),
     "qvk_seeded_matrix": (C.c_int, [P, U64, U32, U32, SZ, F64, P]),

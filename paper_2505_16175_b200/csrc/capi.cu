@@ -1,7 +1,10 @@
 // extern "C" entry points of include/qvk.h: argument validation with the reference's error texts, the host-side
 // group scheduler, and the stream-ordered orchestration of the kernels (score.cu, select.cu, gather.cu,
 // attention.cu, snapkv.cu, exact.cu).  No computation of the path happens on the host.
+#include <cudaTypedefs.h>
+
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -46,6 +49,8 @@ int launch_project_qkv(cudaStream_t, const void*, int64_t, int, const void*, int
                        const qvk_groups*, double*);
 int launch_decode_attention(cudaStream_t, const void*, int, int, int, int, const void*, const void*, int64_t, float,
                             void*, float*, void*, size_t, size_t*);
+int launch_prune_fused_dests(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const double*,
+                             double*, uint32_t*, int, void* const*, void* const*, uint64_t* const*, int);
 bool prune_fused_supported(const qvk_groups*, int, int, const void*, const void*, const void*, const void*);
 int launch_prune_fused(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const double*,
                        double*, uint32_t*, void*, void*, uint64_t*, int);
@@ -351,6 +356,78 @@ int qvk_decode_attention(qvk_stream_t s, const void* q, int32_t n_tq, int32_t n_
                          size_t ws_bytes) {
     if (!ws) QVK_INVALID("decode_attention: workspace required");
     return launch_decode_attention(s, q, n_tq, n_q, n_kv, d_h, kc, vc, rows, scale, o, lse, ws, ws_bytes, nullptr);
+}
+
+// ---- multi-GPU: peer caches ---------------------------------------------------------------------------------------
+int qvk_ipc_get_handle(const void* ptr, void* handle_out, uint64_t* offset_out) {
+    if (!ptr || !handle_out || !offset_out) QVK_INVALID("ipc: null argument");
+    static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+    if (!range) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            QVK_INVALID("ipc: cuMemGetAddressRange unavailable");
+        range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) QVK_INVALID("ipc: not device memory");
+    cudaIpcMemHandle_t h;
+    QVK_CUDA_CHECK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = reinterpret_cast<uint64_t>(ptr) - static_cast<uint64_t>(base);
+    return QVK_OK;
+}
+
+int qvk_ipc_open(const void* handle, void** base_out) {
+    if (!handle || !base_out) QVK_INVALID("ipc: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    QVK_CUDA_CHECK(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return QVK_OK;
+}
+
+int qvk_ipc_close(void* base) {
+    if (base) QVK_CUDA_CHECK(cudaIpcCloseMemHandle(base));
+    return QVK_OK;
+}
+
+int qvk_prune_dests(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int32_t heads, int32_t width,
+                    int32_t scorer, double rho, double* scores_ws, uint32_t* idx_ws, int32_t n_dest,
+                    void* const* kc, void* const* vc, uint64_t* const* origin) {
+    QVK_TRY(check_rho(rho));
+    QVK_TRY(check_groups(g));
+    if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
+    if (!kc || !vc || n_dest < 1) QVK_INVALID("prune: no cache destinations");
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
+    if (rho == 1.0 || (scorer != QVK_KEY_NORM_SMALL && scorer != QVK_VALUE_NORM) ||
+        !prune_fused_supported(g, QVK_BF16, width, k, v, kc[0], vc[0])) {
+        set_error("prune_dests: needs rho < 1, a norm scorer and bf16 rows of 64/128/256/512");
+        return QVK_E_UNSUPPORTED;
+    }
+    return launch_prune_fused_dests(s, g, k, v, heads, width, scorer, nullptr, scores_ws, idx_ws, n_dest, kc, vc,
+                                    origin, 0);
+}
+
+int qvk_prefill_layer_dests(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q,
+                            const void* k, const void* v, void* o, double* scores_ws, uint32_t* idx_ws,
+                            int32_t n_dest, void* const* kc, void* const* vc, uint64_t* const* origin) {
+    if (!p) QVK_INVALID("prefill_layer: null params");
+    QVK_TRY(check_rho(p->rho));
+    QVK_TRY(check_groups(g));
+    if (!kc || !vc || n_dest < 1) QVK_INVALID("prune: no cache destinations");
+    const int heads = p->per_head ? p->n_kv : 1;
+    const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
+    if (p->rho == 1.0 || (p->scorer != QVK_KEY_NORM_SMALL && p->scorer != QVK_VALUE_NORM) ||
+        !prune_fused_supported(g, QVK_BF16, width, k, v, kc[0], vc[0])) {
+        set_error("prefill_layer_dests: needs rho < 1, a norm scorer and bf16 rows of 64/128/256/512");
+        return QVK_E_UNSUPPORTED;
+    }
+    QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
+    return launch_prune_fused_dests(s, g, k, v, heads, width, p->scorer, nullptr, scores_ws, idx_ws, n_dest, kc, vc,
+                                    origin, 1);
 }
 
 // ---- stand-in model pieces --------------------------------------------------------------------------------------

@@ -74,6 +74,17 @@ __device__ __forceinline__ void prune_trace(int slot) {
 #define QVK_PT(slot)
 #endif
 
+// Cache destinations of the compaction: dest 0 is this GPU's cache; dests 1..n-1 are the same cache buffers of the
+// other ranks, mapped into this process over NVLink (CUDA IPC peer pointers, distributed.py PeerCache) — the
+// all-gather of the pruned rows fused into the gather (each retained row is read once and stored n times).
+constexpr int kMaxDests = 8;
+struct Dests {
+    int n;
+    __nv_bfloat16* kc[kMaxDests];
+    __nv_bfloat16* vc[kMaxDests];
+    uint64_t* org[kMaxDests];
+};
+
 struct FusedShared {
     uint32_t hist[2][256];  // double-buffered: round r writes hist[r & 1] (one cluster barrier per round)
     uint32_t warp[kWarps];
@@ -158,8 +169,7 @@ __global__ void __launch_bounds__(kThreads) prune_fused_kernel(
     const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v, int heads,
     const int64_t* __restrict__ tok_off, const int64_t* __restrict__ keep, const int64_t* __restrict__ row_off,
     const uint64_t* __restrict__ first_token, double* __restrict__ scores_out, uint32_t* __restrict__ idx_out,
-    __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc, uint64_t* __restrict__ origin,
-    int overlap_prev) {
+    const Dests dst, int overlap_prev) {
     constexpr int kChunks = W / 8;     // 16-byte chunks per row
     constexpr int kCpl = 4;            // 16-byte chunks per lane per row (chunk sl + c*kLpr)
     constexpr int kLpr = kChunks / kCpl;  // lanes per row: 2 / 4 / 8 / 16
@@ -404,18 +414,19 @@ __global__ void __launch_bounds__(kThreads) prune_fused_kernel(
                 bv[c] = __ldg(reinterpret_cast<const uint4*>(v + src) + sl + c * kLpr);
             }
             const int64_t cu = (crow0 + s) * heads + h;  // cache unit
+            const uint32_t jj = static_cast<uint32_t>(r0 + j);
+            for (int dd = 0; dd < dst.n; ++dd) {
 #pragma unroll
-            for (int c = 0; c < kCpl; ++c) {
-                reinterpret_cast<uint4*>(kc + cu * W)[sl + c * kLpr] = bk[c];
-                reinterpret_cast<uint4*>(vc + cu * W)[sl + c * kLpr] = bv[c];
+                for (int c = 0; c < kCpl; ++c) {
+                    reinterpret_cast<uint4*>(dst.kc[dd] + cu * W)[sl + c * kLpr] = bk[c];
+                    reinterpret_cast<uint4*>(dst.vc[dd] + cu * W)[sl + c * kLpr] = bv[c];
+                }
+                if (sl == 0 && dst.org[dd]) dst.org[dd][cu] = ft + jj;
             }
-            if (sl == 0) {
-                const uint32_t jj = static_cast<uint32_t>(r0 + j);
-                if (idx_out) idx_out[cu] = jj;
-                if (origin) origin[cu] = ft + jj;
-            }
+            if (sl == 0 && idx_out) idx_out[cu] = jj;
         }
     }
+    if (dst.n > 1) __threadfence_system();  // peer stores visible system-wide before the kernel's completion
     QVK_PT(5);
     if (kScore && scores_out) {
         double* so = scores_out + heads * t0 + static_cast<int64_t>(h) * n + r0;
@@ -429,8 +440,8 @@ __global__ void __launch_bounds__(kThreads) prune_fused_kernel(
 
 template <int W, int CL, bool kScore>
 int launch_wc(cudaStream_t stream, const qvk_groups* g, const void* x, const double* scores_in, int negate,
-              const void* k, const void* v, int heads, double* scores_out, uint32_t* idx, void* kc, void* vc,
-              uint64_t* origin, int overlap_prev) {
+              const void* k, const void* v, int heads, double* scores_out, uint32_t* idx, const Dests& dst,
+              int overlap_prev) {
     const int64_t segs = static_cast<int64_t>(g->n_groups) * heads;
     const int rmax = static_cast<int>((g->max_tokens + CL - 1) / CL);
     const size_t smem = static_cast<size_t>(rmax) * (sizeof(double) + sizeof(uint16_t)) + 16;
@@ -463,8 +474,7 @@ int launch_wc(cudaStream_t stream, const qvk_groups* g, const void* x, const dou
     QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, static_cast<const __nv_bfloat16*>(x), scores_in, negate,
                                       static_cast<const __nv_bfloat16*>(k), static_cast<const __nv_bfloat16*>(v),
                                       heads, g->tok_off_d, g->keep_d, g->row_off_d, g->first_token_d, scores_out,
-                                      idx, static_cast<__nv_bfloat16*>(kc), static_cast<__nv_bfloat16*>(vc),
-                                      origin, overlap_prev));
+                                      idx, dst, overlap_prev));
     return QVK_OK;
 }
 
@@ -478,14 +488,14 @@ int cluster_size(int64_t segs, int64_t max_tokens) {
 
 template <int W, bool kScore>
 int launch_w(cudaStream_t stream, const qvk_groups* g, const void* x, const double* scores_in, int negate,
-             const void* k, const void* v, int heads, double* scores_out, uint32_t* idx, void* kc, void* vc,
-             uint64_t* origin, int ov) {
+             const void* k, const void* v, int heads, double* scores_out, uint32_t* idx, const Dests& dst,
+             int ov) {
     switch (cluster_size(static_cast<int64_t>(g->n_groups) * heads, g->max_tokens)) {
-        case 1: return launch_wc<W, 1, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, kc, vc, origin, ov);
-        case 2: return launch_wc<W, 2, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, kc, vc, origin, ov);
-        case 4: return launch_wc<W, 4, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, kc, vc, origin, ov);
-        case 8: return launch_wc<W, 8, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, kc, vc, origin, ov);
-        default: return launch_wc<W, 16, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, kc, vc, origin, ov);
+        case 1: return launch_wc<W, 1, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
+        case 2: return launch_wc<W, 2, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
+        case 4: return launch_wc<W, 4, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
+        case 8: return launch_wc<W, 8, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
+        default: return launch_wc<W, 16, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
     }
 }
 
@@ -505,18 +515,29 @@ bool prune_fused_supported(const qvk_groups* g, int dtype, int width, const void
 // scorer: QVK_KEY_NORM_SMALL / QVK_VALUE_NORM (scores computed here; written to scores_out when non-null) or
 // QVK_SNAPKV = any precomputed scores in scores_in (SnapKV, or the key-norm fused into the projection).
 // overlap_prev: the previous kernel on `stream` does not produce k / v (see the kernel's PDL note).
-int launch_prune_fused(cudaStream_t stream, const qvk_groups* g, const void* k, const void* v, int heads, int width,
-                       int scorer, const double* scores_in, double* scores_out, uint32_t* idx, void* kc, void* vc,
-                       uint64_t* origin, int overlap_prev) {
+// n_dest caches (dest 0 local, the rest peer mappings of the same buffers): the compaction stores every retained row
+// into all of them (<= 8).
+int launch_prune_fused_dests(cudaStream_t stream, const qvk_groups* g, const void* k, const void* v, int heads,
+                             int width, int scorer, const double* scores_in, double* scores_out, uint32_t* idx,
+                             int n_dest, void* const* kc, void* const* vc, uint64_t* const* origin,
+                             int overlap_prev) {
     if (static_cast<int64_t>(g->n_groups) * heads == 0 || g->max_tokens == 0) return QVK_OK;
+    if (n_dest < 1 || n_dest > kMaxDests) QVK_INVALID("prune: 1..8 cache destinations");
+    Dests dst{};
+    dst.n = n_dest;
+    for (int i = 0; i < n_dest; ++i) {
+        dst.kc[i] = static_cast<__nv_bfloat16*>(kc[i]);
+        dst.vc[i] = static_cast<__nv_bfloat16*>(vc[i]);
+        dst.org[i] = origin ? origin[i] : nullptr;
+    }
     const bool pre = scorer == QVK_SNAPKV;
     const void* x = scorer == QVK_VALUE_NORM ? v : k;
     const int negate = scorer == QVK_KEY_NORM_SMALL;
 #define QVK_FUSED_CASE(WW)                                                                                        \
     case WW:                                                                                                      \
-        return pre ? launch_w<WW, false>(stream, g, x, scores_in, negate, k, v, heads, nullptr, idx, kc, vc,      \
-                                         origin, overlap_prev)                                                    \
-                   : launch_w<WW, true>(stream, g, x, nullptr, negate, k, v, heads, scores_out, idx, kc, vc, origin, \
+        return pre ? launch_w<WW, false>(stream, g, x, scores_in, negate, k, v, heads, nullptr, idx, dst,         \
+                                         overlap_prev)                                                            \
+                   : launch_w<WW, true>(stream, g, x, nullptr, negate, k, v, heads, scores_out, idx, dst,         \
                                         overlap_prev);
     switch (width) {
         QVK_FUSED_CASE(64)
@@ -527,6 +548,16 @@ int launch_prune_fused(cudaStream_t stream, const qvk_groups* g, const void* k, 
             QVK_INVALID("prune: fused kernel width");
     }
 #undef QVK_FUSED_CASE
+}
+
+int launch_prune_fused(cudaStream_t stream, const qvk_groups* g, const void* k, const void* v, int heads, int width,
+                       int scorer, const double* scores_in, double* scores_out, uint32_t* idx, void* kc, void* vc,
+                       uint64_t* origin, int overlap_prev) {
+    void* kcs[1] = {kc};
+    void* vcs[1] = {vc};
+    uint64_t* orgs[1] = {origin};
+    return launch_prune_fused_dests(stream, g, k, v, heads, width, scorer, scores_in, scores_out, idx, 1, kcs, vcs,
+                                    origin ? orgs : nullptr, overlap_prev);
 }
 
 }  // namespace qvk

@@ -45,3 +45,58 @@ def allgather_cache(tensors: list[torch.Tensor], bounds: list[tuple[int, int]], 
     for w in works:
         w.wait()
     return []
+
+
+class PeerCache:
+    """The cache all-gather fused into the compaction: every rank maps the other ranks' cache buffers into its address
+    space (CUDA IPC over NVLink; qvk_ipc_*) and the fused prune kernel stores each retained row into ALL ranks' caches
+    (qvk_prefill_layer_dests / qvk_prune_dests), so the pruned cache is replicated as a side effect of the compaction —
+    no separate collective, the NVLink transfers overlap the kernel's own HBM traffic row by row.  After every rank's
+    kernel, one cross-rank barrier (`fence`) makes the replicated cache safe to read.
+
+    tensors: this rank's cache buffers (k_cache, v_cache, origin); the same-shaped buffers of every rank are mapped.
+    """
+
+    def __init__(self, tensors: list[torch.Tensor], group=None):
+        import ctypes as C
+
+        from ._lib import check, lib
+
+        self._lib, self._check = lib, check
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world > 8:
+            raise ValueError("PeerCache: at most 8 ranks (destinations per row)")
+        self.group = group
+        handles = []
+        for t in tensors:
+            h = (C.c_char * 64)()
+            off = C.c_uint64(0)
+            check(lib.qvk_ipc_get_handle(t.data_ptr(), h, C.byref(off)))
+            handles.append((bytes(h), off.value))
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, handles, group=group)
+        self._bases = []
+        self.ptrs = []  # per tensor: [own, then the other ranks in rank order]
+        for i, t in enumerate(tensors):
+            row = [t.data_ptr()]
+            for r in range(self.world):
+                if r == self.rank:
+                    continue
+                base = C.c_void_p(0)
+                hb, off = gathered[r][i]
+                check(lib.qvk_ipc_open(C.create_string_buffer(hb, 64), C.byref(base)))
+                self._bases.append(base.value)
+                row.append(base.value + off)
+            self.ptrs.append(row)
+        self.arrays = [(C.c_void_p * len(row))(*row) for row in self.ptrs]
+
+    def fence(self, device):
+        """Cross-rank barrier after this step's kernels: every peer's stores into our cache have completed."""
+        torch.cuda.current_stream(device).synchronize()
+        dist.barrier(group=self.group)
+
+    def close(self):
+        for b in self._bases:
+            self._check(self._lib.qvk_ipc_close(b))
+        self._bases = []

@@ -360,6 +360,22 @@ def tokenize(frames, tokens_per_frame: int, embed, bf16: bool = False, out=None)
     return out
 
 
+def prefill_layer_dests(q, k, v, groups: DeviceGroups, n_q: int, n_kv: int, rho: float, peers, buffers: LayerBuffers,
+                        scorer: Scorer = Scorer.key_norm_small, scale: float | None = None, cache_row_offset: int = 0):
+    """prefill_layer whose compaction writes every retained row into this rank's cache AND every peer's
+    (distributed.PeerCache over buffers.k_cache / v_cache / origin) — the all-gather fused into the kernel."""
+    d = q.shape[-1]
+    prm = L.QvkLayerParams(n_q, n_kv, d, int(scorer), 1, rho, 1.0 / math.sqrt(d) if scale is None else scale, 32, 1)
+    off = cache_row_offset * n_kv
+    n = len(peers.ptrs[0])
+    kcs = (C.c_void_p * n)(*[p + off * d * 2 for p in peers.ptrs[0]])
+    vcs = (C.c_void_p * n)(*[p + off * d * 2 for p in peers.ptrs[1]])
+    ogs = (C.c_void_p * n)(*[p + off * 8 for p in peers.ptrs[2]])
+    check(lib.qvk_prefill_layer_dests(_stream(), groups.ref, C.byref(prm), _ptr(q), _ptr(k), _ptr(v),
+                                      _ptr(buffers.o), _ptr(buffers.scores), _ptr(buffers.idx), n, kcs, vcs, ogs))
+    return buffers
+
+
 def synth_bf16(seed: int, tag: int, layer: int, group: int, rows: int, heads: int, width: int,
                head_scale: bool, device="cuda") -> torch.Tensor:
     """Synthetic activations generated in HBM (same bits as oracle qvo_synth_bf16)."""
