@@ -169,8 +169,8 @@ struct SnapShared {
     uint64_t q_full, q_empty, acc_full, acc_empty;
     uint64_t kv_full[kSnapStages], kv_empty[kSnapStages];
     uint32_t tmem_base;
-    float bias[256];       // per window column: m + log2(l) (log2 domain); +inf for invalid rows
-    int pos[256];          // per window column: token position of its query row inside the group (-1: invalid)
+    alignas(16) float bias[256];  // per window column: m + log2(l) (log2 domain); +inf for invalid rows
+    alignas(16) int pos[256];     // per window column: token position of its query row inside the group (-1: invalid)
     float part[2][128];    // pass-2 partial sums of the second column half, by key tile parity
 };
 constexpr size_t kSnapSmem = 1024 + 2 * kSnapQChunk + kSnapStages * kSnapKTile + sizeof(SnapShared);
@@ -286,9 +286,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = p.sl2;
         uint32_t acc_no = 0;
-        const int nchunks = p.rows_pad / 32;
-        const int half_chunks = (nchunks + 1) / 2;
-        const int c_lo = set ? half_chunks : 0, c_hi = set ? nchunks : half_chunks;
+        const int c_lo = 4 * set;  // pass 2: set s covers window columns [128 s, 128 s + 128) (bias +inf past rows)
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             const int g = it / p.n_kv, hk = it - g * p.n_kv;
             const int64_t t0 = __ldg(p.tok_off + g);
@@ -326,7 +324,17 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                     const float mn = fmaxf(m, mx * sl2);
                     float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int c = 0; c < 128; ++c) s4[c & 3] += ptx::ex2(fmaf(x[c], sl2, -mn));
+                    for (int c = 0; c < 128; c += 2) {
+                        float e0 = fmaf(x[c], sl2, -mn), e1 = fmaf(x[c + 1], sl2, -mn);
+                        if ((c & 7) == 0) {
+                            ptx::ex2_poly2(e0, e1);  // a quarter of the exponentials on the FMA pipe
+                        } else {
+                            e0 = ptx::ex2(e0);
+                            e1 = ptx::ex2(e1);
+                        }
+                        s4[c & 3] += e0;
+                        s4[(c & 3) + 1] += e1;
+                    }
                     const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                     l = (m == -INFINITY ? 0.f : l * ptx::ex2(m - mn)) + sum;
                     m = mn;
@@ -341,22 +349,51 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 ptx::tc_fence_after();
                 const int j = jt * 128 + i;
                 const bool edge = jt * 128 + 127 > n - p.window;  // some window rows precede some keys
-                float a4[4] = {0.f, 0.f, 0.f, 0.f};
-                for (int ch = c_lo; ch < c_hi; ++ch) {
-                    float x[32];
-                    QVK_TMEM_LD32F(tmem + lane_off + 256 + 32 * ch, x);
-                    ptx::tmem_ld_wait();
+                // load this set's four 32-column chunks at once and release the accumulator BEFORE the
+                // exponentials, so the next key tile's MMAs overlap them.  Columns past the window rows (the last
+                // chunk of set 1 beyond rows_pad, inside the 512 allocated) have bias +inf: they add exp2(-inf) = 0.
+                float x[128];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const int c = 32 * ch + e;
-                        float y = fmaf(x[e], sl2, -sh->bias[c]);
-                        if (edge && j > sh->pos[c]) y = -INFINITY;
-                        a4[e & 3] += ptx::ex2(y);
+                for (int q = 0; q < 4; ++q) QVK_TMEM_LD32F(tmem + lane_off + 256 + 32 * (c_lo + q), (x + 32 * q));
+                ptx::tmem_ld_wait();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&sh->acc_empty);
+                float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4* b4 = reinterpret_cast<const float4*>(sh->bias + 32 * (c_lo + q));
+                    const int4* p4 = reinterpret_cast<const int4*>(sh->pos + 32 * (c_lo + q));
+#pragma unroll
+                    for (int e4 = 0; e4 < 8; ++e4) {
+                        const float4 bb = b4[e4];
+                        const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+                        int pv[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+                        if (edge) {
+                            const int4 pp = p4[e4];
+                            pv[0] = pp.x;
+                            pv[1] = pp.y;
+                            pv[2] = pp.z;
+                            pv[3] = pp.w;
+                        }
+                        float y[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            y[e] = fmaf(x[32 * q + 4 * e4 + e], sl2, -bv[e]);
+                            if (j > pv[e]) y[e] = -INFINITY;
+                        }
+                        if ((e4 & 1) == 0) {  // a quarter of the exponentials on the FMA pipe
+                            ptx::ex2_poly2(y[0], y[1]);
+                            y[2] = ptx::ex2(y[2]);
+                            y[3] = ptx::ex2(y[3]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) y[e] = ptx::ex2(y[e]);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) a4[e] += y[e];
                     }
                 }
                 const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&sh->acc_empty);
                 if (set) sh->part[jt & 1][i] = acc;
                 ptx::named_bar_sync(2 + quarter, 64);
                 if (!set && j < n) p.raw[p.n_kv * t0 + static_cast<int64_t>(hk) * n + j] = acc + sh->part[jt & 1][i];
