@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import ctypes as C
+import os
 import re
 from pathlib import Path
 
@@ -95,7 +96,8 @@ def header_symbols() -> list[str]:
 
 
 def _load() -> C.CDLL:
-    path = LIB_DIR / "libqvk.so"
+    # developer A/B hook: QVK_LIB_PATH points at an alternative build of the same library (tools/ab_build.sh)
+    path = Path(os.environ["QVK_LIB_PATH"]) if os.environ.get("QVK_LIB_PATH") else LIB_DIR / "libqvk.so"
     if not path.exists():
         raise ImportError(f"{path} is missing: run `python -m paper_2505_16175_b200.build` (no CPU fallback exists)")
     lib = C.CDLL(str(path))

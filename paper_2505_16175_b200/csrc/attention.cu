@@ -456,18 +456,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const ptx::f2 sl2x2 = ptx::f2_make(sl2, sl2);
                 const ptx::f2 negx2 = ptx::f2_make(-m_ref, -m_ref);
                 ptx::f2 acc0 = ptx::f2_make(0.f, 0.f), acc1 = acc0;
+                // 16 exponential pairs (32 P columns = 16 packed TMEM columns) per part; x*scale - max on FFMA2,
+                // 2^x on the MUFU except kPolyPairs of every 16 pairs on the FMA pipe (ex2_poly2).
+                auto part = [&](int q, uint32_t (&pk)[16]) {
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {  // 64 probabilities -> 32 packed bf16x2 columns per store
-                    uint32_t pk[32];
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        // x*scale - max on FFMA2; 2^x on the MUFU, except kPolyPairs of every 16 pairs on the FMA
-                        // pipe (ex2_poly2) so the two pipes share the exponentials.
-                        const ptx::f2 y = ptx::f2_fma(ptx::f2_make(x[64 * half + 2 * c], x[64 * half + 2 * c + 1]),
-                                                      sl2x2, negx2);
+                    for (int c = 0; c < 16; ++c) {
+                        const int xc = 32 * q + 2 * c;
+                        const ptx::f2 y = ptx::f2_fma(ptx::f2_make(x[xc], x[xc + 1]), sl2x2, negx2);
                         float p0, p1;
                         ptx::f2_split(y, p0, p1);
-                        if ((c & 15) < kPolyPairs) {
+                        if (c < kPolyPairs) {
                             ptx::ex2_poly2(p0, p1);
                         } else {
                             p0 = ptx::ex2(p0);
@@ -477,11 +475,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else acc0 = ptx::f2_add(acc0, ptx::f2_make(p0, p1));
                         pk[c] = ptx::pack_bf16(p0, p1);
                     }
-                    QVK_TMEM_ST32(s_col + 32 * half, pk);
+                };
+                auto publish = [&](int half) {
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
                     ptx::mbar_arrive(&bar->p_full[t][half]);
                     if (row == 0) QVK_TRACE(512 + t * 256 + j * 8 + 2 + half);
+                };
+                // P half 0 (parts 0, 1) is published after part 2 has been computed, so the wait for its TMEM
+                // stores overlaps 16 exponential pairs instead of stalling the warp.
+                {
+                    uint32_t pk[16];
+                    part(0, pk);
+                    QVK_TMEM_ST16(s_col + 0, pk);
+                    part(1, pk);
+                    QVK_TMEM_ST16(s_col + 16, pk);
+                    part(2, pk);
+                    publish(0);
+                    QVK_TMEM_ST16(s_col + 32, pk);
+                    part(3, pk);
+                    QVK_TMEM_ST16(s_col + 48, pk);
+                    publish(1);
                 }
                 float s0, s1, s2, s3;
                 ptx::f2_split(acc0, s0, s1);
