@@ -604,15 +604,22 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
         QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
-    // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 4).
+    // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 2 | 4 | 6;
+    // DESIGN.md §3.1).
     static int poly = -1;
     if (poly < 0) {
         const char* e = getenv("QVK_ATTN_POLY");
-        poly = (e && atoi(e) == 0) ? 0 : 4;
+        poly = e ? atoi(e) : 4;
+        if (poly != 0 && poly != 2 && poly != 6) poly = 4;
     }
-    if (d_h == 128)
-        return poly ? launch_attention_d<128, 4>(stream, mq, mk, mv, prm, grid)
-                    : launch_attention_d<128, 0>(stream, mq, mk, mv, prm, grid);
+    if (d_h == 128) {
+        switch (poly) {
+            case 0: return launch_attention_d<128, 0>(stream, mq, mk, mv, prm, grid);
+            case 2: return launch_attention_d<128, 2>(stream, mq, mk, mv, prm, grid);
+            case 6: return launch_attention_d<128, 6>(stream, mq, mk, mv, prm, grid);
+            default: return launch_attention_d<128, 4>(stream, mq, mk, mv, prm, grid);
+        }
+    }
     return poly ? launch_attention_d<64, 4>(stream, mq, mk, mv, prm, grid)
                 : launch_attention_d<64, 0>(stream, mq, mk, mv, prm, grid);
 }
