@@ -21,6 +21,8 @@
 // Result identical to score -> nth_element + sort under (score desc, index asc), -0.0 == +0.0 -> ascending gather.
 // Algorithmic bytes per (group, head): N*W*2 (scored tensor) + k*(W*2 (other tensor) + 2*W*2 (writes) + 8 + 4)
 // + N*8 (scores, when written).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -30,7 +32,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxRowsPerCta = 4096;
-constexpr int kRowsTarget = 512;  // rows per CTA the cluster size aims for
+constexpr int kRowsTarget = 1024;  // rows per CTA the cluster size aims for (measured best of 256..4096)
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -480,9 +482,16 @@ int launch_wc(cudaStream_t stream, const qvk_groups* g, const void* x, const dou
 
 // Cluster size: about kRowsTarget rows per CTA, doubled (up to 16) while the grid would leave SMs idle.
 int cluster_size(int64_t segs, int64_t max_tokens) {
+    static int target = -1, fill = -1;  // tuning knobs QVK_PRUNE_ROWS (rows per CTA), QVK_PRUNE_FILL (CTAs per SM)
+    if (target < 0) {
+        const char* e = getenv("QVK_PRUNE_ROWS");
+        target = e && atoi(e) >= 64 ? atoi(e) : kRowsTarget;
+        const char* f = getenv("QVK_PRUNE_FILL");
+        fill = f && atoi(f) >= 1 ? atoi(f) : 2;
+    }
     int cl = 1;
-    while (cl < 16 && max_tokens > static_cast<int64_t>(cl) * kRowsTarget) cl *= 2;
-    while (cl < 16 && segs * cl < 2 * kNumSms && max_tokens >= static_cast<int64_t>(cl) * 2 * 128) cl *= 2;
+    while (cl < 16 && max_tokens > static_cast<int64_t>(cl) * target) cl *= 2;
+    while (cl < 16 && segs * cl < fill * kNumSms && max_tokens >= static_cast<int64_t>(cl) * 2 * 128) cl *= 2;
     return cl;
 }
 
