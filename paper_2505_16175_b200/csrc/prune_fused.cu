@@ -2,7 +2,7 @@
 //
 // prune_group (prefill.cpp:255-282) is three dependent steps; as three kernels (score.cu, select.cu, gather.cu) the
 // select step is latency-bound (one CTA per segment, 2.6 MB of algorithmic traffic) and every launch pays its own
-// ramp and tail.  Here a THREAD-BLOCK CLUSTER of CL CTAs (CL = 1..16, about 512 rows per CTA) owns one segment
+// ramp and tail.  Here a THREAD-BLOCK CLUSTER of CL CTAs (CL = 1..16, about 1024 rows per CTA) owns one segment
 // (N_g rows of one head of one group):
 //   1. score: CTA c scores rows [c*R, (c+1)*R) (R = ceil(N_g / CL)) straight from HBM — a row (width bf16) is read
 //      by W/32 lanes with 4 x 16-byte loads each, two rows in flight per lane group; bf16 magnitudes become doubles
