@@ -17,6 +17,8 @@
 // per thread).  Algorithmic FLOPs: 2 T d_model (n_q + 2 n_kv) d_h.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -53,6 +55,66 @@ constexpr size_t kSmem = 1024 + kStages * kStageBytes + sizeof(ProjBarriers);
 
 __device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk) {
     return ptx::umma_desc_sw128(tile + kk * 32, 16, 1024);  // k-step kk: +32 B inside the 128-byte SW128 rows
+}
+
+// Epilogue of one 128 x 256 accumulator (thread = output row m, TMEM columns acc .. acc + 255): bf16 into the Q / K /
+// V tensors, and for the K heads the key-norm score in the reference's sequential double order (prefill.cpp:207).
+// Once the accumulator is read, arrive on acc_empty — in the peer CTA when `remote` (2-SM kernel: the leader's).
+__device__ __forceinline__ void store_tile(const ProjParams& p, uint32_t acc, int64_t m, int nt, uint32_t acc_empty,
+                                           bool remote) {
+    const bool live = m < p.m;
+    double ss = 0.0;  // key-norm: running sum of squares of the current K head (reference order)
+#pragma unroll 1
+    for (int c = 0; c < kBN / 32; ++c) {
+        float x[32];
+        QVK_TMEM_LD32F(acc + 32 * c, x);
+        ptx::tmem_ld_wait();
+        if (c == kBN / 32 - 1) {  // accumulator fully read: the MMA warp may reuse it
+            ptx::tc_fence_before();
+            if (remote)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc_empty) : "memory");
+            else
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acc_empty) : "memory");
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[e] = ptx::pack_bf16(x[2 * e], x[2 * e + 1]);
+        const int col = nt * kBN + 32 * c;  // global output column of this 32-column chunk
+        __nv_bfloat16* dst;
+        bool is_k = false;
+        int kcol = 0;
+        if (col < p.q_cols) {
+            dst = p.q + m * p.q_cols + col;
+        } else if (col < p.q_cols + p.kv_cols) {
+            kcol = col - p.q_cols;
+            dst = p.k_out + m * p.kv_cols + kcol;
+            is_k = true;
+        } else {
+            dst = p.v + m * p.kv_cols + (col - p.q_cols - p.kv_cols);
+        }
+        if (live) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+        if (is_k && p.scores && live) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const double lo = static_cast<double>(__uint_as_float(pk[e] << 16));
+                const double hi = static_cast<double>(__uint_as_float(pk[e] & 0xffff0000u));
+                ss = __fma_rn(lo, lo, ss);  // squares of bf16 values are exact: rounds like ss + d*d
+                ss = __fma_rn(hi, hi, ss);
+            }
+            if ((kcol + 32) % p.d_h == 0) {  // last chunk of this KV head
+                const int h = kcol / p.d_h;
+                const int g = find_group_fast(p.tok_off, p.n_groups, m, p.max_tokens);
+                const int64_t t0 = __ldg(p.tok_off + g);
+                const int64_t n = __ldg(p.tok_off + g + 1) - t0;
+                p.scores[p.n_kv * t0 + h * n + (m - t0)] = -__dsqrt_rn(ss);  // key_norm_small
+                ss = 0.0;
+            }
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -135,58 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t b = n_acc & 1;
             ptx::mbar_wait(&bar->acc_full[b], (n_acc >> 1) & 1);
             ptx::tc_fence_after();
-            const int64_t m = static_cast<int64_t>(mt) * kBM + row;
-            const bool live = m < p.m;
-            double acc = 0.0;  // key-norm: running sum of squares of the current K head (reference order)
-#pragma unroll 1
-            for (int c = 0; c < kBN / 32; ++c) {
-                float x[32];
-                QVK_TMEM_LD32F(tmem + lane_off + b * kBN + 32 * c, x);
-                ptx::tmem_ld_wait();
-                if (c == kBN / 32 - 1) {  // accumulator fully read: the MMA warp may reuse it
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(&bar->acc_empty[b]);
-                }
-                uint32_t pk[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) pk[e] = ptx::pack_bf16(x[2 * e], x[2 * e + 1]);
-                const int col = nt * kBN + 32 * c;  // global output column of this 32-column chunk
-                __nv_bfloat16* dst;
-                bool is_k = false;
-                int kcol = 0;
-                if (col < p.q_cols) {
-                    dst = p.q + m * p.q_cols + col;
-                } else if (col < p.q_cols + p.kv_cols) {
-                    kcol = col - p.q_cols;
-                    dst = p.k_out + m * p.kv_cols + kcol;
-                    is_k = true;
-                } else {
-                    dst = p.v + m * p.kv_cols + (col - p.q_cols - p.kv_cols);
-                }
-                if (live) {
-                    uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) d4[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                }
-                if (is_k && p.scores && live) {
-                    // prefill.cpp:207: sum over the head's columns in order of double(bf16 value)^2 (exact squares)
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const double lo = static_cast<double>(__uint_as_float(pk[e] << 16));
-                        const double hi = static_cast<double>(__uint_as_float(pk[e] & 0xffff0000u));
-                        acc = __fma_rn(lo, lo, acc);
-                        acc = __fma_rn(hi, hi, acc);
-                    }
-                    if ((kcol + 32) % p.d_h == 0) {  // last chunk of this KV head
-                        const int h = kcol / p.d_h;
-                        const int g = find_group_fast(p.tok_off, p.n_groups, m, p.max_tokens);
-                        const int64_t t0 = __ldg(p.tok_off + g);
-                        const int64_t n = __ldg(p.tok_off + g + 1) - t0;
-                        p.scores[p.n_kv * t0 + h * n + (m - t0)] = -__dsqrt_rn(acc);  // key_norm_small
-                        acc = 0.0;
-                    }
-                }
-            }
+            store_tile(p, tmem + lane_off + b * kBN, static_cast<int64_t>(mt) * kBM + row, nt,
+                       ptx::smem_u32(&bar->acc_empty[b]), false);
         }
     }
     ptx::tc_fence_before();
@@ -194,6 +206,162 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == kMmaWarp) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------------------------------
+// 2-SM variant (tcgen05.mma.cta_group::2): a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 output tile with
+// M = 256 MMAs issued by the leader CTA.  Each CTA stages its own 128 X rows and HALF of the W tile (128 of the 256
+// output columns) per k-block — 32 KB instead of 48 KB per SM per k-block, so L2 -> SMEM traffic and the MMA's
+// shared-memory operand reads per FLOP drop by a third, and the ring gets 6 stages.  Each CTA's TMEM holds its 128
+// rows x 256 columns of the accumulator (double-buffered), drained by its own epilogue warps.
+// Barriers: the TMA of both CTAs signals the leader's full[s] (expect_tx for both halves); the leader's MMA commit
+// multicasts empty[s] / acc_full[b] to both CTAs; both CTAs' epilogues arrive on the leader's acc_empty[b].
+constexpr int kStages2 = 6;
+constexpr uint32_t kBHalf = (kBN / 2) * kBK * 2;       // 16 KB: this CTA's 128 W rows
+constexpr uint32_t kStage2 = kABytes + kBHalf;          // 32 KB
+struct ProjBarriers2 {
+    uint64_t full[kStages2], empty[kStages2];
+    uint64_t acc_full[2], acc_empty[2];
+    uint32_t tmem_base;
+};
+constexpr size_t kSmem2 = 1024 + kStages2 * kStage2 + sizeof(ProjBarriers2);
+
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    project_qkv_2sm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                           const ProjParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    ProjBarriers2* bar = reinterpret_cast<ProjBarriers2*>(smem + kStages2 * kStage2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank_in_cluster();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
+    const int m_tiles = static_cast<int>((p.m + 2 * kBM - 1) / (2 * kBM));
+    const int n_tiles = p.n / kBN;
+    const int tiles = m_tiles * n_tiles;
+    const int kb_count = p.k / kBK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages2; ++s) {
+            ptx::mbar_init(&bar->full[s], 1);   // the leader's expect_tx arrival (tx: both CTAs' TMA)
+            ptx::mbar_init(&bar->empty[s], 1);  // the leader's multicast MMA commit
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bar->acc_full[b], 1);
+            ptx::mbar_init(&bar->acc_empty[b], 2 * 128);  // both CTAs' epilogue threads (leader's copy is used)
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == kMmaWarp) {  // one warp of EACH CTA of the pair allocates collectively
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         ptx::smem_u32(&bar->tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    ptx::tc_fence_before();
+    cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+    ptx::tc_fence_after();
+    const uint32_t tmem = bar->tmem_base;
+
+    if (warp == kTmaWarp) {
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tm_x);
+            ptx::prefetch_tmap(&tm_w);
+            uint32_t it = 0;
+            for (int tile = pair; tile < tiles; tile += pairs) {
+                const int mt = tile / n_tiles, nt = tile - mt * n_tiles;
+                for (int kb = 0; kb < kb_count; ++kb, ++it) {
+                    const uint32_t s = it % kStages2;
+                    ptx::mbar_wait(&bar->empty[s], ((it / kStages2) & 1) ^ 1);
+                    uint8_t* st = smem + s * kStage2;
+                    if (leader) ptx::mbar_arrive_expect_tx(&bar->full[s], 2 * kStage2);
+                    const uint32_t fb = map_to_cta(ptx::smem_u32(&bar->full[s]), 0);  // the leader's full[s]
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+                        "[%0], [%1, {%3, %4}], [%2];" ::"r"(ptx::smem_u32(st)),
+                        "l"(reinterpret_cast<uint64_t>(&tm_x)), "r"(fb), "r"(kb * kBK),
+                        "r"(mt * 2 * kBM + static_cast<int>(rank) * kBM)
+                        : "memory");
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+                        "[%0], [%1, {%3, %4}], [%2];" ::"r"(ptx::smem_u32(st + kABytes)),
+                        "l"(reinterpret_cast<uint64_t>(&tm_w)), "r"(fb), "r"(kb * kBK),
+                        "r"(nt * kBN + static_cast<int>(rank) * (kBN / 2))
+                        : "memory");
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (leader && ptx::elect_one()) {
+            constexpr uint32_t kId = ptx::idesc_bf16_f32(2 * kBM, kBN, false, false);
+            const uint32_t base = ptx::smem_u32(smem);
+            uint32_t it = 0, n_acc = 0;
+            for (int tile = pair; tile < tiles; tile += pairs, ++n_acc) {
+                const uint32_t b = n_acc & 1;
+                ptx::mbar_wait(&bar->acc_empty[b], ((n_acc >> 1) & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d = tmem + b * kBN;
+                for (int kb = 0; kb < kb_count; ++kb, ++it) {
+                    const uint32_t s = it % kStages2;
+                    ptx::mbar_wait(&bar->full[s], (it / kStages2) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = base + s * kStage2, b_addr = a_addr + kABytes;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t da = kdesc(a_addr, kk), db = kdesc(b_addr, kk);
+                        const uint32_t acc = (kb | kk) != 0;
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                            "l"(da), "l"(db), "r"(kId), "r"(acc));
+                    }
+                    asm volatile(
+                        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                        "%1;" ::"r"(ptx::smem_u32(&bar->empty[s])),
+                        "h"(static_cast<uint16_t>(3))
+                        : "memory");
+                }
+                asm volatile(
+                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                    "%1;" ::"r"(ptx::smem_u32(&bar->acc_full[b])),
+                    "h"(static_cast<uint16_t>(3))
+                    : "memory");
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        uint32_t n_acc = 0;
+        for (int tile = pair; tile < tiles; tile += pairs, ++n_acc) {
+            const int mt = tile / n_tiles, nt = tile - mt * n_tiles;
+            const uint32_t b = n_acc & 1;
+            ptx::mbar_wait(&bar->acc_full[b], (n_acc >> 1) & 1);
+            ptx::tc_fence_after();
+            const int64_t m = static_cast<int64_t>(mt) * 2 * kBM + static_cast<int64_t>(rank) * kBM + row;
+            store_tile(p, tmem + lane_off + b * kBN, m, nt, map_to_cta(ptx::smem_u32(&bar->acc_empty[b]), 0),
+                       true);
+        }
+    }
+    ptx::tc_fence_before();
+    cluster_sync_all();  // both CTAs done with TMEM (and with the leader's barriers)
+    if (warp == kMmaWarp) {
+        ptx::tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
     }
 }
 
@@ -263,6 +431,41 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
         int dev = 0;
         QVK_CUDA_CHECK(cudaGetDevice(&dev));
         QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    static int two_sm = -1;  // tuning knob QVK_PROJ_2SM = 0 | 1
+    if (two_sm < 0) {
+        const char* e = getenv("QVK_PROJ_2SM");
+        two_sm = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    if (two_sm) {
+        CUtensorMap mw2;  // W boxes of 128 rows: each CTA of the pair stages half of the 256-column tile
+        if (!make_map_2d(&mw2, w, n, d_model, kBN / 2)) {
+            set_error("project: cuTensorMapEncodeTiled failed");
+            return QVK_E_CUDA;
+        }
+        static bool attr2 = false;
+        if (!attr2) {
+            QVK_CUDA_CHECK(cudaFuncSetAttribute(project_qkv_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(kSmem2)));
+            attr2 = true;
+        }
+        const int64_t tiles2 = ((tokens + 2 * kBM - 1) / (2 * kBM)) * (n / kBN);
+        if (tiles2 > 0x7fffffff) QVK_INVALID("project: too many tiles");
+        const unsigned pairs = static_cast<unsigned>(std::min<int64_t>(tiles2, sms / 2));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmem2;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, project_qkv_2sm_kernel, mx, mw2, p));
+        return QVK_OK;
     }
     const int64_t tiles = ((tokens + kBM - 1) / kBM) * (n / kBN);
     if (tiles > 0x7fffffff) QVK_INVALID("project: too many tiles");
