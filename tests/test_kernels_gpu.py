@@ -569,3 +569,33 @@ def test_frame_prefill_matches_device_layer(cuda):
     assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
     assert torch.equal(out_o, buf.origin.cpu())
     assert torch.equal(fp.o, buf.o)
+
+
+def test_project_qkv_one_sm_variant(cuda, tmp_path):
+    """The 1-SM GEMM variant (QVK_PROJ_2SM=0, read once per process: run in a subprocess) agrees with the default
+    2-SM kernel within the bf16 tolerance and its fused key-norm equals qvk_score on its own K bit for bit."""
+    import subprocess
+    import sys
+    code = r"""
+import math, sys, torch
+sys.path.insert(0, %r)
+import paper_2505_16175_b200 as qp
+dev = torch.device('cuda', 0)
+sizes = [1000, 777]
+plan = qp.GroupPlan.from_sizes(sizes, 0.5); g = plan.to(dev); T = sum(sizes)
+x = qp.synth_bf16(5, 7, 0, 0, T, 1, 1024, False, dev).view(T, 1024)
+w = (qp.synth_bf16(5, 8, 0, 0, 8 * 128, 1, 1024, False, dev).float() / 32).to(torch.bfloat16).view(-1, 1024)
+q, k, v, sc = qp.project_qkv(x, w, 4, 2, 128, g, with_scores=True)
+assert sc.cpu().numpy().tobytes() == qp.score(k, v, g, 2, 128, qp.Scorer.key_norm_small).cpu().numpy().tobytes()
+torch.save({'q': q.cpu(), 'k': k.cpu(), 'v': v.cpu()}, %r)
+"""
+    outs = []
+    for flag in ("0", "1"):
+        path = tmp_path / f"p{flag}.pt"
+        env = dict(__import__("os").environ, QVK_PROJ_2SM=flag)
+        r = subprocess.run([sys.executable, "-c", code % (str(GOLD.parent.parent), str(path))], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(torch.load(path))
+    for name in ("q", "k", "v"):
+        check_tol(outs[0][name], outs[1][name], f"1-SM vs 2-SM {name}")
