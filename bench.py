@@ -262,6 +262,9 @@ def main():
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     clocks = sampler.stop()
+    # per-kernel times right after the timed region, before the clock probe below heats the GPU further
+    kernel_times(max(10, args.steps))
+    torch.cuda.synchronize()
     if clocks["samples"] < 3:  # timed region shorter than the sampling period: probe the same step for ~1 s
         sampler = ClockSampler(local)
         t0 = time.perf_counter()
@@ -271,8 +274,6 @@ def main():
             torch.cuda.synchronize()
         clocks = sampler.stop()
         clocks["note"] = "sampled over a 1.2 s run of the same step right after the timed region"
-    kernel_times(max(3, args.steps))
-    torch.cuda.synchronize()
     attn_ms = [a.elapsed_time(b) for a, b in attn_ev]
     prune_ms = [a.elapsed_time(b) for a, b in prune_ev]
     el = torch.tensor([elapsed_ms, statistics.mean(attn_ms), statistics.mean(prune_ms)], device=dev)
@@ -453,7 +454,7 @@ def main():
                          "peak": tf_burst, "unit": "TFLOP/s", "frac": achieved / tf_burst, "traffic": traffic,
                          "peak_source": peak_src + " burst", "flop_per_launch": fl,
                          "avg_launch_ms": attn_avg,
-                         "timing": "CUDA events around each launch in a serialised pass of max(3, steps) launches right "
+                         "timing": "CUDA events around each launch in a serialised pass of max(10, steps) launches right "
                                    "after the timed region (in the timed steps the prune overlaps the attention tail)"},
             "secondary": {"kernels": "prune_fused_kernel: score+select+gather in one cluster launch (qvk_prune)", "avg_ms": prune_avg,
                           "algorithmic_bytes": pb, "achieved_gbs": pb / (prune_avg / 1e3) / 1e9,
