@@ -599,3 +599,45 @@ torch.save({'q': q.cpu(), 'k': k.cpu(), 'v': v.cpu()}, %r)
         outs.append(torch.load(path))
     for name in ("q", "k", "v"):
         check_tol(outs[0][name], outs[1][name], f"1-SM vs 2-SM {name}")
+
+
+@pytest.mark.parametrize("scorer,per_head", [(qp.Scorer.snapkv, True), (qp.Scorer.value_norm, True),
+                                             (qp.Scorer.key_norm_small, False)])
+def test_prefill_layer_x_other_scorers(cuda, scorer, per_head):
+    """qvk_prefill_layer_x without the fused key-norm (SnapKV, value-norm, per-token pruning) == projection followed
+    by qvk_prefill_layer, bit for bit; ragged groups."""
+    sizes, d_model, n_q, n_kv, d_h, rho = [1024, 700, 1024], 1024, 8, 2, 128, 0.25
+    T = sum(sizes)
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    x, w = _proj_inputs(T, d_model, n_q, n_kv, d_h, cuda, seed=13)
+    buf, _ = qp.prefill_layer_x(x, w, g, n_q, n_kv, d_h, rho, scorer, per_head)
+    q, k, v = qp.project_qkv(x, w, n_q, n_kv, d_h)
+    buf2 = qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, scorer, per_head)
+    torch.cuda.synchronize()
+    assert torch.equal(buf.o, buf2.o)
+    assert torch.equal(buf.k_cache, buf2.k_cache) and torch.equal(buf.v_cache, buf2.v_cache)
+    assert torch.equal(buf.origin, buf2.origin)
+
+
+def test_frame_prefill_ragged_last_group(cuda):
+    """FramePrefill with a frame count that leaves a short last group (prefill.cpp:170-183) == device path."""
+    F, fpg, tpf, H, W = 23, 4, 64, 64, 64
+    n_q, n_kv, d_h, d_model, rho = 8, 2, 128, 512, 0.5
+    plan = qp.GroupPlan.plan(F, fpg, tpf, rho, 1)
+    assert int(plan.sizes[-1]) == 3 * tpf
+    g = plan.to(cuda)
+    fr = _frames(F, H, W, cuda, seed=9)
+    embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(5)) * 2 - 1) / 255).to(cuda)
+    w = (torch.randn((n_q + 2 * n_kv) * d_h, d_model, generator=torch.Generator().manual_seed(6)) /
+         math.sqrt(d_model)).to(torch.bfloat16).to(cuda)
+    buf, _ = qp.prefill_layer_x(qp.tokenize(fr, tpf, embed, bf16=True), w, g, n_q, n_kv, d_h, rho)
+    fp = qp.FramePrefill(plan, tpf, H, W, embed, w, n_q, n_kv, d_h, rho, cuda, chunks=4)
+    hf = fr.cpu().pin_memory()
+    out_k = torch.empty(fp.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+    out_v = torch.empty_like(out_k).pin_memory()
+    out_o = torch.empty(fp.origin.numel(), dtype=torch.int64).pin_memory()
+    fp.run(hf, out_k, out_v, out_o)
+    torch.cuda.synchronize()
+    assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
+    assert torch.equal(out_o, buf.origin.cpu())
