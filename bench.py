@@ -401,7 +401,8 @@ def main():
         embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(11)) * 2 - 1) / 255).to(dev)
         wqkv = (qp.synth_bf16(1, 8, 0, 0, (n_q + 2 * n_kv) * d, 1, d_model, False, dev).float()
                 * (1.0 / math.sqrt(d_model))).to(torch.bfloat16).view(-1, d_model)
-        e2e_chunks = int(os.environ.get("QVK_E2E_CHUNKS", "8"))  # dev knob: group chunks of the pipeline
+        e2e_chunks = os.environ.get("QVK_E2E_CHUNKS", "8")  # dev knob: group chunks of the pipeline (n | taper)
+        e2e_chunks = int(e2e_chunks) if e2e_chunks.isdigit() else e2e_chunks
         fp = qp.FramePrefill(local_plan, c["tokens_per_frame"], side, side, embed, wqkv, n_q, n_kv, d, rho, dev,
                              chunks=e2e_chunks, cache_rows=plan.total_rows, row_base=row_base)
         gather_f = (lambda: allgather_cache([fp.k_cache, fp.v_cache, fp.origin], bounds, [unit, unit, n_kv])) \
@@ -411,7 +412,7 @@ def main():
                "h2d_bytes_per_step": hframes.numel() * hframes.element_size(), "d2h_bytes_per_step": d2h,
                "path": "FramePrefill (public API, pipeline.py): pinned host video frames (%d x 3 x %d x %d uint8) -> "
                        "qvk_tokenize_bf16 -> qvk_prefill_layer_x (QKV projection GEMM with fused key-norm, attention, "
-                       "select+gather) -> pruned cache to pinned host; %d group chunks, copies on two streams "
+                       "select+gather) -> pruned cache to pinned host; %s group chunks, copies on two streams "
                        "overlapped with the kernels" % (n_frames, side, side, e2e_chunks),
                "includes": "frames upload, tokenizer, projection GEMM (not in `value`), attention, prune, readback"}
         del fp, hframes, wqkv, embed

@@ -19,6 +19,24 @@ from ._lib import check, lib
 from .prefill import GroupPlan, Scorer
 
 
+def chunk_bounds(n_groups: int, chunks) -> np.ndarray:
+    """Group boundaries of the pipeline chunks.  `chunks` is a count (equal chunks) or "taper": small chunks at both
+    ends (the first chunk's upload and the last chunk's kernels + readback are the parts no other chunk overlaps),
+    large ones in the middle — e.g. 16 groups -> 1, 2, 3, 4, 3, 2, 1."""
+    G = n_groups
+    if chunks == "taper":
+        sizes, k = [], 1
+        while sum(sizes) + 2 * k <= G:
+            sizes = sizes[:len(sizes) // 2] + [k, k] + sizes[len(sizes) // 2:]
+            k += 1
+        rest = G - sum(sizes)
+        if rest:
+            sizes.insert(len(sizes) // 2, rest)
+        return np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+    chunks = max(1, min(int(chunks), G))
+    return np.linspace(0, G, chunks + 1).round().astype(int)
+
+
 class HostPrefill:
     def __init__(self, plan: GroupPlan, n_q: int, n_kv: int, d_h: int, rho: float, device,
                  scorer: Scorer = Scorer.key_norm_small, chunks: int = 4, cache_rows: int | None = None,
@@ -26,8 +44,7 @@ class HostPrefill:
         self.plan, self.n_q, self.n_kv, self.d, self.rho = plan, n_q, n_kv, d_h, rho
         self.dev = torch.device(device)
         G = plan.n_groups
-        chunks = max(1, min(chunks, G))
-        bounds = np.linspace(0, G, chunks + 1).round().astype(int)
+        bounds = chunk_bounds(G, chunks)
         self.parts = []
         for a, b in zip(bounds[:-1], bounds[1:]):
             if b <= a:
@@ -126,8 +143,7 @@ class FramePrefill:
         self.embed, self.w = embed, w_qkv
         self.d_model = int(embed.shape[0])
         G = plan.n_groups
-        chunks = max(1, min(chunks, G))
-        bounds = np.linspace(0, G, chunks + 1).round().astype(int)
+        bounds = chunk_bounds(G, chunks)
         self.parts = []
         for a, b in zip(bounds[:-1], bounds[1:]):
             if b <= a:
