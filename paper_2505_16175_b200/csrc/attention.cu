@@ -546,13 +546,8 @@ bool make_map(CUtensorMap* m, const void* base, int heads, int64_t tokens, int k
 template <int D, int kPoly>
 int launch_attention_d(cudaStream_t stream, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                        const AttnParams& prm, unsigned grid) {
-    static bool attr = false;
-    if (!attr) {
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(attention_fwd_kernel<D, kPoly>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem_bytes<D>())));
-        attr = true;
-    }
+    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(attention_fwd_kernel<D, kPoly>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes<D>())));
     attention_fwd_kernel<D, kPoly><<<grid, kThreads, smem_bytes<D>(), stream>>>(mq, mk, mv, prm);
     QVK_LAUNCH_CHECK();
     return QVK_OK;

@@ -5,6 +5,9 @@
 
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -14,6 +17,21 @@ namespace qvk {
 
 thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, int>, int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(func, dev, static_cast<int>(attr));
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= value) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, attr, value);
+    if (e == cudaSuccess) done[key] = value;
+    return e;
+}
 
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {
     static bool pooled[64] = {};

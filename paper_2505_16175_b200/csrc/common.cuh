@@ -20,6 +20,10 @@ void set_error(const std::string& msg);
 // threshold of 0 every synchronise returns it to the driver and the next call pays a real allocation, ~0.4 ms).
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
 
+// cudaFuncSetAttribute(func, attr, value) once per (function, device, attribute) — raised when a larger value is
+// asked for; attributes are per device, and one process may drive several GPUs.
+cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value);
+
 constexpr int kNumSms = 148;
 
 // Order-preserving map of a double score onto uint64: larger score <=> larger key.  -0.0 is canonicalised to +0.0

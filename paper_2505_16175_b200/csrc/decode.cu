@@ -389,14 +389,10 @@ int launch_decode_attention(cudaStream_t stream, const void* q, int n_tq, int n_
     p.part_o = static_cast<float*>(ws);
     p.part_ml = p.part_o + part * kDD;
     constexpr size_t smem = (kQRows + 4 * kKvRows) * kPad * sizeof(__nv_bfloat16);
-    static bool attr = false;
-    if (!attr) {
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(decode_attention_kernel<true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(decode_attention_kernel<false>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
+    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(decode_attention_kernel<true>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(decode_attention_kernel<false>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const dim3 grid(mtiles, static_cast<unsigned>(splits), n_kv);
     if (ws_mode)
         decode_attention_kernel<true><<<grid, kDecThreads, smem, stream>>>(p);

@@ -420,12 +420,8 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
     p.tok_off = g ? g->tok_off_d : nullptr;
     p.n_groups = g ? g->n_groups : 0;
     p.max_tokens = g ? g->max_tokens : 0;
-    static bool attr = false;
-    if (!attr) {
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(project_qkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(kSmem)));
-        attr = true;
-    }
+    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(project_qkv_kernel),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -443,12 +439,8 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
             set_error("project: cuTensorMapEncodeTiled failed");
             return QVK_E_CUDA;
         }
-        static bool attr2 = false;
-        if (!attr2) {
-            QVK_CUDA_CHECK(cudaFuncSetAttribute(project_qkv_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                static_cast<int>(kSmem2)));
-            attr2 = true;
-        }
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(project_qkv_2sm_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem2)));
         const int64_t tiles2 = ((tokens + 2 * kBM - 1) / (2 * kBM)) * (n / kBN);
         if (tiles2 > 0x7fffffff) QVK_INVALID("project: too many tiles");
         const unsigned pairs = static_cast<unsigned>(std::min<int64_t>(tiles2, sms / 2));

@@ -448,17 +448,11 @@ int launch_wc(cudaStream_t stream, const qvk_groups* g, const void* x, const dou
     const int rmax = static_cast<int>((g->max_tokens + CL - 1) / CL);
     const size_t smem = static_cast<size_t>(rmax) * (sizeof(double) + sizeof(uint16_t)) + 16;
     auto kern = prune_fused_kernel<W, CL, kScore>;
-    static size_t attr = 0;
-    static bool np = false;
-    if (CL > 8 && !np) {
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        np = true;
-    }
-    if (smem > 48 * 1024 && smem > attr) {
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem)));
-        attr = smem;
-    }
+    if (CL > 8)
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(kern), cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (smem > 48 * 1024)
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(segs * CL));
     cfg.blockDim = dim3(kThreads);

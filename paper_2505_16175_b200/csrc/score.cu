@@ -296,12 +296,8 @@ template <int NB>
 int launch_score_tma(cudaStream_t stream, const CUtensorMap& tm, int64_t units, int heads, const qvk_groups* g,
                      int negate, double* scores) {
     constexpr size_t smem = 1024 + kTmaStages * NB * kTmaRows * 128 + sizeof(ScoreTmaShared);
-    static bool attr = false;
-    if (!attr) {
-        QVK_CUDA_CHECK(cudaFuncSetAttribute(score_norm_tma_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            static_cast<int>(smem)));
-        attr = true;
-    }
+    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(score_norm_tma_kernel<NB>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     static int sms = 0;
     if (!sms) {
         int dev = 0;

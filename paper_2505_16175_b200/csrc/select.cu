@@ -322,12 +322,8 @@ int launch_select(cudaStream_t stream, const qvk_groups* g, const double* scores
     const size_t smem = static_cast<size_t>(g->max_tokens) * sizeof(uint64_t);
     constexpr size_t kMaxDyn = 200 * 1024;
     if (smem <= kMaxDyn) {
-        static bool attr_set = false;
-        if (!attr_set) {
-            QVK_CUDA_CHECK(cudaFuncSetAttribute(select_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                static_cast<int>(kMaxDyn)));
-            attr_set = true;
-        }
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(select_kernel<true>),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaxDyn)));
         select_kernel<true><<<static_cast<unsigned>(segs), kSelThreads, smem, stream>>>(
             scores, g->tok_off_d, g->keep_d, g->row_off_d, heads, idx);
     } else {

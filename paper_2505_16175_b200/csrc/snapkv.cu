@@ -454,12 +454,8 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
             set_error("snapkv: cuTensorMapEncodeTiled failed");
             return QVK_E_CUDA;
         }
-        static bool attr = false;
-        if (!attr) {
-            QVK_CUDA_CHECK(cudaFuncSetAttribute(snapkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                static_cast<int>(kSnapSmem)));
-            attr = true;
-        }
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(snapkv_tc_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSnapSmem)));
         SnapParams sp;
         sp.tok_off = g->tok_off_d;
         sp.n_groups = g->n_groups;
