@@ -13,7 +13,12 @@
 // fragments; the operand tiles are too small for tcgen05 and the kernel is memory-bound), online softmax in
 // registers; a second kernel merges the chunk partials (max / sum rescaling).
 // Algorithmic bytes: 2 * R * n_kv * d * 2 (K and V) + queries and outputs.
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace qvk {
 namespace {
@@ -341,6 +346,279 @@ __global__ void __launch_bounds__(kCombThreads) decode_combine_kernel(const DecP
     }
 }
 
+// ---------------------------------------------------------------------------------------------------------------------
+// tcgen05 variant for prompt-sized query batches (more than 16 query rows per KV head): the mma.sync kernel above is
+// compute-bound there (~200 TFLOP/s).  A CTA takes two 128-row query tiles of one KV head and one chunk of cache
+// rows, and runs the prefill kernel's ping-pong (attention.cu) without the causal mask: S_t = Q_t K(j)^T into TMEM,
+// softmax in registers (thread = query row), P (bf16) written over S in TMEM, O_t += P V(j) with P as the TMEM
+// operand; order PV0(j) S0(j+1) PV1(j) S1(j+1) so the tensor pipe works on one tile while the other's softmax runs.
+// Q rows (token t, head h*g + i) are gathered by the softmax threads into the 128-byte-swizzled smem layout the UMMA
+// descriptors expect; K / V blocks of 128 rows stream through a 4-stage TMA ring.  The chunk partials (unnormalised
+// O, running max, sum) go to the same workspace as the mma.sync kernel's, merged by decode_combine_kernel.
+constexpr int kTcThreads = 320;  // warps 0-3 softmax tile 0, 4-7 tile 1, 8 TMA, 9 MMA
+constexpr int kTcStages = 4;
+constexpr uint32_t kTcChunk = 128 * 128;      // one 128-row x 128-byte SW128 chunk (64 head-dim columns)
+constexpr uint32_t kTcTile = 2 * kTcChunk;    // 128 rows x 128 d bf16
+constexpr float kTcRescale = 8.0f;
+
+struct TcBar {
+    uint64_t q_ready;
+    uint64_t kv_full[kTcStages], kv_empty[kTcStages];
+    uint64_t s_full[2], p_full[2], o_done[2];
+    uint32_t tmem_base;
+};
+constexpr size_t kTcSmem = 1024 + 2 * kTcTile + kTcStages * kTcTile + sizeof(TcBar);
+
+__device__ __forceinline__ uint64_t tc_kdesc(uint32_t tile, int kk) {
+    return ptx::umma_desc_sw128(tile + (kk >> 2) * kTcChunk + (kk & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t tc_vdesc(uint32_t tile, int kk) {
+    return ptx::umma_desc_sw128(tile + kk * 16 * 128, kTcChunk, 1024);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    decode_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                     const DecParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                   // [tile][d chunk][128 rows x 128 B], swizzled
+    uint8_t* sKV = smem + 2 * kTcTile;    // ring
+    TcBar* bar = reinterpret_cast<TcBar*>(sKV + kTcStages * kTcTile);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int split = blockIdx.x, tp = blockIdx.y, h = blockIdx.z;
+    const int64_t r_begin = static_cast<int64_t>(split) * p.rows_per_split;
+    const int64_t r_end = min(p.rows, r_begin + p.rows_per_split);
+    const int nb = static_cast<int>((r_end - r_begin + 127) / 128);
+    const bool has1 = tp * 256 + 128 < p.m_rows;  // second query tile present
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar->q_ready, 256);
+        for (int s = 0; s < kTcStages; ++s) {
+            ptx::mbar_init(&bar->kv_full[s], 1);
+            ptx::mbar_init(&bar->kv_empty[s], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            ptx::mbar_init(&bar->s_full[t], 1);
+            ptx::mbar_init(&bar->p_full[t], 128);
+            ptx::mbar_init(&bar->o_done[t], 1);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 9) ptx::tmem_alloc<512>(&bar->tmem_base);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = bar->tmem_base;
+
+    if (warp == 8) {
+        if (ptx::elect_one()) {  // ===== TMA producer: K0 V0 K1 V1 ... =====
+            ptx::prefetch_tmap(&tm_k);
+            ptx::prefetch_tmap(&tm_v);
+            for (int it = 0; it < 2 * nb; ++it) {
+                const uint32_t st = it % kTcStages;
+                ptx::mbar_wait(&bar->kv_empty[st], ((it / kTcStages) & 1) ^ 1);
+                const CUtensorMap* map = (it & 1) ? &tm_v : &tm_k;
+                const int row = static_cast<int>(r_begin) + (it >> 1) * 128;
+                uint8_t* dst = sKV + st * kTcTile;
+                ptx::mbar_arrive_expect_tx(&bar->kv_full[st], kTcTile);
+                ptx::tma_load_3d(dst, map, &bar->kv_full[st], 0, h, row);
+                ptx::tma_load_3d(dst + kTcChunk, map, &bar->kv_full[st], 64, h, row);
+            }
+        }
+    } else if (warp == 9) {
+        if (ptx::elect_one()) {  // ===== MMA issuer =====
+            constexpr uint32_t kIdS = ptx::idesc_bf16_f32(128, 128, false, false);
+            constexpr uint32_t kIdPV = ptx::idesc_bf16_f32(128, kDD, false, true);
+            const uint32_t q_addr = ptx::smem_u32(sQ), ring = ptx::smem_u32(sKV);
+            const int ntile = has1 ? 2 : 1;
+            auto wait_item = [&](int it) -> uint32_t {
+                const uint32_t st = it % kTcStages;
+                ptx::mbar_wait(&bar->kv_full[st], (it / kTcStages) & 1);
+                ptx::tc_fence_after();
+                return ring + st * kTcTile;
+            };
+            auto issue_s = [&](int t, uint32_t k_addr) {
+#pragma unroll
+                for (int kk = 0; kk < kDD / 16; ++kk)
+                    ptx::mma_ss(tmem + t * 128, tc_kdesc(q_addr + t * kTcTile, kk), tc_kdesc(k_addr, kk), kIdS, kk > 0);
+                ptx::mma_commit(&bar->s_full[t]);
+            };
+            auto issue_pv = [&](int t, uint32_t v_addr, int j) {
+                ptx::mbar_wait(&bar->p_full[t], j & 1);
+                ptx::tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, tc_vdesc(v_addr, kk), kIdPV,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+                if (j == nb - 1) ptx::mma_commit(&bar->o_done[t]);
+            };
+            ptx::mbar_wait(&bar->q_ready, 0);
+            ptx::tc_fence_after();
+            const uint32_t k0 = wait_item(0);
+            for (int t = 0; t < ntile; ++t) issue_s(t, k0);
+            ptx::mma_commit(&bar->kv_empty[0]);
+            for (int j = 0; j < nb; ++j) {
+                const int v_it = 2 * j + 1;
+                const uint32_t v_addr = wait_item(v_it);
+                const bool more = j + 1 < nb;
+                const uint32_t kn = more ? wait_item(v_it + 1) : 0u;
+                issue_pv(0, v_addr, j);
+                if (more) issue_s(0, kn);
+                if (ntile > 1) {
+                    issue_pv(1, v_addr, j);
+                    if (more) issue_s(1, kn);
+                }
+                ptx::mma_commit(&bar->kv_empty[v_it % kTcStages]);
+                if (more) ptx::mma_commit(&bar->kv_empty[(v_it + 1) % kTcStages]);
+            }
+        }
+    } else {
+        // ===== softmax (thread = query row of tile t) =====
+        const int t = warp >> 2, quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t s_col = tmem + lane_off + t * 128, o_col = tmem + lane_off + 256 + t * 128;
+        const int qr = tp * 256 + t * 128 + row;  // query row of this KV head: token qr / g, head h*g + qr % g
+        const bool live = qr < p.m_rows;
+        {   // gather Q into the SW128 K-major layout (chunk c = d/64; 16-byte unit u of the 128-byte row at u ^ row%8)
+            const int tok = live ? qr / p.group : 0, hq = h * p.group + (live ? qr % p.group : 0);
+            const uint4* src = reinterpret_cast<const uint4*>(p.q + (static_cast<int64_t>(tok) * p.n_q + hq) * kDD);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const uint4 x = live ? __ldg(src + u) : make_uint4(0u, 0u, 0u, 0u);
+                const int c = u >> 3, uu = u & 7;
+                ptx::sts128(ptx::smem_u32(sQ + t * kTcTile + c * kTcChunk + row * 128 + ((uu ^ (row & 7)) << 4)), x.x,
+                            x.y, x.z, x.w);
+            }
+            ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor cores
+            ptx::mbar_arrive(&bar->q_ready);
+        }
+        const bool run = t == 0 || has1;
+        const float sl2 = p.scale_log2;
+        float m_ref = -INFINITY, l = 0.f;
+        for (int j = 0; run && j < nb; ++j) {
+            ptx::mbar_wait(&bar->s_full[t], j & 1);
+            ptx::tc_fence_after();
+            float x[128];
+            QVK_TMEM_LD32F(s_col + 0, (x + 0));
+            QVK_TMEM_LD32F(s_col + 32, (x + 32));
+            QVK_TMEM_LD32F(s_col + 64, (x + 64));
+            QVK_TMEM_LD32F(s_col + 96, (x + 96));
+            ptx::tmem_ld_wait();
+            const int64_t valid = r_end - (r_begin + static_cast<int64_t>(j) * 128);  // keys of this block in range
+            if (valid < 128) {
+#pragma unroll
+                for (int c = 0; c < 128; ++c)
+                    if (c >= valid) x[c] = -INFINITY;
+            }
+            float mx0 = x[0], mx1 = x[1], mx2 = x[2], mx3 = x[3];
+#pragma unroll
+            for (int c = 4; c < 128; c += 4) {
+                mx0 = fmaxf(mx0, x[c]);
+                mx1 = fmaxf(mx1, x[c + 1]);
+                mx2 = fmaxf(mx2, x[c + 2]);
+                mx3 = fmaxf(mx3, x[c + 3]);
+            }
+            const float m_new = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+            if (j == 0) {
+                m_ref = m_new;
+            } else {
+                const bool need = m_new > m_ref + kTcRescale;
+                if (__any_sync(0xffffffffu, need)) {  // the commit of S_t(j) proved PV_t(j-1) retired
+                    const float m_upd = need ? m_new : m_ref;
+                    const float f = ptx::ex2(m_ref - m_upd);
+                    l *= f;
+                    m_ref = m_upd;
+#pragma unroll
+                    for (int c = 0; c < kDD / 16; ++c) {
+                        uint32_t o[16];
+                        QVK_TMEM_LD16(o_col + c * 16, o);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                        QVK_TMEM_ST16(o_col + c * 16, o);
+                    }
+                    ptx::tmem_st_wait();
+                }
+            }
+            const ptx::f2 sl2x2 = ptx::f2_make(sl2, sl2), negx2 = ptx::f2_make(-m_ref, -m_ref);
+            ptx::f2 acc0 = ptx::f2_make(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const ptx::f2 y =
+                        ptx::f2_fma(ptx::f2_make(x[64 * half + 2 * c], x[64 * half + 2 * c + 1]), sl2x2, negx2);
+                    float p0, p1;
+                    ptx::f2_split(y, p0, p1);
+                    if ((c & 15) < 4) {
+                        ptx::ex2_poly2(p0, p1);
+                    } else {
+                        p0 = ptx::ex2(p0);
+                        p1 = ptx::ex2(p1);
+                    }
+                    if (c & 1) acc1 = ptx::f2_add(acc1, ptx::f2_make(p0, p1));
+                    else acc0 = ptx::f2_add(acc0, ptx::f2_make(p0, p1));
+                    pk[c] = ptx::pack_bf16(p0, p1);
+                }
+                QVK_TMEM_ST32(s_col + 32 * half, pk);
+            }
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&bar->p_full[t]);
+            float s0, s1, s2, s3;
+            ptx::f2_split(acc0, s0, s1);
+            ptx::f2_split(acc1, s2, s3);
+            l += (s0 + s1) + (s2 + s3);
+        }
+        if (run) {
+            ptx::mbar_wait(&bar->o_done[t], 0);
+            ptx::tc_fence_after();
+            const int64_t base = (static_cast<int64_t>(h) * p.splits + split) * p.m_rows + qr;
+#pragma unroll
+            for (int c = 0; c < kDD / 16; ++c) {
+                uint32_t o[16];
+                QVK_TMEM_LD16(o_col + c * 16, o);
+                ptx::tmem_ld_wait();
+                if (live) {
+                    float4* dst = reinterpret_cast<float4*>(p.part_o + base * kDD + c * 16);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        dst[e] = make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
+                                             __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
+                }
+            }
+            if (live) *reinterpret_cast<float2*>(p.part_ml + base * 2) = make_float2(m_ref, l);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+bool dec_map(CUtensorMap* m, const void* base, int heads, int64_t rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(kDD), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(kDD) * 2, static_cast<cuuint64_t>(heads) * kDD * 2};
+    cuuint32_t box[3] = {64, 1, 128};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 int launch_decode_attention(cudaStream_t stream, const void* q, int n_tq, int n_q, int n_kv, int d_h,
@@ -367,16 +645,24 @@ int launch_decode_attention(cudaStream_t stream, const void* q, int n_tq, int n_
     p.group = n_q / n_kv;
     p.m_rows = n_tq * p.group;
     p.scale_log2 = scale * 1.4426950408889634f;
-    const int mtiles = (p.m_rows + kQRows - 1) / kQRows;
-    const int64_t blocks = (rows + kKvRows - 1) / kKvRows;
+    static int tc_env = -1;  // QVK_DECODE_TC = 0 keeps prompt-sized batches on the mma.sync kernel
+    if (tc_env < 0) {
+        const char* e = getenv("QVK_DECODE_TC");
+        tc_env = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    const bool tc = tc_env && p.m_rows > 16 && rows <= 0x7fffffff;
+    const int mtiles = tc ? (p.m_rows + 255) / 256 : (p.m_rows + kQRows - 1) / kQRows;  // tc: pairs of 128-row tiles
+    const int rows_blk = tc ? 128 : kKvRows;
+    const int64_t blocks = (rows + rows_blk - 1) / rows_blk;
     const int64_t base = static_cast<int64_t>(mtiles) * n_kv;
-    const bool ws_mode = p.m_rows <= 16;
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(blocks, (4 * kNumSms + base - 1) / base));
+    const bool ws_mode = !tc && p.m_rows <= 16;
+    const int64_t per_sm = tc ? 2 : 4;  // target CTAs per SM worth of chunks
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(blocks, (per_sm * kNumSms + base - 1) / base));
     const int64_t blocks_per = (blocks + splits - 1) / splits;
     splits = (blocks + blocks_per - 1) / blocks_per;
-    if (blocks_per * kKvRows > 0x7fffffff || splits > 16383 || mtiles > 65535)
+    if (blocks_per * rows_blk > 0x7fffffff || splits > 16383 || mtiles > 65535)
         QVK_INVALID("decode_attention: problem too large");
-    p.rows_per_split = static_cast<int>(blocks_per * kKvRows);
+    p.rows_per_split = static_cast<int>(blocks_per * rows_blk);
     p.splits = static_cast<int>(splits);  // partials per (KV head, query row): one per chunk
     const size_t part = static_cast<size_t>(n_kv) * p.splits * p.m_rows;
     const size_t need = part * kDD * sizeof(float) + part * 2 * sizeof(float);
@@ -388,16 +674,28 @@ int launch_decode_attention(cudaStream_t stream, const void* q, int n_tq, int n_
     if (ws_bytes < need) QVK_INVALID("decode_attention: workspace too small");
     p.part_o = static_cast<float*>(ws);
     p.part_ml = p.part_o + part * kDD;
-    constexpr size_t smem = (kQRows + 4 * kKvRows) * kPad * sizeof(__nv_bfloat16);
-    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(decode_attention_kernel<true>),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(decode_attention_kernel<false>),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const dim3 grid(mtiles, static_cast<unsigned>(splits), n_kv);
-    if (ws_mode)
-        decode_attention_kernel<true><<<grid, kDecThreads, smem, stream>>>(p);
-    else
-        decode_attention_kernel<false><<<grid, kDecThreads, smem, stream>>>(p);
+    const dim3 grid(tc ? static_cast<unsigned>(splits) : static_cast<unsigned>(mtiles),
+                    tc ? static_cast<unsigned>(mtiles) : static_cast<unsigned>(splits), n_kv);
+    if (tc) {
+        CUtensorMap mk, mv;
+        if (!dec_map(&mk, k_cache, n_kv, rows) || !dec_map(&mv, v_cache, n_kv, rows)) {
+            set_error("decode_attention: cuTensorMapEncodeTiled failed");
+            return QVK_E_CUDA;
+        }
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(decode_tc_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTcSmem)));
+        decode_tc_kernel<<<grid, kTcThreads, kTcSmem, stream>>>(mk, mv, p);
+    } else {
+        constexpr size_t smem = (kQRows + 4 * kKvRows) * kPad * sizeof(__nv_bfloat16);
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(decode_attention_kernel<true>),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(decode_attention_kernel<false>),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        if (ws_mode)
+            decode_attention_kernel<true><<<grid, kDecThreads, smem, stream>>>(p);
+        else
+            decode_attention_kernel<false><<<grid, kDecThreads, smem, stream>>>(p);
+    }
     QVK_LAUNCH_CHECK();
     decode_combine_kernel<<<static_cast<unsigned>(n_kv * p.m_rows), kCombThreads, 0, stream>>>(
         p, static_cast<__nv_bfloat16*>(o), lse);

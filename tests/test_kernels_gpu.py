@@ -510,7 +510,7 @@ def test_prefill_layer_x_matches_projection_then_layer(cuda):
 
 # ------------------------------------------------------------------------------------------------ decode consumer (§8f-4)
 @pytest.mark.parametrize("n_tq,rows,n_q,n_kv", [(1, 32768, 28, 4), (3, 100, 28, 4), (64, 5000, 28, 4), (1, 1, 4, 2),
-                                                (10, 70001, 8, 8)])
+                                                (10, 70001, 8, 8), (40, 33333, 8, 2), (20, 129, 28, 4)])
 def test_decode_attention_vs_torch(cuda, n_tq, rows, n_q, n_kv):
     """Query tokens attending over a pruned cache (non-causal, GQA) vs a torch fp32 reference: O within
     1e-2 + 1e-2 |ref| (bf16 output), natural-log LSE within 1e-3 absolute."""
