@@ -287,10 +287,18 @@ def main():
     #      stores its retained rows into all ranks' caches over NVLink peer memory; one barrier per step) ----
     fused_ag = None
     if world > 1:
-        try:
-            from paper_2505_16175_b200.distributed import PeerCache
+        from paper_2505_16175_b200.distributed import PeerCache
 
+        peers, err = None, None
+        try:
             peers = PeerCache([buf.k_cache, buf.v_cache, buf.origin])
+        except Exception as e:  # noqa: BLE001
+            err = repr(e)[:300]
+        ok = torch.tensor([0 if peers is None else 1], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank must have mapped its peers, else all skip together
+        try:
+            if ok.item() == 0:
+                raise RuntimeError(err or "a peer rank could not map the caches")
 
             def fused_step():
                 qp.prefill_layer_dests(q, k, v, g, n_q, n_kv, rho, peers, buf, cache_row_offset=row_base)
