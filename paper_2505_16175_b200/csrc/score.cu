@@ -331,6 +331,35 @@ __global__ void __launch_bounds__(128) score_attention_kernel(const T* __restric
     out[i] = __ddiv_rn(sum, divisor);
 }
 
+// Same sum, with each thread's key row staged in shared memory (row stride d + 1 words: conflict-free column reads)
+// and the text-query element broadcast: the sequential t-outer / j-inner double chain of prefill.cpp:220-226 is then
+// bound by the DADD latency instead of an L1/L2 miss per element (the per-thread rows of the kernel above do not fit
+// L1).  R rows (threads) per CTA, R = min(32, what fits in 96 KB).
+template <typename T>
+__global__ void score_attention_smem_kernel(const T* __restrict__ k, int64_t tokens, int d,
+                                            const float* __restrict__ q, int64_t text_count, double divisor,
+                                            double* __restrict__ out) {
+    extern __shared__ float srow[];  // [R][d + 1]
+    const int R = blockDim.x;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * R;
+    const int nr = static_cast<int>(tokens - i0 < R ? tokens - i0 : R);
+    for (int e = threadIdx.x; e < nr * d; e += R) {
+        const int r = e / d, c = e - r * d;
+        srow[r * (d + 1) + c] = static_cast<float>(k[(i0 + r) * d + c]);
+    }
+    __syncthreads();
+    if (threadIdx.x >= nr) return;
+    const float* key = srow + threadIdx.x * (d + 1);
+    double sum = 0.0;
+    for (int64_t t = 0; t < text_count; ++t) {
+        const float* qt = q + t * d;
+#pragma unroll 8
+        for (int j = 0; j < d; ++j)
+            sum = __dadd_rn(sum, __dmul_rn(static_cast<double>(key[j]), static_cast<double>(__ldg(qt + j))));
+    }
+    out[i0 + threadIdx.x] = __ddiv_rn(sum, divisor);
+}
+
 }  // namespace
 
 int launch_score(cudaStream_t stream, const qvk_groups* g, int64_t total_tokens, const void* k, const void* v,
@@ -372,6 +401,25 @@ int launch_score(cudaStream_t stream, const qvk_groups* g, int64_t total_tokens,
         if (total_tokens == 0) return QVK_OK;
         const unsigned blocks = static_cast<unsigned>((total_tokens + 127) / 128);
         const double divisor = static_cast<double>(text_count) * static_cast<double>(n_h);
+        const int rows = std::min<int>(32, static_cast<int>((96 * 1024) / ((static_cast<size_t>(width) + 1) * 4)));
+        if (rows >= 1) {  // staged-row kernel (every width up to 24575)
+            const size_t smem = static_cast<size_t>(rows) * (width + 1) * sizeof(float);
+            const unsigned grid = static_cast<unsigned>((total_tokens + rows - 1) / rows);
+            if (dtype == QVK_F32) {
+                QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(score_attention_smem_kernel<float>),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                score_attention_smem_kernel<float><<<grid, rows, smem, stream>>>(
+                    static_cast<const float*>(k), total_tokens, width, text_query, text_count, divisor, scores);
+            } else {
+                QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(score_attention_smem_kernel<__nv_bfloat16>),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                score_attention_smem_kernel<__nv_bfloat16><<<grid, rows, smem, stream>>>(
+                    static_cast<const __nv_bfloat16*>(k), total_tokens, width, text_query, text_count, divisor,
+                    scores);
+            }
+            QVK_LAUNCH_CHECK();
+            return QVK_OK;
+        }
         if (dtype == QVK_F32)
             score_attention_kernel<float><<<blocks, 128, 0, stream>>>(static_cast<const float*>(k), total_tokens,
                                                                      width, text_query, text_count, divisor, scores);

@@ -7,6 +7,7 @@
 //       JSON line with bitwise comparisons of tokens, text query, every layer's K/V/origin and the cache stats.
 //   parity_driver errors
 //       drives the documented misuse cases through both APIs and prints each pair of qv::Error messages.
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -72,10 +73,12 @@ int pipeline(char** a) {
         fb.write_slot(f, {pixels.data() + f * fb.slot_bytes(), fb.slot_bytes()});
     }
 
-    // drop-in (GPU)
+    // drop-in (GPU); the timed part is tokenize + prefill, the same scope as the reference call timed below
     qv::StandInModel model(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
     const auto groups = model.tokenize(fb, fpg);
     const qv::KvCache cache = qv::prefill(model, groups, prune);
+    const double dropin_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 
     // reference (CPU)
     void* ref = qvref_model_create(cfg.d_model, cfg.n_h, cfg.d_h, cfg.layers, cfg.tokens_per_frame,
@@ -99,7 +102,9 @@ int pipeline(char** a) {
     const auto q = model.text_query();
     const bool query_equal = same_bits(std::vector<float>(q.begin(), q.end()), ref_q.data(), ref_q.size());
 
+    const auto t1 = std::chrono::steady_clock::now();
     void* rc = qvref_prefill_frames(ref, pixels.data(), frames, w, h, fpg, static_cast<int>(prune.scorer), prune.rho);
+    const double ref_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
     bool cache_equal = rc && qvref_cache_layers(rc) == cache.layers.size();
     size_t rows = 0;
     int first_bad_layer = -1;
@@ -124,10 +129,11 @@ int pipeline(char** a) {
     for (size_t i = 0; stats_equal && i < rpg.size(); ++i) stats_equal = rpg[i] == cache.retained_per_group[i];
     std::printf(
         "{\"tokens_equal\": %s, \"query_equal\": %s, \"cache_equal\": %s, \"stats_equal\": %s, \"groups\": %zu, "
-        "\"rows\": %zu, \"first_bad_layer\": %d, \"value_bytes\": %llu}\n",
+        "\"rows\": %zu, \"first_bad_layer\": %d, \"value_bytes\": %llu, \"dropin_ms\": %.3f, "
+        "\"reference_ms\": %.3f}\n",
         tokens_equal ? "true" : "false", query_equal ? "true" : "false", cache_equal ? "true" : "false",
         stats_equal ? "true" : "false", groups.size(), rows, first_bad_layer,
-        static_cast<unsigned long long>(cache.value_bytes()));
+        static_cast<unsigned long long>(cache.value_bytes()), dropin_ms, ref_ms);
     if (rc) qvref_cache_destroy(rc);
     qvref_model_destroy(ref);
     return tokens_equal && query_equal && cache_equal && stats_equal ? 0 : 1;
