@@ -38,6 +38,8 @@ def test_pipeline_bitexact_c1(cuda, pattern, scorer, rho):
     (1, 3, 9, 48, 24, 96, 3, 32, 3, 6, 5, 4, "attention_score", 0.3),    # non-square patch grid, 3 layers
     (3, 2, 3, 16, 16, 32, 2, 16, 1, 1, 2, 1, "value_norm", 0.9),          # one token per frame
     (2, 5, 12, 64, 64, 128, 2, 64, 1, 16, 4, 5, "key_norm_small", 0.05),  # constant frames: 64-fold exact ties
+    (1, 5, 4, 64, 64, 3584, 28, 128, 1, 64, 64, 4, "key_norm_small", 0.5),  # the 7B shape (d_model 3584, 28 heads)
+    (0, 3, 64, 64, 64, 512, 4, 128, 2, 64, 64, 16, "attention_score", 0.25),  # 4096 tokens, 2 layers
 ])
 def test_pipeline_bitexact_misc(cuda, args):
     rc, out, err = run("pipeline", *args)
