@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const float sl2 = p.sl2;
         uint32_t acc_no = 0;
         const int c_lo = 4 * set;  // pass 2: set s covers window columns [128 s, 128 s + 128) (bias +inf past rows)
+        const int nch = min(4, max(0, (p.rows - 128 * set + 31) / 32));  // 32-column chunks holding window rows
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             const int g = it / p.n_kv, hk = it - g * p.n_kv;
             const int64_t t0 = __ldg(p.tok_off + g);
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
+                    if (q >= nch) continue;  // warp-uniform: no window rows in this chunk (exp2(-inf) terms)
                     const float4* b4 = reinterpret_cast<const float4*>(sh->bias + 32 * (c_lo + q));
                     const int4* p4 = reinterpret_cast<const int4*>(sh->pos + 32 * (c_lo + q));
 #pragma unroll
