@@ -518,15 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
-    return fn;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
 }
 
 // (tokens, heads, 128) bf16 viewed as a 3-D tensor {d, heads, tokens}; box {64, 1, 128}, 128-byte swizzle.
@@ -583,30 +575,19 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     prm.tiles_max = static_cast<int>(tiles);
     prm.scale_log2 = scale * 1.4426950408889634f;
     prm.o = static_cast<__nv_bfloat16*>(o);
-    static int pre = -1;
-    if (pre < 0) {
-        const char* e = getenv("QVK_ATTN_PRE");
-        pre = (e && atoi(e) == 0) ? 0 : 1;
-    }
+    static const int pre = env_knob("QVK_ATTN_PRE", 1) != 0;
     prm.pre_issue = pre;
     const int64_t units = static_cast<int64_t>((prm.tiles_max + 1) / 2) * g->n_groups * n_q;
     if (units > 0x7fffffff) QVK_INVALID("attention: too many work units");
     prm.total_units = static_cast<int>(units);
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        QVK_CUDA_CHECK(cudaGetDevice(&dev));
-        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    const int sms = sm_count();
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
     // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 2 | 4 | 6;
     // DESIGN.md §3.1).
-    static int poly = -1;
-    if (poly < 0) {
-        const char* e = getenv("QVK_ATTN_POLY");
-        poly = e ? atoi(e) : 4;
-        if (poly != 0 && poly != 2 && poly != 6) poly = 4;
-    }
+    static const int poly = [] {
+        const int v = env_knob("QVK_ATTN_POLY", 4);
+        return (v == 0 || v == 2 || v == 6) ? v : 4;
+    }();
     if (d_h == 128) {
         switch (poly) {
             case 0: return launch_attention_d<128, 0>(stream, mq, mk, mv, prm, grid);

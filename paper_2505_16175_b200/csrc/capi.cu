@@ -5,8 +5,10 @@
 
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <mutex>
+#include <set>
 #include <tuple>
 #include <string>
 #include <vector>
@@ -34,19 +36,50 @@ cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value) {
 }
 
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {
-    static bool pooled[64] = {};
+    static std::mutex mu;
+    static std::set<int> pooled;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64 && !pooled[dev]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (pooled.insert(dev).second) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
         }
-        pooled[dev] = true;
     }
     return cudaMallocAsync(p, bytes, stream);
+}
+
+int sm_count() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            return kNumSms;
+        return v;
+    }();
+    return n;
+}
+
+int env_knob(const char* name, int def) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : def;
+}
+
+void* tensor_map_encoder() {
+    static void* const fn = [] {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<void*>(nullptr);
+        return ptr;
+    }();
+    return fn;
 }
 
 int launch_score(cudaStream_t, const qvk_groups*, int64_t, const void*, const void*, int, int, int, int,
@@ -379,15 +412,15 @@ int qvk_decode_attention(qvk_stream_t s, const void* q, int32_t n_tq, int32_t n_
 // ---- multi-GPU: peer caches ---------------------------------------------------------------------------------------
 int qvk_ipc_get_handle(const void* ptr, void* handle_out, uint64_t* offset_out) {
     if (!ptr || !handle_out || !offset_out) QVK_INVALID("ipc: null argument");
-    static PFN_cuMemGetAddressRange_v3020 range = nullptr;
-    if (!range) {
+    static const PFN_cuMemGetAddressRange_v3020 range = [] {
         cudaDriverEntryPointQueryResult q;
         void* fn = nullptr;
         if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
             q != cudaDriverEntryPointSuccess)
-            QVK_INVALID("ipc: cuMemGetAddressRange unavailable");
-        range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
-    }
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+    }();
+    if (!range) QVK_INVALID("ipc: cuMemGetAddressRange unavailable");
     CUdeviceptr base = 0;
     size_t size = 0;
     if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) QVK_INVALID("ipc: not device memory");

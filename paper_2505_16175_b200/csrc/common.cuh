@@ -24,6 +24,12 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream);
 // asked for; attributes are per device, and one process may drive several GPUs.
 cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value);
 
+// Process-wide lookups, initialised once in a thread-safe way (capi.cu): the SM count of the current device at first
+// use, an integer tuning knob from the environment (default when unset), and the driver's cuTensorMapEncodeTiled.
+int sm_count();
+int env_knob(const char* name, int def);
+void* tensor_map_encoder();  // PFN_cuTensorMapEncodeTiled_v12000, or nullptr
+
 constexpr int kNumSms = 148;
 
 // Order-preserving map of a double score onto uint64: larger score <=> larger key.  -0.0 is canonicalised to +0.0

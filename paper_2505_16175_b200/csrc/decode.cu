@@ -601,15 +601,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 bool dec_map(CUtensorMap* m, const void* base, int heads, int64_t rows) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        cudaDriverEntryPointQueryResult q;
-        void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return false;
-        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
+    const auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+    if (!enc) return false;
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(kDD), static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(rows)};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(kDD) * 2, static_cast<cuuint64_t>(heads) * kDD * 2};
     cuuint32_t box[3] = {64, 1, 128};
@@ -645,11 +638,7 @@ int launch_decode_attention(cudaStream_t stream, const void* q, int n_tq, int n_
     p.group = n_q / n_kv;
     p.m_rows = n_tq * p.group;
     p.scale_log2 = scale * 1.4426950408889634f;
-    static int tc_env = -1;  // QVK_DECODE_TC = 0 keeps prompt-sized batches on the mma.sync kernel
-    if (tc_env < 0) {
-        const char* e = getenv("QVK_DECODE_TC");
-        tc_env = (e && atoi(e) == 0) ? 0 : 1;
-    }
+    static const int tc_env = env_knob("QVK_DECODE_TC", 1) != 0;  // 0: prompt batches on the mma.sync kernel
     const bool tc = tc_env && p.m_rows > 16 && rows <= 0x7fffffff;
     const int mtiles = tc ? (p.m_rows + 255) / 256 : (p.m_rows + kQRows - 1) / kQRows;  // tc: pairs of 128-row tiles
     const int rows_blk = tc ? 128 : kKvRows;

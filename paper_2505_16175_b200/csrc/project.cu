@@ -366,15 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        cudaDriverEntryPointQueryResult q;
-        void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return false;
-        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
+    const auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+    if (!enc) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
     cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(box_rows)};
@@ -422,17 +415,8 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
     p.max_tokens = g ? g->max_tokens : 0;
     QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(project_qkv_kernel),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        QVK_CUDA_CHECK(cudaGetDevice(&dev));
-        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    static int two_sm = -1;  // tuning knob QVK_PROJ_2SM = 0 | 1
-    if (two_sm < 0) {
-        const char* e = getenv("QVK_PROJ_2SM");
-        two_sm = (e && atoi(e) == 0) ? 0 : 1;
-    }
+    const int sms = sm_count();
+    static const int two_sm = env_knob("QVK_PROJ_2SM", 1) != 0;  // tuning knob QVK_PROJ_2SM = 0 | 1
     if (two_sm) {
         CUtensorMap mw2;  // W boxes of 128 rows: each CTA of the pair stages half of the 256-column tile
         if (!make_map_2d(&mw2, w, n, d_model, kBN / 2)) {

@@ -476,13 +476,9 @@ int launch_wc(cudaStream_t stream, const qvk_groups* g, const void* x, const dou
 
 // Cluster size: about kRowsTarget rows per CTA, doubled (up to 16) while the grid would leave SMs idle.
 int cluster_size(int64_t segs, int64_t max_tokens) {
-    static int target = -1, fill = -1;  // tuning knobs QVK_PRUNE_ROWS (rows per CTA), QVK_PRUNE_FILL (CTAs per SM)
-    if (target < 0) {
-        const char* e = getenv("QVK_PRUNE_ROWS");
-        target = e && atoi(e) >= 64 ? atoi(e) : kRowsTarget;
-        const char* f = getenv("QVK_PRUNE_FILL");
-        fill = f && atoi(f) >= 1 ? atoi(f) : 2;
-    }
+    // tuning knobs QVK_PRUNE_ROWS (rows per CTA), QVK_PRUNE_FILL (CTAs per SM)
+    static const int target = std::max(64, env_knob("QVK_PRUNE_ROWS", kRowsTarget));
+    static const int fill = std::max(1, env_knob("QVK_PRUNE_FILL", 2));
     int cl = 1;
     while (cl < 16 && max_tokens > static_cast<int64_t>(cl) * target) cl *= 2;
     while (cl < 16 && segs * cl < fill * kNumSms && max_tokens >= static_cast<int64_t>(cl) * 2 * 128) cl *= 2;

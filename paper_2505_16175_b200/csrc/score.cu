@@ -274,15 +274,8 @@ __global__ void __launch_bounds__(kTmaConsumers + 32) score_norm_tma_kernel(
 }
 
 bool score_map(CUtensorMap* m, const void* base, int64_t units, int width) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        cudaDriverEntryPointQueryResult q;
-        void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return false;
-        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
+    const auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+    if (!enc) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(units)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 2};
     cuuint32_t box[2] = {64, static_cast<cuuint32_t>(kTmaRows)};
@@ -298,12 +291,7 @@ int launch_score_tma(cudaStream_t stream, const CUtensorMap& tm, int64_t units, 
     constexpr size_t smem = 1024 + kTmaStages * NB * kTmaRows * 128 + sizeof(ScoreTmaShared);
     QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(score_norm_tma_kernel<NB>),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        QVK_CUDA_CHECK(cudaGetDevice(&dev));
-        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    const int sms = sm_count();
     const int64_t tiles = (units + kTmaRows - 1) / kTmaRows;
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, 2 * static_cast<int64_t>(sms)));
     score_norm_tma_kernel<NB><<<grid, kTmaConsumers + 32, smem, stream>>>(tm, units, heads, g->tok_off_d,

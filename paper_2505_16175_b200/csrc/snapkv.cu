@@ -412,15 +412,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
 }
 
 bool snap_map(CUtensorMap* m, const void* base, int heads, int64_t tokens, uint32_t box_heads, uint32_t box_rows) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        cudaDriverEntryPointQueryResult q;
-        void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return false;
-        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
+    const auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+    if (!enc) return false;
     cuuint64_t dims[3] = {128, static_cast<cuuint64_t>(heads), static_cast<cuuint64_t>(tokens)};
     cuuint64_t strides[2] = {256, static_cast<cuuint64_t>(heads) * 256};
     cuuint32_t box[3] = {64, box_heads, box_rows};
@@ -448,7 +441,7 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
     const int64_t total = g->total_tokens * n_kv;
     QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
     const int gq = n_q / n_kv;
-    if (gq * window <= 256 && window <= 256 && !getenv("QVK_SNAPKV_SIMT")) {
+    if (gq * window <= 256 && window <= 256 && !env_knob("QVK_SNAPKV_SIMT", 0)) {
         CUtensorMap mq, mk;
         if (!snap_map(&mq, q, n_q, g->total_tokens, static_cast<uint32_t>(gq), static_cast<uint32_t>(window)) ||
             !snap_map(&mk, k, n_kv, g->total_tokens, 1, 128)) {
@@ -468,9 +461,7 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         sp.rows_pad = (sp.rows + 31) / 32 * 32;
         sp.sl2 = sl2;
         sp.raw = raw;
-        int dev = 0, sms = 0;
-        QVK_CUDA_CHECK(cudaGetDevice(&dev));
-        QVK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int sms = sm_count();
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(static_cast<int64_t>(g->n_groups) * n_kv, sms));
         snapkv_tc_kernel<<<grid, kSnapThreads, kSnapSmem, stream>>>(mq, mk, sp);
         QVK_LAUNCH_CHECK();
