@@ -34,6 +34,6 @@ from .prefill import (  # noqa: F401
     top_k_indices,
 )
 
-from .pipeline import FramePrefill, HostPrefill  # noqa: F401,E402
+from .pipeline import FramePrefill, HostPrefill, StreamingPrefill  # noqa: F401,E402
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -229,3 +229,52 @@ class FramePrefill:
         done_h2d = torch.cuda.Event()
         done_h2d.record(self.h2d)
         main.wait_event(done_h2d)
+
+
+class StreamingPrefill(FramePrefill):
+    """The overlap pipeline of the paper (SPEC.md:462-535 `overlap_pipeline`): a producer — e.g. the
+    CPU video decoder, whose `IntervalHooks::on_done` (decode.hpp:93-99) marks frames ready — submits each group's
+    frames as soon as they are decoded, and the group's upload and kernels are enqueued at once, so decoding group
+    g + 1 on the CPU overlaps prefilling group g on the GPU: t_total ~ max(t_dec + t_prefill(last group),
+    t_prefill + t_dec(first group)).  Groups may be submitted in any order (every group writes its rows at its static
+    cache offset, prefill.cpp:235-238); `finish` reads the cache back once every group has been submitted.
+
+        sp = StreamingPrefill(plan, tpf, H, W, embed, w_qkv, n_q, n_kv, d_h, rho, device)
+        for g, frames in decoder:          # frames: pinned (frames_in_group, 3, H, W) uint8
+            sp.submit(g, frames)
+        sp.finish(out_k, out_v, out_o)
+    """
+
+    def __init__(self, plan: GroupPlan, tokens_per_frame: int, height: int, width: int, embed, w_qkv, n_q: int,
+                 n_kv: int, d_h: int, rho: float, device, cache_rows: int | None = None, row_base: int = 0):
+        super().__init__(plan, tokens_per_frame, height, width, embed, w_qkv, n_q, n_kv, d_h, rho, device,
+                         chunks=plan.n_groups, cache_rows=cache_rows, row_base=row_base)
+        self.submitted = set()
+
+    def submit(self, group: int, frames) -> None:
+        """Enqueue group `group`: its frames (pinned host, the group's frame slots) -> HBM, then its kernels."""
+        if group in self.submitted or not 0 <= group < len(self.parts):
+            raise ValueError(f"group {group} already submitted or out of range")
+        part = self.parts[group]
+        t0, t1 = part[0], part[1]
+        f0, f1 = t0 // self.tpf, t1 // self.tpf
+        if tuple(frames.shape) != tuple(self.frames[f0:f1].shape):
+            raise ValueError("frames do not match the group's frame slots")
+        main = torch.cuda.current_stream(self.dev)
+        e_in = torch.cuda.Event()
+        with torch.cuda.stream(self.h2d):
+            self.frames[f0:f1].copy_(frames, non_blocking=True)
+            e_in.record(self.h2d)
+        main.wait_event(e_in)
+        self._layer(part, main)
+        self.submitted.add(group)
+
+    def finish(self, out_k=None, out_v=None, out_o=None) -> None:
+        if len(self.submitted) != len(self.parts):
+            raise ValueError("not every group was submitted")
+        if out_k is not None:
+            out_k.copy_(self.k_cache, non_blocking=True)
+            out_v.copy_(self.v_cache, non_blocking=True)
+            out_o.copy_(self.origin, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        self.submitted = set()

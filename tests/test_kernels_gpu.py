@@ -641,3 +641,54 @@ def test_frame_prefill_ragged_last_group(cuda):
     torch.cuda.synchronize()
     assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
     assert torch.equal(out_o, buf.origin.cpu())
+
+
+def test_streaming_prefill_overlaps_a_slow_producer(cuda):
+    """Overlap pipeline: groups submitted by a producer thread as they are 'decoded' (a fixed delay per group), in
+    a shuffled order; the result equals the batch path, and the wall time stays close to the producer's time (the
+    GPU work of group g hides under the decoding of group g + 1)."""
+    import threading
+    import time
+    F, fpg, tpf, H, W = 32, 4, 64, 64, 64
+    n_q, n_kv, d_h, d_model, rho = 8, 2, 128, 512, 0.5
+    plan = qp.GroupPlan.plan(F, fpg, tpf, rho, 1)
+    g = plan.to(cuda)
+    fr = _frames(F, H, W, cuda, seed=21)
+    embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(8)) * 2 - 1) / 255).to(cuda)
+    w = (torch.randn((n_q + 2 * n_kv) * d_h, d_model, generator=torch.Generator().manual_seed(9)) /
+         math.sqrt(d_model)).to(torch.bfloat16).to(cuda)
+    buf, _ = qp.prefill_layer_x(qp.tokenize(fr, tpf, embed, bf16=True), w, g, n_q, n_kv, d_h, rho)
+    hf = fr.cpu().pin_memory()
+    sp = qp.StreamingPrefill(plan, tpf, H, W, embed, w, n_q, n_kv, d_h, rho, cuda)
+    order = [3, 0, 7, 1, 6, 2, 5, 4]
+    delay = 0.02
+    ready = []
+    cv = threading.Condition()
+
+    def producer():
+        for gi in order:
+            time.sleep(delay)  # "decode" the group's frames
+            with cv:
+                ready.append(gi)
+                cv.notify()
+
+    t = threading.Thread(target=producer)
+    t0 = time.perf_counter()
+    t.start()
+    done = 0
+    while done < len(order):
+        with cv:
+            while len(ready) <= done:
+                cv.wait()
+            gi = ready[done]
+        sp.submit(gi, hf[gi * fpg:(gi + 1) * fpg])
+        done += 1
+    out_k = torch.empty(sp.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+    out_v = torch.empty_like(out_k).pin_memory()
+    out_o = torch.empty(sp.origin.numel(), dtype=torch.int64).pin_memory()
+    sp.finish(out_k, out_v, out_o)
+    wall = time.perf_counter() - t0
+    t.join()
+    assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
+    assert torch.equal(out_o, buf.origin.cpu())
+    assert wall < len(order) * delay + 0.5, wall  # prefill hidden under the producer (plus a first-launch margin)
