@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     ptx::tc_fence_before();
     cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+    __syncthreads();     // (also orders the allocator's smem write of tmem_base for the CTA-local readers)
     ptx::tc_fence_after();
     const uint32_t tmem = bar->tmem_base;
 
