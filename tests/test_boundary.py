@@ -150,3 +150,31 @@ def test_patch_grid_matches_reference():
             O.ref.qvref_patch_grid(tpf, C.byref(rr), C.byref(cc))
             assert (r.value, c.value) == (rr.value, cc.value)
         assert r.value * c.value == tpf
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5, 8, 16, 17, 64, 225])
+@pytest.mark.parametrize("chunks", [1, 4, 8, "taper"])
+def test_pipeline_chunk_bounds_cover_every_group_once(G, chunks):
+    """Host pipeline chunking (pipeline.chunk_bounds): contiguous, non-empty, ascending, covering [0, G) exactly;
+    'taper' is symmetric-ish with the smallest chunks at both ends."""
+    from paper_2505_16175_b200.pipeline import chunk_bounds
+    b = [int(x) for x in chunk_bounds(G, chunks)]
+    assert b[0] == 0 and b[-1] == G
+    assert all(y > x for x, y in zip(b, b[1:]))
+    if chunks == "taper" and len(b) > 3:
+        sizes = [y - x for x, y in zip(b, b[1:])]
+        assert sizes[0] == min(sizes) and sizes[-1] == min(sizes)
+
+
+def test_c_abi_rejects_bad_arguments_without_a_gpu():
+    """Argument validation of the C ABI runs before any device work (the reference's texts where one exists)."""
+    import ctypes as C
+    lib = qp.lib
+    assert lib.qvk_validate_rho(0.0) == -1 and "retention ratio" in lib.qvk_last_error().decode()
+    assert lib.qvk_validate_rho(0.5) == 0
+    n = C.c_size_t(0)
+    # decode workspace size query is pure host arithmetic; bad shapes are rejected
+    assert lib.qvk_decode_workspace(1, 28, 4, 64, 100, C.byref(n)) == -3  # head_dim 64: unsupported
+    assert lib.qvk_decode_workspace(1, 27, 4, 128, 100, C.byref(n)) == -1  # n_q not a multiple of n_kv
+    assert lib.qvk_decode_workspace(1, 28, 4, 128, 100, C.byref(n)) == 0 and n.value > 0
+    assert lib.qvk_ipc_get_handle(None, None, None) == -1
