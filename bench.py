@@ -402,9 +402,10 @@ def main():
         out_v = torch.empty_like(out_k).pin_memory()
         out_o = torch.empty(buf.origin.numel(), dtype=torch.int64).pin_memory()
 
-        def timed_steps(fn):
+        def timed_steps(fn, join):
             for _ in range(max(1, args.warmup)):
                 fn()
+            join()
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
@@ -412,6 +413,7 @@ def main():
             e0.record(stream)
             for _ in range(args.steps):
                 fn()
+            join()  # the last step's readback is inside the timed region
             e1.record(stream)
             torch.cuda.synchronize()
             t = torch.tensor([e0.elapsed_time(e1)], device=dev)
@@ -437,13 +439,14 @@ def main():
                              chunks=e2e_chunks, cache_rows=plan.total_rows, row_base=row_base)
         gather_f = (lambda: allgather_cache([fp.k_cache, fp.v_cache, fp.origin], bounds, [unit, unit, n_kv])) \
             if world > 1 else None
-        t_f = timed_steps(lambda: fp.run(hframes, out_k, out_v, out_o, after_compute=gather_f))
+        t_f = timed_steps(lambda: fp.run(hframes, out_k, out_v, out_o, after_compute=gather_f, join=False), fp.join)
         e2e = {"value": total_tokens * args.steps / (t_f / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": hframes.numel() * hframes.element_size(), "d2h_bytes_per_step": d2h,
                "path": "FramePrefill (public API, pipeline.py): pinned host video frames (%d x 3 x %d x %d uint8) -> "
                        "qvk_tokenize_bf16 -> qvk_prefill_layer_x (QKV projection GEMM with fused key-norm, attention, "
                        "select+gather) -> pruned cache to pinned host; %s group chunks, copies on two streams "
-                       "overlapped with the kernels" % (n_frames, side, side, e2e_chunks),
+                       "overlapped with the kernels, consecutive steps chained (run(join=False): step i+1's uploads "
+                       "overlap step i's kernels and readback)" % (n_frames, side, side, e2e_chunks),
                "includes": "frames upload, tokenizer, projection GEMM (not in `value`), attention, prune, readback"}
         del fp, hframes, wqkv, embed
         # (2) the same step from host Q/K/V (the `value` step's inputs in pinned host memory; PCIe-bound)
@@ -452,12 +455,12 @@ def main():
                             row_base=row_base)
         gather = (lambda: allgather_cache([hp.k_cache, hp.v_cache, hp.origin], bounds, [unit, unit, n_kv])) \
             if world > 1 else None
-        t_q = timed_steps(lambda: hp.run(hq, hk, hv, out_k, out_v, out_o, after_compute=gather))
+        t_q = timed_steps(lambda: hp.run(hq, hk, hv, out_k, out_v, out_o, after_compute=gather, join=False), hp.join)
         e2e_qkv = {"value": total_tokens * args.steps / (t_q / 1e3), "unit": "tokens/s",
                    "h2d_bytes_per_step": sum(x.numel() * x.element_size() for x in (hq, hk, hv)),
                    "d2h_bytes_per_step": d2h,
                    "path": "HostPrefill: qvk_prefill_layer (C ABI) per 4-group chunk, pinned host Q/K/V in and pruned "
-                           "cache out on two copy streams overlapped with the kernels"}
+                           "cache out on two copy streams overlapped with the kernels, consecutive steps chained"}
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
     fl = flops_attention(sizes, n_q, d)

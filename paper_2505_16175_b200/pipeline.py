@@ -37,7 +37,83 @@ def chunk_bounds(n_groups: int, chunks) -> np.ndarray:
     return np.linspace(0, G, chunks + 1).round().astype(int)
 
 
-class HostPrefill:
+class _Pipeline:
+    """Chunk pipeline shared by HostPrefill / FramePrefill: per chunk, upload (copy stream h2d) -> kernels (the
+    caller's stream) -> readback of the chunk's pruned rows (copy stream d2h).  Dependencies are tracked per chunk
+    with events, not per call, so consecutive calls (the layers or videos of a serving loop) overlap too: call i+1's
+    upload of chunk c waits only for call i's kernels of chunk c (its input slots are free), and call i+1's kernels
+    of chunk c wait only for call i's readback of chunk c (its cache rows are read)."""
+
+    def _init_pipeline(self):
+        self.h2d = torch.cuda.Stream(self.dev)
+        self.d2h = torch.cuda.Stream(self.dev)
+        self._consumed = [None] * len(self.parts)  # main: chunk's kernels done (input slots reusable)
+        self._read = [None] * len(self.parts)      # d2h: chunk's cache rows read back
+        self._tail = []                            # copy-stream events of the last call not yet joined
+        self._chained = False                      # last call ran with join=False
+
+    def join(self, stream=None) -> None:
+        """Make `stream` (default: current) wait for the copies of earlier calls.  run(join=True) does this at its
+        end, so the stream order covers the host outputs; run(join=False) leaves the last readbacks in flight so
+        the next call's uploads and kernels overlap them — call join() (or synchronize) before reading the host
+        outputs of the last call.  A call following a join=False call does not order its uploads after the work
+        already on the caller's stream (that is the overlap): its host inputs must be ready on the host."""
+        s = stream or torch.cuda.current_stream(self.dev)
+        for e in self._tail:
+            s.wait_event(e)
+        self._tail = []
+
+    def _pipeline(self, upload, out_k, out_v, out_o, unit, after_compute, join):
+        main = torch.cuda.current_stream(self.dev)
+        start = torch.cuda.Event()
+        start.record(main)  # inputs / outputs the caller prepared on its stream before this call
+        if not self._chained:
+            self.h2d.wait_event(start)
+        self.d2h.wait_event(start)
+        self._chained = not join
+        per_chunk_out = out_k is not None and after_compute is None
+        for c, part in enumerate(self.parts):
+            r0, r1 = part[2], part[3]
+            e_in = torch.cuda.Event()
+            with torch.cuda.stream(self.h2d):
+                if self._consumed[c] is not None:
+                    self.h2d.wait_event(self._consumed[c])
+                upload(part)
+                e_in.record(self.h2d)
+            main.wait_event(e_in)
+            if self._read[c] is not None:
+                main.wait_event(self._read[c])
+            self._layer(part, main)
+            self._consumed[c] = torch.cuda.Event()
+            self._consumed[c].record(main)
+            if per_chunk_out:
+                self.d2h.wait_event(self._consumed[c])
+                a, b = self.row_base + r0, self.row_base + r1
+                with torch.cuda.stream(self.d2h):
+                    out_k[a * unit:b * unit].copy_(self.k_cache[a * unit:b * unit], non_blocking=True)
+                    out_v[a * unit:b * unit].copy_(self.v_cache[a * unit:b * unit], non_blocking=True)
+                    out_o[a * self.n_kv:b * self.n_kv].copy_(self.origin[a * self.n_kv:b * self.n_kv],
+                                                             non_blocking=True)
+                    self._read[c] = torch.cuda.Event()
+                    self._read[c].record(self.d2h)
+        if after_compute is not None:
+            after_compute()
+            if out_k is not None:  # whole cache on the caller's stream: later kernels are ordered after it
+                out_k.copy_(self.k_cache, non_blocking=True)
+                out_v.copy_(self.v_cache, non_blocking=True)
+                out_o.copy_(self.origin, non_blocking=True)
+            self._read = [None] * len(self.parts)
+        tail = []
+        for s in (self.d2h, self.h2d):
+            e = torch.cuda.Event()
+            e.record(s)
+            tail.append(e)
+        self._tail = tail
+        if join:
+            self.join(main)
+
+
+class HostPrefill(_Pipeline):
     def __init__(self, plan: GroupPlan, n_q: int, n_kv: int, d_h: int, rho: float, device,
                  scorer: Scorer = Scorer.key_norm_small, chunks: int = 4, cache_rows: int | None = None,
                  row_base: int = 0):
@@ -67,8 +143,7 @@ class HostPrefill:
         self.origin = torch.empty(rows * n_kv, dtype=torch.int64, device=self.dev)
         self.row_base = row_base
         self.prm = L.QvkLayerParams(n_q, n_kv, d_h, int(scorer), 1, rho, 1.0 / math.sqrt(d_h), 32, 1)
-        self.h2d = torch.cuda.Stream(self.dev)
-        self.d2h = torch.cuda.Stream(self.dev)
+        self._init_pipeline()
 
     def _layer(self, part, stream):
         t0, t1, r0, r1, g = part
@@ -80,52 +155,22 @@ class HostPrefill:
                                     self.k_cache[cr * unit:].data_ptr(), self.v_cache[cr * unit:].data_ptr(),
                                     self.origin[cr * self.n_kv:].data_ptr()))
 
-    def run(self, hq, hk, hv, out_k=None, out_v=None, out_o=None, after_compute=None):
+    def run(self, hq, hk, hv, out_k=None, out_v=None, out_o=None, after_compute=None, join=True):
         """One pruned-prefill layer from host Q/K/V (pinned, (T, heads, d) bf16) into the device cache; optional
         pinned host outputs receive this rank's pruned rows (or the whole cache when `after_compute` — e.g. the
-        multi-GPU all-gather — runs between the kernels and the readback)."""
-        main = torch.cuda.current_stream(self.dev)
-        start = torch.cuda.Event()
-        start.record(main)
-        self.h2d.wait_event(start)
-        self.d2h.wait_event(start)
+        multi-GPU all-gather — runs between the kernels and the readback).  join=False: see `_Pipeline.join`."""
         unit = self.n_kv * self.d
-        per_chunk_out = out_k is not None and after_compute is None
-        for part in self.parts:
-            t0, t1, r0, r1, _ = part
-            e_in = torch.cuda.Event()
-            with torch.cuda.stream(self.h2d):
-                self.q[t0:t1].copy_(hq[t0:t1], non_blocking=True)
-                self.k[t0:t1].copy_(hk[t0:t1], non_blocking=True)
-                self.v[t0:t1].copy_(hv[t0:t1], non_blocking=True)
-                e_in.record(self.h2d)
-            main.wait_event(e_in)
-            self._layer(part, main)
-            if per_chunk_out:
-                e_out = torch.cuda.Event()
-                e_out.record(main)
-                self.d2h.wait_event(e_out)
-                a, b = self.row_base + r0, self.row_base + r1
-                with torch.cuda.stream(self.d2h):
-                    out_k[a * unit:b * unit].copy_(self.k_cache[a * unit:b * unit], non_blocking=True)
-                    out_v[a * unit:b * unit].copy_(self.v_cache[a * unit:b * unit], non_blocking=True)
-                    out_o[a * self.n_kv:b * self.n_kv].copy_(self.origin[a * self.n_kv:b * self.n_kv],
-                                                             non_blocking=True)
-        if after_compute is not None:
-            after_compute()
-            if out_k is not None:
-                out_k.copy_(self.k_cache, non_blocking=True)
-                out_v.copy_(self.v_cache, non_blocking=True)
-                out_o.copy_(self.origin, non_blocking=True)
-        done = torch.cuda.Event()
-        done.record(self.d2h)
-        main.wait_event(done)
-        done_h2d = torch.cuda.Event()
-        done_h2d.record(self.h2d)
-        main.wait_event(done_h2d)
+
+        def upload(part):
+            t0, t1 = part[0], part[1]
+            self.q[t0:t1].copy_(hq[t0:t1], non_blocking=True)
+            self.k[t0:t1].copy_(hk[t0:t1], non_blocking=True)
+            self.v[t0:t1].copy_(hv[t0:t1], non_blocking=True)
+
+        self._pipeline(upload, out_k, out_v, out_o, unit, after_compute, join)
 
 
-class FramePrefill:
+class FramePrefill(_Pipeline):
     """Video frames in host memory -> one layer's pruned KV cache: the end-to-end path of the reference's
     `prefill(model, tokenize(frames), prune)` (prefill.hpp:86-87, 137-138; prefill.cpp:170-183, 293-323) on the GPU.
 
@@ -170,8 +215,7 @@ class FramePrefill:
         self.origin = torch.empty(rows * n_kv, dtype=torch.int64, device=self.dev)
         self.row_base = row_base
         self.prm = L.QvkLayerParams(n_q, n_kv, d_h, int(Scorer.key_norm_small), 1, rho, 1.0 / math.sqrt(d_h), 32, 1)
-        self.h2d = torch.cuda.Stream(self.dev)
-        self.d2h = torch.cuda.Stream(self.dev)
+        self._init_pipeline()
 
     def _layer(self, part, stream):
         t0, t1, r0, r1, g = part
@@ -188,47 +232,15 @@ class FramePrefill:
                                       self.k_cache[cr * unit:].data_ptr(), self.v_cache[cr * unit:].data_ptr(),
                                       self.origin[cr * self.n_kv:].data_ptr()))
 
-    def run(self, hframes, out_k=None, out_v=None, out_o=None, after_compute=None):
+    def run(self, hframes, out_k=None, out_v=None, out_o=None, after_compute=None, join=True):
         """One layer from pinned host frames (F, 3, H, W) uint8 into the device cache (and optional pinned host
-        outputs, per chunk — or the whole cache after `after_compute`, e.g. the multi-GPU all-gather)."""
-        main = torch.cuda.current_stream(self.dev)
-        start = torch.cuda.Event()
-        start.record(main)
-        self.h2d.wait_event(start)
-        self.d2h.wait_event(start)
-        unit = self.n_kv * self.d
-        per_chunk_out = out_k is not None and after_compute is None
-        for part in self.parts:
-            t0, t1, r0, r1, _ = part
-            f0, f1 = t0 // self.tpf, t1 // self.tpf
-            e_in = torch.cuda.Event()
-            with torch.cuda.stream(self.h2d):
-                self.frames[f0:f1].copy_(hframes[f0:f1], non_blocking=True)
-                e_in.record(self.h2d)
-            main.wait_event(e_in)
-            self._layer(part, main)
-            if per_chunk_out:
-                e_out = torch.cuda.Event()
-                e_out.record(main)
-                self.d2h.wait_event(e_out)
-                a, b = self.row_base + r0, self.row_base + r1
-                with torch.cuda.stream(self.d2h):
-                    out_k[a * unit:b * unit].copy_(self.k_cache[a * unit:b * unit], non_blocking=True)
-                    out_v[a * unit:b * unit].copy_(self.v_cache[a * unit:b * unit], non_blocking=True)
-                    out_o[a * self.n_kv:b * self.n_kv].copy_(self.origin[a * self.n_kv:b * self.n_kv],
-                                                             non_blocking=True)
-        if after_compute is not None:
-            after_compute()
-            if out_k is not None:
-                out_k.copy_(self.k_cache, non_blocking=True)
-                out_v.copy_(self.v_cache, non_blocking=True)
-                out_o.copy_(self.origin, non_blocking=True)
-        done = torch.cuda.Event()
-        done.record(self.d2h)
-        main.wait_event(done)
-        done_h2d = torch.cuda.Event()
-        done_h2d.record(self.h2d)
-        main.wait_event(done_h2d)
+        outputs, per chunk — or the whole cache after `after_compute`, e.g. the multi-GPU all-gather).
+        join=False: see `_Pipeline.join`."""
+        def upload(part):
+            f0, f1 = part[0] // self.tpf, part[1] // self.tpf
+            self.frames[f0:f1].copy_(hframes[f0:f1], non_blocking=True)
+
+        self._pipeline(upload, out_k, out_v, out_o, self.n_kv * self.d, after_compute, join)
 
 
 class StreamingPrefill(FramePrefill):
@@ -263,10 +275,14 @@ class StreamingPrefill(FramePrefill):
         main = torch.cuda.current_stream(self.dev)
         e_in = torch.cuda.Event()
         with torch.cuda.stream(self.h2d):
+            if self._consumed[group] is not None:  # the previous video's kernels of this group read the slots
+                self.h2d.wait_event(self._consumed[group])
             self.frames[f0:f1].copy_(frames, non_blocking=True)
             e_in.record(self.h2d)
         main.wait_event(e_in)
         self._layer(part, main)
+        self._consumed[group] = torch.cuda.Event()
+        self._consumed[group].record(main)
         self.submitted.add(group)
 
     def finish(self, out_k=None, out_v=None, out_o=None) -> None:

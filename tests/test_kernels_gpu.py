@@ -571,6 +571,61 @@ def test_frame_prefill_matches_device_layer(cuda):
     assert torch.equal(fp.o, buf.o)
 
 
+def test_frame_prefill_chained_calls(cuda):
+    """run(join=False) chains consecutive calls (call i+1's uploads and kernels overlap call i's readback): three
+    different videos back to back into three host output sets, each equal to its own device-path result."""
+    F, fpg, tpf, H, W = 24, 4, 64, 64, 64
+    n_q, n_kv, d_h, d_model, rho = 8, 2, 128, 512, 0.5
+    plan = qp.GroupPlan.plan(F, fpg, tpf, rho, 1)
+    g = plan.to(cuda)
+    embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(2)) * 2 - 1) / 255).to(cuda)
+    w = (torch.randn((n_q + 2 * n_kv) * d_h, d_model, generator=torch.Generator().manual_seed(4)) /
+         math.sqrt(d_model)).to(torch.bfloat16).to(cuda)
+    fp = qp.FramePrefill(plan, tpf, H, W, embed, w, n_q, n_kv, d_h, rho, cuda, chunks=3)
+    vids, outs, refs = [], [], []
+    for seed in (31, 32, 33):
+        fr = _frames(F, H, W, cuda, seed=seed)
+        buf, _ = qp.prefill_layer_x(qp.tokenize(fr, tpf, embed, bf16=True), w, g, n_q, n_kv, d_h, rho)
+        refs.append((buf.k_cache.cpu(), buf.v_cache.cpu(), buf.origin.cpu()))
+        vids.append(fr.cpu().pin_memory())
+        ok = torch.empty(fp.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+        outs.append((ok, torch.empty_like(ok).pin_memory(),
+                     torch.empty(fp.origin.numel(), dtype=torch.int64).pin_memory()))
+    torch.cuda.synchronize()
+    for hf, (ok, ov, oo) in zip(vids, outs):
+        fp.run(hf, ok, ov, oo, join=False)
+    fp.join()
+    torch.cuda.synchronize()
+    for (ok, ov, oo), (rk, rv, ro) in zip(outs, refs):
+        assert torch.equal(ok, rk) and torch.equal(ov, rv) and torch.equal(oo, ro)
+
+
+def test_host_prefill_chained_calls(cuda):
+    """HostPrefill.run(join=False) back to back on two Q/K/V sets: each host output set equals its device result."""
+    sizes, n_q, n_kv, rho = [1024, 777, 1024, 1024], 28, 4, 0.5
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    hp = qp.HostPrefill(plan, n_q, n_kv, 128, rho, cuda, chunks=2)
+    ins, outs, refs = [], [], []
+    for s in (0, 10):
+        q = synth_groups(sizes, n_q, 128, 3 + s, False, cuda)
+        k = synth_groups(sizes, n_kv, 128, 1 + s, True, cuda)
+        v = synth_groups(sizes, n_kv, 128, 2 + s, False, cuda)
+        buf = qp.prefill_layer(q, k, v, g, n_q, n_kv, rho)
+        refs.append((buf.k_cache.cpu(), buf.v_cache.cpu(), buf.origin.cpu()))
+        ins.append(tuple(t.cpu().pin_memory() for t in (q, k, v)))
+        ok = torch.empty(hp.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+        outs.append((ok, torch.empty_like(ok).pin_memory(),
+                     torch.empty(hp.origin.numel(), dtype=torch.int64).pin_memory()))
+    torch.cuda.synchronize()
+    for (hq, hk, hv), (ok, ov, oo) in zip(ins, outs):
+        hp.run(hq, hk, hv, ok, ov, oo, join=False)
+    hp.join()
+    torch.cuda.synchronize()
+    for (ok, ov, oo), (rk, rv, ro) in zip(outs, refs):
+        assert torch.equal(ok, rk) and torch.equal(ov, rv) and torch.equal(oo, ro)
+
+
 def test_project_qkv_one_sm_variant(cuda, tmp_path):
     """The 1-SM GEMM variant (QVK_PROJ_2SM=0, read once per process: run in a subprocess) agrees with the default
     2-SM kernel within the bf16 tolerance and its fused key-norm equals qvk_score on its own K bit for bit."""
