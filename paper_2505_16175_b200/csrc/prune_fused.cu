@@ -64,11 +64,17 @@ __device__ __forceinline__ void cluster_sync() {
 #ifdef QVK_PRUNE_TRACE
 // Developer timeline (tools/prune_trace.cu): %globaltimer_lo at the phase boundaries of every CTA.
 __device__ uint32_t* g_prune_trace;
+__device__ uint32_t* g_prune_smid;
 __device__ __forceinline__ void prune_trace(int slot) {
     if (threadIdx.x == 0) {
         uint32_t t;
         asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
         g_prune_trace[blockIdx.x * 8 + slot] = t;
+        if (slot == 0) {
+            uint32_t sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            g_prune_smid[blockIdx.x] = sm;
+        }
     }
 }
 #define QVK_PT(slot) prune_trace(slot)

@@ -66,15 +66,27 @@ def main():
             qp.select(sc, g, H, out=ix)
             qp.gather(k, v, g, H, D, ix, kc, vc, og)
 
-        for f in (fused, separate):
+        def score_only():
+            qp.score(k, v, g, H, D, qp.Scorer.key_norm_small, out=sc)
+
+        def sg_only():
+            qp.select_gather(sc, k, v, g, H, D, ix, kc, vc, og)
+
+        def two_kernels():
+            score_only()
+            sg_only()
+
+        for f in (fused, separate, two_kernels):
             f()
         torch.cuda.synchronize()
         tf, ts = timed(fused, args.reps, flush), timed(separate, args.reps, flush)
+        t2, t_sc, t_sg = (timed(f, args.reps, flush) for f in (two_kernels, score_only, sg_only))
         alg = T * H * (2 * D + 8) + R * H * (6 * D + 12)
         print(json.dumps({"config": name, "G": G, "N": N, "heads": H, "width": D, "rho": rho,
                           "fused_us": tf * 1e3, "separate_us": ts * 1e3, "alg_bytes": alg,
                           "fused_gbs": alg / tf / 1e6, "fused_frac_hbm": alg / tf / 1e6 / hbm,
-                          "separate_gbs": alg / ts / 1e6}), flush=True)
+                          "separate_gbs": alg / ts / 1e6, "score_then_select_gather_us": t2 * 1e3,
+                          "score_us": t_sc * 1e3, "select_gather_us": t_sg * 1e3}), flush=True)
 
 
 if __name__ == "__main__":

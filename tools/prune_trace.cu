@@ -14,6 +14,11 @@
 
 namespace qvk {
 void set_error(const std::string& m) { fprintf(stderr, "qvk error: %s\n", m.c_str()); }
+int env_knob(const char* name, int def) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : def;
+}
+cudaError_t func_attr(const void* f, cudaFuncAttribute a, int v) { return cudaFuncSetAttribute(f, a, v); }
 }
 
 __global__ void fill(__nv_bfloat16* p, size_t n, uint32_t seed) {
@@ -49,6 +54,8 @@ int main(int argc, char** argv) {
     const int ctas = G * H * 16;
     uint32_t* tr; cudaMalloc(&tr, ctas * 8 * 4);
     cudaMemcpyToSymbol(qvk::g_prune_trace, &tr, sizeof(tr));
+    uint32_t* smid; cudaMalloc(&smid, ctas * 4);
+    cudaMemcpyToSymbol(qvk::g_prune_smid, &smid, sizeof(smid));
     void* flush; cudaMalloc(&flush, 256 << 20);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms = 0;
@@ -75,6 +82,24 @@ int main(int argc, char** argv) {
         std::sort(x.begin(), x.end());
         printf("%-14s min %7u  p50 %7u  p90 %7u  max %7u ns\n", names[s], x[0], x[x.size() / 2], x[x.size() * 9 / 10],
                x.back());
+    }
+    // SM load: CTAs per SM, and the scoring time (start -> scored) of CTAs by the load of their SM
+    std::vector<uint32_t> sm(ctas);
+    cudaMemcpy(sm.data(), smid, ctas * 4, cudaMemcpyDeviceToHost);
+    std::vector<int> load(256, 0);
+    for (int c = 0; c < used; ++c) ++load[sm[c]];
+    int sms = 0;
+    for (int i = 0; i < 256; ++i) sms += load[i] > 0;
+    printf("SMs used %d\n", sms);
+    for (int l = 1; l <= 16; ++l) {
+        std::vector<uint32_t> x, y;
+        for (int c = 0; c < used; ++c)
+            if (load[sm[c]] == l) { x.push_back(h[c * 8 + 1] - h[c * 8]); y.push_back(h[c * 8 + 1] - t0); }
+        if (x.empty()) continue;
+        std::sort(x.begin(), x.end());
+        std::sort(y.begin(), y.end());
+        printf("SM load %2d: %4zu CTAs  score dur p50 %6u max %6u | scored at p50 %6u max %6u ns\n", l, x.size(),
+               x[x.size() / 2], x.back(), y[y.size() / 2], y.back());
     }
     return 0;
 }
