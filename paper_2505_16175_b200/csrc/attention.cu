@@ -68,6 +68,35 @@ __device__ long long g_attn_trace[1024];
     } while (0)
 #endif
 
+#ifdef QVK_ATTN_STALLS
+// Debug stall accounting (tools/attn_stalls.cu): clock64 cycles per CTA spent in each barrier wait category.
+//   0 MMA: q_full  1 MMA: kv_full  2 MMA: o_free  3 MMA: p_full  4 MMA: loop total  5 units (MMA)
+//   6 softmax tile 0 (warp 0 lane 0): s_full   7 epilogue (warp 8 lane 0): l_full + o_done
+__device__ unsigned long long g_attn_stall[1024][8];
+#define QVK_SWAIT(cat, b, ph)                                                                  \
+    do {                                                                                       \
+        const long long _s0 = clock64();                                                       \
+        ptx::mbar_wait((b), (ph));                                                             \
+        if (blockIdx.x < 1024) g_attn_stall[blockIdx.x][(cat)] += clock64() - _s0;             \
+    } while (0)
+#define QVK_SWAIT_T(tid, cat, b, ph)                                                           \
+    do {                                                                                       \
+        const long long _s0 = clock64();                                                       \
+        ptx::mbar_wait((b), (ph));                                                             \
+        if (threadIdx.x == (tid) && blockIdx.x < 1024) g_attn_stall[blockIdx.x][(cat)] += clock64() - _s0; \
+    } while (0)
+#define QVK_STALL_ADD(cat, v) \
+    do {                      \
+        if (blockIdx.x < 1024) g_attn_stall[blockIdx.x][(cat)] += (v); \
+    } while (0)
+#else
+#define QVK_SWAIT(cat, b, ph) ptx::mbar_wait((b), (ph))
+#define QVK_SWAIT_T(tid, cat, b, ph) ptx::mbar_wait((b), (ph))
+#define QVK_STALL_ADD(cat, v) \
+    do {                      \
+    } while (0)
+#endif
+
 struct AttnParams {
     const int64_t* tok_off;
     int n_groups;
@@ -243,9 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t pv_step[2] = {0, 0};  // P publications consumed per tile (p_full phases)
             uint32_t o_units[2] = {0, 0};  // units per tile (o_free phases)
             bool s0_pre = false;           // S0(0) of this unit was issued ahead, during the previous unit's last step
+#ifdef QVK_ATTN_STALLS
+            const long long loop0 = clock64();
+#endif
             auto wait_item = [&](uint32_t it) -> uint32_t {
                 const uint32_t st = it % kStages;
-                ptx::mbar_wait(&bar->kv_full[st], (it / kStages) & 1);
+                QVK_SWAIT(1, &bar->kv_full[st], (it / kStages) & 1);
                 ptx::tc_fence_after();
                 return ring + st * kTileBytes;
             };
@@ -261,15 +293,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int nt[2] = {w.n0, w.n1};
                 const int qb = unit_iter & 1;
                 const uint32_t q_addr = q_base + qb * 2 * kTileBytes;
-                ptx::mbar_wait(&bar->q_full[qb], (unit_iter >> 1) & 1);
+                QVK_SWAIT(0, &bar->q_full[qb], (unit_iter >> 1) & 1);
                 ptx::tc_fence_after();
                 auto issue_s = [&](int t, uint32_t k_addr) { issue_s_at(t, q_addr + t * kTileBytes, k_addr); };
                 // O_t += P_t(j) V(j), in two halves as the softmax publishes P (p_full[t][0], p_full[t][1]).
                 auto issue_pv = [&](int t, uint32_t v_addr, int j) {
-                    if (j == 0) ptx::mbar_wait(&bar->o_free[t], (o_units[t] & 1) ^ 1);
+                    if (j == 0) QVK_SWAIT(2, &bar->o_free[t], (o_units[t] & 1) ^ 1);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        ptx::mbar_wait(&bar->p_full[t][h], pv_step[t] & 1);
+                        QVK_SWAIT(3, &bar->p_full[t][h], pv_step[t] & 1);
                         QVK_TRACE(j * 8 + 1 + 3 * t + h);
                         ptx::tc_fence_after();
 #pragma unroll
@@ -326,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         while (un < p.total_units && !decode_unit(p, un).valid) un += gridDim.x;
                         if (un < p.total_units) {
                             const int qbn = (unit_iter + 1) & 1;
-                            ptx::mbar_wait(&bar->q_full[qbn], ((unit_iter + 1) >> 1) & 1);
+                            QVK_SWAIT(0, &bar->q_full[qbn], ((unit_iter + 1) >> 1) & 1);
                             ptx::tc_fence_after();
                             const uint32_t kn0 = wait_item(item + 2 * w.nkv);
                             issue_s_at(0, q_base + qbn * 2 * kTileBytes, kn0);
@@ -338,7 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 item += 2 * w.nkv;
                 ++unit_iter;
                 s0_pre = next_pre;
+                QVK_STALL_ADD(5, 1);
             }
+#ifdef QVK_ATTN_STALLS
+            QVK_STALL_ADD(4, clock64() - loop0);
+#endif
         }
     } else if (warp >= kEpiWarp0) {
         ptx::setmaxnreg_dec<kRegsEpilogue>();
@@ -353,10 +389,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = 0; t < 2; ++t) {
                 if (t == 1 && !w.n1) continue;
                 const uint32_t ph = t_units[t] & 1;
-                ptx::mbar_wait(&bar->l_full[t], ph);
+                QVK_SWAIT_T(256, 7, &bar->l_full[t], ph);
                 const float inv = 1.f / bar->row_sum[t][row];
                 ptx::mbar_arrive(&bar->l_free[t]);
-                ptx::mbar_wait(&bar->o_done[t], ph);
+                QVK_SWAIT_T(256, 7, &bar->o_done[t], ph);
                 ptx::tc_fence_after();
                 const uint32_t o_col = tmem + lane_off + 256 + t * 128;
                 const int qrow = (t ? w.mt1 : w.mt0) * kBM + row;
@@ -407,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             float m_ref = -INFINITY, l = 0.f;
             for (int j = 0; j < nt; ++j, ++step) {
-                ptx::mbar_wait(&bar->s_full[t], step & 1);
+                QVK_SWAIT_T(0, 6, &bar->s_full[t], step & 1);
                 if (row == 0) QVK_TRACE(512 + t * 256 + j * 8);
                 ptx::tc_fence_after();
                 float x[128];

@@ -1,8 +1,9 @@
-// Developer tool (not part of the product): timeline of one attention CTA.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DQVK_ATTN_TRACE -Iinclude \
-//        -Ipaper_2505_16175_b200/csrc tools/attn_trace.cu -lcuda -o build/attn_trace && build/attn_trace
-// Builds attention.cu with QVK_ATTN_TRACE, runs the C2 shape (16 groups x 4096 tokens, 28/4 heads, d 128) and prints
-// the clock64 stamps CTA 0 (the heaviest query-tile pair of group 0, head 0) recorded per K/V step.
+// Developer tool (not part of the product): where the attention kernel's MMA issuer waits.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DQVK_ATTN_STALLS -Iinclude \
+//        -Ipaper_2505_16175_b200/csrc tools/attn_stalls.cu -lcuda -o build/attn_stalls && build/attn_stalls [G N]
+// Builds attention.cu with QVK_ATTN_STALLS and prints, averaged over CTAs, the cycles per unit the MMA warp spent
+// waiting on each barrier (Q loaded, K/V tile loaded, O released by the epilogue, P published by the softmax), the
+// tile-0 softmax's wait for S, and the epilogue's wait for l / O.
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -52,34 +53,31 @@ int main(int argc, char** argv) {
     qvk_groups grp{G, N, T, T / 2, off_d, off_d, off_d, nullptr};
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (int it = 0; it < 3; ++it) qvk::launch_attention(0, &grp, q, k, v, nq, nkv, d, 0.0883883f, o);
+    void* sym; cudaGetSymbolAddress(&sym, qvk::g_attn_stall);
+    cudaMemset(sym, 0, sizeof(unsigned long long) * 1024 * 8);
     cudaEventRecord(e0);
     int rc = qvk::launch_attention(0, &grp, q, k, v, nq, nkv, d, 0.0883883f, o);
     cudaEventRecord(e1);
-    cudaError_t err = cudaDeviceSynchronize();
+    cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    printf("rc=%d err=%s  %.3f ms  %.1f TFLOP/s\n", rc, cudaGetErrorString(err), ms,
-           G * 4.0 * d * nq * (double)N * (N + 1) / 2 / (ms * 1e-3) / 1e12);
-#ifndef QVK_ATTN_TRACE
-    return 0;
-#else
-    long long tr[1024];
-    cudaMemcpyFromSymbol(tr, qvk::g_attn_trace, sizeof(tr));
-    const long long t0 = tr[1022];
-    printf("  j |  V rdy   P0h0   P0h1  S0iss   P1h0   P1h1  S1iss || sm0:S rdy  max   h0    h1 | sm1:S rdy  max   h0    h1\n");
-    for (int j = 0; j < 32; ++j) {
-        printf("%3d |", j);
-        for (int e = 0; e < 7; ++e) printf(" %6lld", tr[j * 8 + e] ? (tr[j * 8 + e] - t0) : -1);
-        printf(" ||");
-        for (int t = 0; t < 2; ++t) {
-            for (int e = 0; e < 4; ++e) {
-                long long x = tr[512 + t * 256 + j * 8 + e];
-                printf(" %6lld", x ? x - t0 : -1);
-            }
-            printf(" |");
-        }
-        printf("\n");
+    if (rc) { printf("rc %d\n", rc); return 1; }
+    std::vector<unsigned long long> h(1024 * 8);
+    cudaMemcpy(h.data(), sym, h.size() * 8, cudaMemcpyDeviceToHost);
+    double tot[8] = {0};
+    int ctas = 0;
+    for (int c = 0; c < 1024; ++c) {
+        if (!h[c * 8 + 5]) continue;
+        ++ctas;
+        for (int k2 = 0; k2 < 8; ++k2) tot[k2] += h[c * 8 + k2];
     }
-    printf("o_done seen: tile0 %lld tile1 %lld\n", tr[512 + 255] - t0, tr[768 + 255] - t0);
+    const double units = tot[5];
+    const double flops = 4.0 * d * nq * (double)N * (N + 1) / 2 * G;
+    printf("G=%d N=%d: %.3f ms  %.0f TFLOP/s  %d CTAs  %.1f units/CTA  MMA loop %.0f cycles/CTA -> %.0f MHz\n", G, N,
+           ms, flops / ms / 1e9, ctas, units / ctas, tot[4] / ctas, tot[4] / ctas / (ms * 1e3));
+    const char* names[8] = {"MMA q_full", "MMA kv_full", "MMA o_free", "MMA p_full", "MMA loop", "units",
+                            "softmax0 s_full", "epilogue l/o"};
+    for (int k2 = 0; k2 < 8; ++k2)
+        if (k2 != 5) printf("  %-16s %9.0f cycles per unit  (%.1f %% of the MMA loop)\n", names[k2], tot[k2] / units,
+                            100.0 * tot[k2] / tot[4]);
     return 0;
-#endif
 }

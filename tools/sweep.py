@@ -120,7 +120,7 @@ def run(name, c, steps, warmup, dev):
         times["score"].append(e[1].elapsed_time(e[2]))
         times["prune"].append(e[2].elapsed_time(e[3]))
     avg = {k_: statistics.mean(v_) for k_, v_ in times.items()}
-    hbm, tf_burst, _, src = peaks()
+    hbm, tf_burst, tf_sus, src = peaks()
     fl = flops_attention(sizes, n_q, d)
     T, Rr = plan.total_tokens, plan.total_rows
     if rho == 1.0:  # identity copy: K, V rows read and written, origin written
@@ -142,13 +142,15 @@ def run(name, c, steps, warmup, dev):
         "tokens_per_s": T * steps / (wall_ms / 1e3), "ms_per_step": wall_ms / steps,
         "path": "qvk_prefill_layer per layer (prune launched with PDL, overlapping the attention tail)",
         "attention": {"ms": avg["attention"], "tflops": fl / (avg["attention"] / 1e3) / 1e12,
-                      "frac": fl / (avg["attention"] / 1e3) / 1e12 / tf_burst},
+                      "frac": fl / (avg["attention"] / 1e3) / 1e12 / tf_burst,
+                      # the sustained peak (under the power cap) is the denominator for a kernel inside a long step
+                      "frac_sustained": fl / (avg["attention"] / 1e3) / 1e12 / tf_sus if tf_sus else None},
         "prune": {"kernels": "identity gather" if rho == 1.0 else
                   ("snapkv score, then fused select+gather" if snap else "fused score+select+gather"),
                   "ms": avg["score"] + avg["prune"], "bytes": b_score + b_prune,
                   "gbs": gbs(b_score + b_prune, avg["score"] + avg["prune"]),
                   "frac": (gbs(b_score + b_prune, avg["score"] + avg["prune"]) or 0) / hbm},
-        "peaks": {"tflops": tf_burst, "hbm_gbs": hbm, "source": src},
+        "peaks": {"tflops": tf_burst, "tflops_sustained": tf_sus, "hbm_gbs": hbm, "source": src},
     }
     if snap:
         out["snapkv_score"] = {"ms": avg["score"], "bytes": b_score, "gbs": gbs(b_score, avg["score"]),
