@@ -107,6 +107,73 @@ class ClockSampler:
                 "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("[N/A]", ""))}
 
 
+class NvmlSampler:
+    """SM clock and clock-event reasons polled through NVML every ~1 ms on a background thread: covers a timed
+    region too short for nvidia-smi's 200 ms sampling (a C2 step is ~1.7 ms)."""
+
+    BITS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+            ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+            ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+            ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+            ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, device):
+        import threading
+
+        import torch
+
+        self.ok = False
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = None
+            try:
+                pr = torch.cuda.get_device_properties(device)
+                h = N.nvmlDeviceGetHandleByPciBusId(
+                    "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id))
+            except Exception:
+                h = N.nvmlDeviceGetHandleByIndex(torch.device(device).index or 0)
+            self.N, self.h = N, h
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+            return
+        self.rows = []
+        self.stop_ev = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _run(self):
+        N, h = self.N, self.h
+        while not self.stop_ev.is_set():
+            try:
+                self.rows.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM),
+                                  N.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            time.sleep(0.001)
+
+    def stop(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + getattr(self, "err", "")],
+                    "samples": 0}
+        self.stop_ev.set()
+        self.th.join(timeout=5)
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        reasons = set()
+        for _, r in rows:
+            for name, attr in self.BITS:
+                if r & getattr(self.N, attr, 0):
+                    reasons.add(name)
+        sm = [float(c) for c, _ in rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(rows), "source": "NVML, polled every ~1 ms during the timed region"}
+
+
 # ------------------------------------------------------------------------------------------------ CPU baseline
 def cpu_sample(seconds: float, cores: int):
     """Bounded CPU sample of the same workload on the host cores: the reference's prune path (oracle/_ref
@@ -272,6 +339,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    nv = NvmlSampler(dev)
     t_start, t_end = ev(), ev()
     t_start.record(stream)
     for _ in range(args.steps):
@@ -279,10 +347,14 @@ def main():
     drain()  # the last layers' all-gathers complete inside the timed region
     t_end.record(stream)
     torch.cuda.synchronize()
+    nv_clocks = nv.stop()
     if world > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     clocks = sampler.stop()
+    if nv_clocks["samples"] >= 3:
+        nv_clocks["nvidia_smi"] = clocks  # the 200 ms nvidia-smi samples over warm-up + timed steps
+        clocks = nv_clocks
     # per-kernel times right after the timed region, before the clock probe below heats the GPU further
     kernel_times(max(10, args.steps))
     torch.cuda.synchronize()
