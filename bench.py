@@ -493,7 +493,9 @@ def main():
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return t.item()
 
-        d2h = sum(x.numel() * x.element_size() for x in (out_k, out_v, out_o))
+        # each rank reads back the pruned rows it computed (the all-gather replicates the cache on the devices,
+        # where the decode step consumes it)
+        d2h = local_plan.total_rows * n_kv * (2 * d * 2 + 8)
         # (1) the user's call from video frames (the reference's prefill(model, tokenize(frames), prune) scope):
         #     pinned host uint8 frames -> GPU tokenizer -> QKV projection (key-norm fused) -> attention -> select +
         #     gather -> pruned cache back to pinned host, per 4-group chunk with both copies overlapped

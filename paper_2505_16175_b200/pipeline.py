@@ -71,7 +71,6 @@ class _Pipeline:
             self.h2d.wait_event(start)
         self.d2h.wait_event(start)
         self._chained = not join
-        per_chunk_out = out_k is not None and after_compute is None
         for c, part in enumerate(self.parts):
             r0, r1 = part[2], part[3]
             e_in = torch.cuda.Event()
@@ -86,7 +85,7 @@ class _Pipeline:
             self._layer(part, main)
             self._consumed[c] = torch.cuda.Event()
             self._consumed[c].record(main)
-            if per_chunk_out:
+            if out_k is not None:
                 self.d2h.wait_event(self._consumed[c])
                 a, b = self.row_base + r0, self.row_base + r1
                 with torch.cuda.stream(self.d2h):
@@ -97,12 +96,7 @@ class _Pipeline:
                     self._read[c] = torch.cuda.Event()
                     self._read[c].record(self.d2h)
         if after_compute is not None:
-            after_compute()
-            if out_k is not None:  # whole cache on the caller's stream: later kernels are ordered after it
-                out_k.copy_(self.k_cache, non_blocking=True)
-                out_v.copy_(self.v_cache, non_blocking=True)
-                out_o.copy_(self.origin, non_blocking=True)
-            self._read = [None] * len(self.parts)
+            after_compute()  # e.g. the multi-GPU all-gather: device cache replicated, on the caller's stream
         tail = []
         for s in (self.d2h, self.h2d):
             e = torch.cuda.Event()
@@ -157,8 +151,9 @@ class HostPrefill(_Pipeline):
 
     def run(self, hq, hk, hv, out_k=None, out_v=None, out_o=None, after_compute=None, join=True):
         """One pruned-prefill layer from host Q/K/V (pinned, (T, heads, d) bf16) into the device cache; optional
-        pinned host outputs receive this rank's pruned rows (or the whole cache when `after_compute` — e.g. the
-        multi-GPU all-gather — runs between the kernels and the readback).  join=False: see `_Pipeline.join`."""
+        pinned host outputs (full cache size) receive this rank's pruned rows at their global offsets, chunk by
+        chunk; `after_compute` (e.g. the multi-GPU all-gather) runs on the device after the last chunk's kernels.
+        join=False: see `_Pipeline.join`."""
         unit = self.n_kv * self.d
 
         def upload(part):
@@ -233,9 +228,9 @@ class FramePrefill(_Pipeline):
                                       self.origin[cr * self.n_kv:].data_ptr()))
 
     def run(self, hframes, out_k=None, out_v=None, out_o=None, after_compute=None, join=True):
-        """One layer from pinned host frames (F, 3, H, W) uint8 into the device cache (and optional pinned host
-        outputs, per chunk — or the whole cache after `after_compute`, e.g. the multi-GPU all-gather).
-        join=False: see `_Pipeline.join`."""
+        """One layer from pinned host frames (F, 3, H, W) uint8 into the device cache; optional pinned host outputs
+        receive this rank's pruned rows chunk by chunk; `after_compute` (e.g. the multi-GPU all-gather) runs on the
+        device after the last chunk's kernels.  join=False: see `_Pipeline.join`."""
         def upload(part):
             f0, f1 = part[0] // self.tpf, part[1] // self.tpf
             self.frames[f0:f1].copy_(hframes[f0:f1], non_blocking=True)

@@ -600,6 +600,30 @@ def test_frame_prefill_chained_calls(cuda):
         assert torch.equal(ok, rk) and torch.equal(ov, rv) and torch.equal(oo, ro)
 
 
+def test_frame_prefill_after_compute_hook(cuda):
+    """after_compute (the multi-GPU all-gather in bench.py) runs on the caller's stream after the last chunk's
+    kernels, sees the complete device cache, and the host outputs still receive every computed row."""
+    F, fpg, tpf, H, W = 16, 4, 64, 64, 64
+    n_q, n_kv, d_h, d_model, rho = 8, 2, 128, 512, 0.5
+    plan = qp.GroupPlan.plan(F, fpg, tpf, rho, 1)
+    g = plan.to(cuda)
+    fr = _frames(F, H, W, cuda, seed=41)
+    embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(3)) * 2 - 1) / 255).to(cuda)
+    w = (torch.randn((n_q + 2 * n_kv) * d_h, d_model, generator=torch.Generator().manual_seed(5)) /
+         math.sqrt(d_model)).to(torch.bfloat16).to(cuda)
+    buf, _ = qp.prefill_layer_x(qp.tokenize(fr, tpf, embed, bf16=True), w, g, n_q, n_kv, d_h, rho)
+    fp = qp.FramePrefill(plan, tpf, H, W, embed, w, n_q, n_kv, d_h, rho, cuda, chunks=2)
+    seen = torch.zeros_like(fp.k_cache)
+    out_k = torch.empty(fp.k_cache.numel(), dtype=torch.bfloat16).pin_memory()
+    out_v = torch.empty_like(out_k).pin_memory()
+    out_o = torch.empty(fp.origin.numel(), dtype=torch.int64).pin_memory()
+    fp.run(fr.cpu().pin_memory(), out_k, out_v, out_o, after_compute=lambda: seen.copy_(fp.k_cache))
+    torch.cuda.synchronize()
+    assert torch.equal(seen.cpu(), buf.k_cache.cpu())
+    assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
+    assert torch.equal(out_o, buf.origin.cpu())
+
+
 def test_host_prefill_chained_calls(cuda):
     """HostPrefill.run(join=False) back to back on two Q/K/V sets: each host output set equals its device result."""
     sizes, n_q, n_kv, rho = [1024, 777, 1024, 1024], 28, 4, 0.5
