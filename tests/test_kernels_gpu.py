@@ -209,6 +209,26 @@ def test_prune_properties_full_c2(cuda):
         assert (sets[0.5][gi] == want).all()
 
 
+@pytest.mark.parametrize("n", [65536, 70001])
+def test_prune_maximum_group_sizes_vs_oracle(cuda, n):
+    """The largest group the fused kernel takes (16 CTAs x 4096 rows = 65536 tokens) and one past it (the three
+    separate kernels take over), per KV head, against the oracle's exact select."""
+    H, D, rho = 2, 64, 0.25
+    plan = qp.GroupPlan.from_sizes([n], rho)
+    g = plan.to(cuda)
+    k = synth_groups([n], H, D, 5, True, cuda)
+    v = synth_groups([n], H, D, 6, False, cuda)
+    kc, vc, origin, idx = qp.prune(k, v, g, H, D, qp.Scorer.key_norm_small, rho)
+    kk = plan.keep[0]
+    want = O.select_heads(O.score_norm(f32_of(k), H, D, True), n, H, kk).astype(np.int64)
+    got = idx.view(-1, H).cpu().numpy().astype(np.int64)
+    assert (got == want).all()
+    src = torch.from_numpy(want).to(cuda)
+    heads = torch.arange(H, device=cuda)[None, :]
+    assert torch.equal(k[src, heads].reshape(-1), kc.view(-1))
+    assert torch.equal(v[src, heads].reshape(-1), vc.view(-1))
+
+
 def test_identity_rho_one(cuda):
     sizes = [100, 37]
     plan = qp.GroupPlan.from_sizes(sizes, 1.0)
