@@ -368,6 +368,38 @@ def main():
         clocks = sampler.stop()
         clocks["note"] = "sampled over a 1.2 s run of the same step right after the timed region"
     drain()
+    # ---- N > 1: how much of the cache all-gather the overlap hides (SURVEY.md §8e "exposed vs hidden") ----
+    ag_report = None
+    if world > 1:
+        def timed(fn):
+            for _ in range(2):
+                fn()
+            drain()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            drain()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.item()
+
+        comp_ms = timed(lambda: qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, buffers=bufs[0],
+                                                 cache_row_offset=row_base))
+        ag_ms = timed(lambda: allgather_cache([bufs[0].k_cache, bufs[0].v_cache, bufs[0].origin], bounds,
+                                              [unit, unit, n_kv]))
+        step_ms = elapsed_ms / args.steps
+        exposed = max(0.0, step_ms - comp_ms)
+        recv = (plan.total_rows - local_plan.total_rows) * n_kv * (2 * d * 2 + 8)
+        ag_report = {"allgather_ms_alone": ag_ms, "compute_ms_alone": comp_ms, "step_ms": step_ms,
+                     "exposed_ms": exposed, "hidden_frac": (1.0 - exposed / ag_ms) if ag_ms > 0 else None,
+                     "bytes_received_per_rank_per_step": recv,
+                     "note": "exposed = step - compute-only step (max over ranks); the all-gather of layer l runs on "
+                             "NCCL's stream while layer l+1 computes"}
     attn_ms = [a.elapsed_time(b) for a, b in attn_ev]
     prune_ms = [a.elapsed_time(b) for a, b in prune_ev]
     el = torch.tensor([elapsed_ms, statistics.mean(attn_ms), statistics.mean(prune_ms)], device=dev)
@@ -571,6 +603,7 @@ def main():
                           "algorithmic_bytes": pb, "achieved_gbs": pb / (prune_avg / 1e3) / 1e9,
                           "hbm_peak_gbs": hbm, "frac": pb / (prune_avg / 1e3) / 1e9 / hbm, "traffic": traffic_p},
             "clocks": clocks, "e2e": e2e, "e2e_qkv": e2e_qkv, "gpu_launches": 2 * args.steps,
+            "allgather": ag_report,
             "full_layer": full, "fused_allgather": fused_ag,
         }
         if world == 1 and not args.no_cpu_baseline:
