@@ -65,10 +65,10 @@ int main(int argc, char** argv) {
     long long tr[1024];
     cudaMemcpyFromSymbol(tr, qvk::g_attn_trace, sizeof(tr));
     const long long t0 = tr[1022];
-    printf("  j |  V rdy   P0h0   P0h1  S0iss   P1h0   P1h1  S1iss || sm0:S rdy  max   h0    h1 | sm1:S rdy  max   h0    h1\n");
+    printf("  j |  V rdy   P0h0   P0h1  S0iss   P1h0   P1h1  S1iss  prolog || sm0:S rdy  max   h0    h1 | sm1:S rdy  max   h0    h1\n");
     for (int j = 0; j < 32; ++j) {
         printf("%3d |", j);
-        for (int e = 0; e < 7; ++e) printf(" %6lld", tr[j * 8 + e] ? (tr[j * 8 + e] - t0) : -1);
+        for (int e = 0; e < 8; ++e) printf(" %6lld", tr[j * 8 + e] ? (tr[j * 8 + e] - t0) : -1);
         printf(" ||");
         for (int t = 0; t < 2; ++t) {
             for (int e = 0; e < 4; ++e) {
