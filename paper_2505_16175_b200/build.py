@@ -13,7 +13,6 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
-import shutil
 import subprocess
 import sys
 from pathlib import Path
