@@ -87,6 +87,13 @@ int main(int argc, char** argv) {
     std::vector<uint32_t> sm(ctas);
     cudaMemcpy(sm.data(), smid, ctas * 4, cudaMemcpyDeviceToHost);
     std::vector<int> load(256, 0);
+    std::vector<int> rounds(32, 0);
+    for (int c = 0; c < used; ++c) ++rounds[std::min(31u, sm[c] >> 16)];
+    printf("select rounds per CTA:");
+    for (int r = 0; r < 32; ++r)
+        if (rounds[r]) printf("  %d: %d", r, rounds[r]);
+    printf("\n");
+    for (auto& x : sm) x &= 0xffffu;
     for (int c = 0; c < used; ++c) ++load[sm[c]];
     int sms = 0;
     for (int i = 0; i < 256; ++i) sms += load[i] > 0;
