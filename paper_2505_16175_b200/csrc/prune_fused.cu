@@ -364,6 +364,9 @@ __global__ void __launch_bounds__(kThreads) prune_fused_kernel(
             if (whole) break;
             top = shift - 1;
         }
+#ifdef QVK_PRUNE_TRACE
+        if (threadIdx.x == 0) g_prune_smid[blockIdx.x] |= static_cast<uint32_t>(round) << 16;
+#endif
     }
     // else: every key equal, or k == N: mask = 0 puts all keys in the bucket, the first `need` (= k) by index.
 
