@@ -107,8 +107,8 @@ class ClockSampler:
 
 
 class NvmlSampler:
-    """SM clock and clock-event reasons polled through NVML every ~1 ms on a background thread: covers a timed
-    region too short for nvidia-smi's 200 ms sampling (a C2 step is ~1.7 ms)."""
+    """SM clock and clock-event reasons polled through NVML back to back (~0.5 ms per sample) on a background
+    thread: covers a timed region too short for nvidia-smi's 200 ms sampling (a C2 step is ~1.7 ms)."""
 
     BITS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -152,7 +152,7 @@ class NvmlSampler:
                                   N.nvmlDeviceGetCurrentClocksEventReasons(h)))
             except Exception:
                 pass
-            time.sleep(0.001)
+            time.sleep(0.0002)  # an NVML query itself takes ~0.1-0.5 ms
 
     def stop(self):
         if not self.ok:
@@ -170,7 +170,7 @@ class NvmlSampler:
                     reasons.add(name)
         sm = [float(c) for c, _ in rows]
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
-                "samples": len(rows), "source": "NVML, polled every ~1 ms during the timed region"}
+                "samples": len(rows), "source": "NVML, polled back to back during the timed region"}
 
 
 # ------------------------------------------------------------------------------------------------ CPU baseline
