@@ -154,16 +154,21 @@ __global__ void snap_pool_kernel(const float* __restrict__ raw, const int64_t* _
 //           key tiles — thread-local (thread = TMEM lane = window row);
 //   pass 2  S' = K_t Q_obs^T  (M = 128 keys, N = ceil32(gq W) window rows): per-key sum of the normalised
 //           probabilities — again thread-local (thread = key), so no cross-thread column reduction is needed.
-// Work item = (group, KV head), persistent over items.  320 threads: warps 0-3 / 4-7 = two compute sets (pass 1:
-// M-tile A / B rows; pass 2: the first / second half of the window columns, combined through smem), warp 8 TMA,
-// warp 9 MMA.  TMEM: pass-1 S_A | S_B (256 columns), pass-2 S' (<= 256 columns).
+// Work item = (group, KV head), persistent over items.  576 threads: warps 0-15 = four compute sets of four warps
+// (one warp per TMEM lane quarter each; four warps per SM sub-partition keep the MUFU busy — two were ~50 % idle on
+// latency), warp 16 TMA, warp 17 MMA.  Pass 1: set s takes M-tile s & 1 (window rows 0-127 / 128-255) and key
+// columns 64 (s >> 1) .. +63 of every key tile, each keeping its own running (max, sum) per row, merged once per
+// item; pass 2: set s takes window columns 64 s .. 64 s + 63, the four partial per-key sums combined through smem.
+// TMEM: pass-1 S_A | S_B (256 columns), pass-2 S' (<= 256 columns).
 // Algorithmic bytes per (group, layer): K read once from HBM (pass 2 re-reads it from L2) + the window Q rows +
 // n_kv * N * 8 score bytes.
 constexpr int kSnapStages = 3;
 constexpr uint32_t kSnapChunk = 128 * 128;          // 128 rows x 128 B (one SW128 chunk of a key tile)
 constexpr uint32_t kSnapKTile = 2 * kSnapChunk;      // 128 keys x 128 d bf16
 constexpr uint32_t kSnapQChunk = 256 * 128;          // window-row operand: up to 256 rows x 128 B per d-chunk
-constexpr int kSnapThreads = 320;
+constexpr int kSnapThreads = 576;
+constexpr int kSnapCompute = 512;  // compute threads (warps 0-15)
+constexpr int kSnapTmaWarp = 16, kSnapMmaWarp = 17;
 
 struct SnapShared {
     uint64_t q_full, q_empty, acc_full, acc_empty;
@@ -171,7 +176,8 @@ struct SnapShared {
     uint32_t tmem_base;
     alignas(16) float bias[256];  // per window column: m + log2(l) (log2 domain); +inf for invalid rows
     alignas(16) int pos[256];     // per window column: token position of its query row inside the group (-1: invalid)
-    float part[2][128];    // pass-2 partial sums of the second column half, by key tile parity
+    float2 stat[256];             // pass 1: (m, l) of the key-column half 1 of every window row, merged by half 0
+    float part[2][3][128];        // pass-2 partial sums of column sets 1-3, by key tile parity
 };
 constexpr size_t kSnapSmem = 1024 + 2 * kSnapQChunk + kSnapStages * kSnapKTile + sizeof(SnapShared);
 
@@ -202,20 +208,31 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         ptx::mbar_init(&sh->q_full, 1);
         ptx::mbar_init(&sh->q_empty, 1);
         ptx::mbar_init(&sh->acc_full, 1);
-        ptx::mbar_init(&sh->acc_empty, 256);
+        ptx::mbar_init(&sh->acc_empty, kSnapCompute);
         for (int st = 0; st < kSnapStages; ++st) {
             ptx::mbar_init(&sh->kv_full[st], 1);
             ptx::mbar_init(&sh->kv_empty[st], 1);
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 9) ptx::tmem_alloc<512>(&sh->tmem_base);
+    // Window-operand rows past gq * W are never written by the TMA (its box is exactly gq * W rows) but the
+    // pass-2 MMA (N = rows_pad) and the pass-1 M-tile B read them: zero them once, so their columns of S' are 0 and
+    // exp2(0 * scale - inf) = 0 exactly (stale smem could hold inf / nan bit patterns).
+    if (p.rows < 256) {
+        const int bytes = (256 - p.rows) * 128;
+        for (int b = threadIdx.x * 16; b < bytes; b += kSnapThreads * 16) {
+            *reinterpret_cast<uint4*>(sQ + p.rows * 128 + b) = make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(sQ + kSnapQChunk + p.rows * 128 + b) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        ptx::fence_proxy_async_smem();  // generic-proxy stores -> read by the tensor core (async proxy)
+    }
+    if (warp == kSnapMmaWarp) ptx::tmem_alloc<512>(&sh->tmem_base);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = sh->tmem_base;
 
-    if (warp == 8) {
+    if (warp == kSnapTmaWarp) {
         if (ptx::elect_one()) {  // ===== TMA producer =====
             uint32_t item_no = 0, tile_no = 0;
             for (int it = blockIdx.x; it < items; it += gridDim.x, ++item_no) {
@@ -240,7 +257,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                     }
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == kSnapMmaWarp) {
         if (ptx::elect_one()) {  // ===== MMA issuer =====
             const uint32_t id1 = ptx::idesc_bf16_f32(128, 128, false, false);
             const uint32_t id2 = ptx::idesc_bf16_f32(128, p.rows_pad, false, false);
@@ -280,132 +297,158 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             }
         }
     } else {
-        // ===== compute: warps 0-3 (set 0) and 4-7 (set 1) =====
+        // ===== compute: warps 0-15, set = warp / 4 (four warps, one per TMEM lane quarter) =====
         const int set = warp >> 2, quarter = warp & 3;
         const int i = quarter * 32 + lane;  // TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = p.sl2;
         uint32_t acc_no = 0;
-        const int c_lo = 4 * set;  // pass 2: set s covers window columns [128 s, 128 s + 128) (bias +inf past rows)
-        const int nch = min(4, max(0, (p.rows - 128 * set + 31) / 32));  // 32-column chunks holding window rows
+        const int mt = set & 1, ch = set >> 1;  // pass 1: M-tile (window rows 128 mt ..) and key-column half
+        const int c_lo = 2 * set;               // pass 2: window columns [64 set, 64 set + 64) = 32-col chunks c_lo, +1
+        const int nch = min(2, max(0, (p.rows - 64 * set + 31) / 32));  // chunks holding window rows
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             const int g = it / p.n_kv, hk = it - g * p.n_kv;
             const int64_t t0 = __ldg(p.tok_off + g);
             const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - t0);
             const int nt = (n + 127) / 128;
             // window column c = r * gq + h -> query token position n - W + r (invalid when < 0)
-            const int c_row = set * 128 + i;
+            const int c_row = mt * 128 + i;
             const int my_pos = c_row < p.rows ? n - p.window + c_row / p.gq : -1;
-            // ---- pass 1: row max / sum of window row c_row (set 0: rows 0..127, set 1: rows 128..255) ----
+            // ---- pass 1: running max / sum of window row c_row over key columns [64 ch, 64 ch + 64) of each tile ----
             float m = -INFINITY, l = 0.f;
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
                 ptx::mbar_wait(&sh->acc_full, acc_no & 1);
                 ptx::tc_fence_after();
-                float x[128];
-                const uint32_t col = tmem + lane_off + set * 128;
+                float x[64];
+                const uint32_t col = tmem + lane_off + mt * 128 + ch * 64;
                 QVK_TMEM_LD32F(col + 0, (x + 0));
                 QVK_TMEM_LD32F(col + 32, (x + 32));
-                QVK_TMEM_LD32F(col + 64, (x + 64));
-                QVK_TMEM_LD32F(col + 96, (x + 96));
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&sh->acc_empty);
                 if (my_pos >= 0) {
-                    const int j0 = jt * 128;
-                    if (j0 + 127 > my_pos) {
+                    const int j0 = jt * 128 + ch * 64;
+                    if (j0 > my_pos) continue;  // every key of this half lies after the row: all masked
+                    if (j0 + 63 > my_pos) {
 #pragma unroll
-                        for (int c = 0; c < 128; ++c)
+                        for (int c = 0; c < 64; ++c)
                             if (j0 + c > my_pos) x[c] = -INFINITY;
                     }
                     // four independent max / sum chains (the serial FMNMX / FADD chains were latency-bound)
                     float mx4[4] = {x[0], x[1], x[2], x[3]};
 #pragma unroll
-                    for (int c = 4; c < 128; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], x[c]);
+                    for (int c = 4; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], x[c]);
                     const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
                     const float mn = fmaxf(m, mx * sl2);
-                    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+                    // packed pairs (FFMA2 / FADD2): the same fp32 operations per element, half the instructions
+                    const ptx::f2 sl2x2 = ptx::f2_make(sl2, sl2), nmn2 = ptx::f2_make(-mn, -mn);
+                    ptx::f2 sa = ptx::f2_make(0.f, 0.f), sb = sa;  // (s4[0], s4[1]), (s4[2], s4[3])
 #pragma unroll
-                    for (int c = 0; c < 128; c += 2) {
-                        float e0 = fmaf(x[c], sl2, -mn), e1 = fmaf(x[c + 1], sl2, -mn);
+                    for (int c = 0; c < 64; c += 2) {
+                        float e0, e1;
+                        ptx::f2_split(ptx::f2_fma(ptx::f2_make(x[c], x[c + 1]), sl2x2, nmn2), e0, e1);
                         if ((c & 7) == 0) {
                             ptx::ex2_poly2(e0, e1);  // a quarter of the exponentials on the FMA pipe
                         } else {
                             e0 = ptx::ex2(e0);
                             e1 = ptx::ex2(e1);
                         }
-                        s4[c & 3] += e0;
-                        s4[(c & 3) + 1] += e1;
+                        if (c & 2) sb = ptx::f2_add(sb, ptx::f2_make(e0, e1));
+                        else sa = ptx::f2_add(sa, ptx::f2_make(e0, e1));
                     }
-                    const float sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                    float s0, s1, s2, s3;
+                    ptx::f2_split(sa, s0, s1);
+                    ptx::f2_split(sb, s2, s3);
+                    const float sum = (s0 + s1) + (s2 + s3);
                     l = (m == -INFINITY ? 0.f : l * ptx::ex2(m - mn)) + sum;
                     m = mn;
                 }
             }
-            sh->bias[c_row] = my_pos >= 0 ? m + __log2f(l) : INFINITY;
-            sh->pos[c_row] = my_pos;
-            ptx::named_bar_sync(1, 256);
-            // ---- pass 2: key j = jt*128 + i, columns [32 c_lo, 32 c_hi) of this set ----
+            // merge the two key-column halves of every row: half 1 publishes (m, l), half 0 combines
+            if (ch == 1) sh->stat[c_row] = make_float2(m, l);
+            ptx::named_bar_sync(1, kSnapCompute);
+            if (ch == 0) {
+                const float2 o = sh->stat[c_row];
+                const float mm = fmaxf(m, o.x);
+                const float ll = (m == -INFINITY ? 0.f : l * ptx::ex2(m - mm)) + (o.x == -INFINITY ? 0.f : o.y * ptx::ex2(o.x - mm));
+                sh->bias[c_row] = my_pos >= 0 ? -(mm + __log2f(ll)) : -INFINITY;  // negated: y = x scale + bias
+                sh->pos[c_row] = my_pos;
+            }
+            ptx::named_bar_sync(1, kSnapCompute);
+            // ---- pass 2: key j = jt*128 + i, window columns [64 set, 64 set + 64) ----
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
                 ptx::mbar_wait(&sh->acc_full, acc_no & 1);
                 ptx::tc_fence_after();
                 const int j = jt * 128 + i;
                 const bool edge = jt * 128 + 127 > n - p.window;  // some window rows precede some keys
-                // load this set's four 32-column chunks at once and release the accumulator BEFORE the
-                // exponentials, so the next key tile's MMAs overlap them.  Columns past the window rows (the last
-                // chunk of set 1 beyond rows_pad, inside the 512 allocated) have bias +inf: they add exp2(-inf) = 0.
-                float x[128];
+                // load this set's two 32-column chunks and release the accumulator BEFORE the exponentials, so the
+                // next key tile's MMAs overlap them.  Columns past the window rows (beyond rows_pad, inside the 512
+                // allocated) have bias +inf: they add exp2(-inf) = 0.
+                float x[64];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) QVK_TMEM_LD32F(tmem + lane_off + 256 + 32 * (c_lo + q), (x + 32 * q));
+                for (int q = 0; q < 2; ++q) QVK_TMEM_LD32F(tmem + lane_off + 256 + 32 * (c_lo + q), (x + 32 * q));
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&sh->acc_empty);
-                float a4[4] = {0.f, 0.f, 0.f, 0.f};
+                const ptx::f2 sl2x2 = ptx::f2_make(sl2, sl2);
+                ptx::f2 a01 = ptx::f2_make(0.f, 0.f), a23 = a01;  // (a4[0], a4[1]), (a4[2], a4[3])
+                // y = x * scale - (m + log2 l) of the column's window row, masked where the row precedes the key
+                // (only on `edge` tiles: a warp-uniform branch keeps the compare off the other tiles)
+                auto column4 = [&](const float* xq, const float4 bb, const int* pv, bool masked, bool poly) {
+                    float y0, y1, y2, y3;
+                    ptx::f2_split(ptx::f2_fma(ptx::f2_make(xq[0], xq[1]), sl2x2, ptx::f2_make(bb.x, bb.y)), y0, y1);
+                    ptx::f2_split(ptx::f2_fma(ptx::f2_make(xq[2], xq[3]), sl2x2, ptx::f2_make(bb.z, bb.w)), y2, y3);
+                    if (masked) {
+                        if (j > pv[0]) y0 = -INFINITY;
+                        if (j > pv[1]) y1 = -INFINITY;
+                        if (j > pv[2]) y2 = -INFINITY;
+                        if (j > pv[3]) y3 = -INFINITY;
+                    }
+                    if (poly) {  // a quarter of the exponentials on the FMA pipe
+                        ptx::ex2_poly2(y0, y1);
+                    } else {
+                        y0 = ptx::ex2(y0);
+                        y1 = ptx::ex2(y1);
+                    }
+                    y2 = ptx::ex2(y2);
+                    y3 = ptx::ex2(y3);
+                    a01 = ptx::f2_add(a01, ptx::f2_make(y0, y1));
+                    a23 = ptx::f2_add(a23, ptx::f2_make(y2, y3));
+                };
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 2; ++q) {
                     if (q >= nch) continue;  // warp-uniform: no window rows in this chunk (exp2(-inf) terms)
                     const float4* b4 = reinterpret_cast<const float4*>(sh->bias + 32 * (c_lo + q));
                     const int4* p4 = reinterpret_cast<const int4*>(sh->pos + 32 * (c_lo + q));
+                    if (edge) {
 #pragma unroll
-                    for (int e4 = 0; e4 < 8; ++e4) {
-                        const float4 bb = b4[e4];
-                        const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
-                        int pv[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
-                        if (edge) {
+                        for (int e4 = 0; e4 < 8; ++e4) {
                             const int4 pp = p4[e4];
-                            pv[0] = pp.x;
-                            pv[1] = pp.y;
-                            pv[2] = pp.z;
-                            pv[3] = pp.w;
+                            const int pv[4] = {pp.x, pp.y, pp.z, pp.w};
+                            column4(x + 32 * q + 4 * e4, b4[e4], pv, true, (e4 & 1) == 0);
                         }
-                        float y[4];
+                    } else {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            y[e] = fmaf(x[32 * q + 4 * e4 + e], sl2, -bv[e]);
-                            if (j > pv[e]) y[e] = -INFINITY;
-                        }
-                        if ((e4 & 1) == 0) {  // a quarter of the exponentials on the FMA pipe
-                            ptx::ex2_poly2(y[0], y[1]);
-                            y[2] = ptx::ex2(y[2]);
-                            y[3] = ptx::ex2(y[3]);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) y[e] = ptx::ex2(y[e]);
-                        }
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) a4[e] += y[e];
+                        for (int e4 = 0; e4 < 8; ++e4)
+                            column4(x + 32 * q + 4 * e4, b4[e4], nullptr, false, (e4 & 1) == 0);
                     }
                 }
+                float a4[4];
+                ptx::f2_split(a01, a4[0], a4[1]);
+                ptx::f2_split(a23, a4[2], a4[3]);
                 const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-                if (set) sh->part[jt & 1][i] = acc;
-                ptx::named_bar_sync(2 + quarter, 64);
-                if (!set && j < n) p.raw[p.n_kv * t0 + static_cast<int64_t>(hk) * n + j] = acc + sh->part[jt & 1][i];
+                if (set) sh->part[jt & 1][set - 1][i] = acc;
+                ptx::named_bar_sync(2 + quarter, 128);  // the four sets of this lane quarter
+                if (!set && j < n)
+                    p.raw[p.n_kv * t0 + static_cast<int64_t>(hk) * n + j] =
+                        acc + ((sh->part[jt & 1][0][i] + sh->part[jt & 1][1][i]) + sh->part[jt & 1][2][i]);
             }
-            ptx::named_bar_sync(1, 256);  // bias / pos reused by the next item
+            ptx::named_bar_sync(1, kSnapCompute);  // bias / pos / stat reused by the next item
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 9) {
+    if (warp == kSnapMmaWarp) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem);
     }
