@@ -52,14 +52,20 @@ constexpr int kRegsProducer = 96;
 constexpr float kRescaleThreshold = 8.0f;     // log2 units: rescale O only when a row max grows by > 256x
 
 #ifdef QVK_ATTN_TRACE
-// Debug timeline (tools/attn_trace.cu): clock64 stamps of CTA 0's first (heaviest) unit.
+// Debug timeline (tools/attn_trace.cu): clock64 stamps of CTA 0's first (heaviest) unit.  With
+// QVK_ATTN_TRACE_UNITS=4 the first four units of CTA 0 are traced instead (units of <= 8 K/V steps, e.g. 1024-token
+// groups): unit u's stamps are shifted by 64 slots inside the MMA (0..255) and per-tile softmax (512 + 256 t) areas.
 __device__ long long g_attn_trace[1024];
+#ifndef QVK_ATTN_TRACE_UNITS
+#define QVK_ATTN_TRACE_UNITS 1
+#endif
 #define QVK_TRACE(slot)                                                                   \
     do {                                                                                  \
-        if (blockIdx.x == 0 && unit_iter == 0) {                                          \
+        if (blockIdx.x == 0 && unit_iter < QVK_ATTN_TRACE_UNITS) {                        \
             long long _c;                                                                 \
             asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c));                            \
-            g_attn_trace[(slot)] = _c;                                                    \
+            const int _s = (slot);                                                        \
+            g_attn_trace[_s >= 1000 ? _s : _s + unit_iter * 64] = _c;                     \
         }                                                                                 \
     } while (0)
 #else
@@ -128,6 +134,14 @@ struct Barriers {
 template <int D>
 constexpr size_t smem_bytes() { return (2 * kQBufs + kStages) * tile_bytes<D>() + sizeof(Barriers); }
 
+// Descriptor of the same operand at a byte offset: only the 14-bit start-address field (addr >> 4, bits 0-13)
+// changes and it cannot carry (shared memory < 256 KB), so one 32-bit add on the low word — instead of rebuilding
+// the descriptor (shift, mask, or, ~4 uniform-datapath ops) for each of the 8 k-steps of every MMA.
+__device__ __forceinline__ uint64_t desc_plus(uint64_t d, uint32_t off_bytes) {
+    const uint32_t lo = static_cast<uint32_t>(d) + (off_bytes >> 4);
+    return (d & 0xffffffff00000000ull) | lo;
+}
+__device__ __forceinline__ uint32_t kmajor_off(int kk) { return (kk >> 2) * kChunkBytes + (kk & 3) * 32; }
 __device__ __forceinline__ uint64_t kmajor_desc(uint32_t tile_addr, int kk) {
     // k-step kk (16 elements) of a K-major SW128 tile: chunk kk/4, +32 B per step inside the 128-byte row.
     return ptx::umma_desc_sw128(tile_addr + (kk >> 2) * kChunkBytes + (kk & 3) * 32, 16, 1024);
@@ -283,17 +297,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             // S_t(j) = Q_t K(j)^T into TMEM columns [128 t, 128 t + 128)
             auto issue_s_at = [&](int t, uint32_t qa, uint32_t k_addr) {
+                const uint64_t dq = kmajor_desc(qa, 0), dk = kmajor_desc(k_addr, 0);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
-                    ptx::mma_ss(tmem + t * 128, kmajor_desc(qa, kk), kmajor_desc(k_addr, kk), kIdS, kk > 0);
+                    ptx::mma_ss(tmem + t * 128, desc_plus(dq, kmajor_off(kk)), desc_plus(dk, kmajor_off(kk)), kIdS,
+                                kk > 0);
             };
             for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+                QVK_TRACE(39);  // unit loop top
                 const Unit w = decode_unit(p, u);
                 if (!w.valid) continue;
+                QVK_TRACE(23);  // decoded
                 const int nt[2] = {w.n0, w.n1};
                 const int qb = unit_iter & 1;
                 const uint32_t q_addr = q_base + qb * 2 * kTileBytes;
                 QVK_SWAIT(0, &bar->q_full[qb], (unit_iter >> 1) & 1);
+                QVK_TRACE(31);  // Q ready
                 ptx::tc_fence_after();
                 auto issue_s = [&](int t, uint32_t k_addr) { issue_s_at(t, q_addr + t * kTileBytes, k_addr); };
                 // O_t += P_t(j) V(j), in two halves as the softmax publishes P (p_full[t][0], p_full[t][1]).
@@ -304,9 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         QVK_SWAIT(3, &bar->p_full[t][h], pv_step[t] & 1);
                         QVK_TRACE(j * 8 + 1 + 3 * t + h);
                         ptx::tc_fence_after();
+                        const uint64_t dv = mnmajor_desc(v_addr, 0);
 #pragma unroll
                         for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
-                            ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmajor_desc(v_addr, kk),
+                            ptx::mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, desc_plus(dv, kk * 16 * 128),
                                         kIdPV, (j > 0 || kk > 0) ? 1u : 0u);
                     }
                     ++pv_step[t];
@@ -316,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 };
                 const uint32_t k0 = wait_item(item);
+                QVK_TRACE(15);  // K(0) ready
                 if (!s0_pre) {
                     issue_s(0, k0);
                     ptx::mma_commit(&bar->s_full[0]);
@@ -324,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     issue_s(1, k0);
                     ptx::mma_commit(&bar->s_full[1]);
                 }
+                QVK_TRACE(7);  // S1(0) issued
                 if (w.nkv == 1) ptx::mma_commit(&bar->q_empty[qb]);  // every S of the unit issued
                 ptx::mma_commit(&bar->kv_empty[item % kStages]);
                 bool next_pre = false;
@@ -367,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+                QVK_TRACE((w.nkv - 1) * 8 + 7);  // unit's MMAs all issued
                 item += 2 * w.nkv;
                 ++unit_iter;
                 s0_pre = next_pre;

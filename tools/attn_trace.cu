@@ -2,7 +2,10 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DQVK_ATTN_TRACE -Iinclude \
 //        -Ipaper_2505_16175_b200/csrc tools/attn_trace.cu -lcuda -o build/attn_trace && build/attn_trace
 // Builds attention.cu with QVK_ATTN_TRACE, runs the C2 shape (16 groups x 4096 tokens, 28/4 heads, d 128) and prints
-// the clock64 stamps CTA 0 (the heaviest query-tile pair of group 0, head 0) recorded per K/V step.
+// the clock64 stamps CTA 0 (the heaviest query-tile pair of group 0, head 0) recorded per K/V step.  Add
+// -DQVK_ATTN_TRACE_UNITS=4 (and run e.g. `64 1024`) to trace CTA 0's first four units, rows 8u..8u+7; the `prolog`
+// column of rows 8u..8u+4 holds unit u's prologue stamps (S1(0) issued, K(0) ready, decoded, Q ready, loop top) and
+// row 8u+nkv-1 the time its last MMA was issued.
 #include <cstdio>
 #include <cstdlib>
 #include <string>
