@@ -1,0 +1,63 @@
+"""The C ABI from plain C (examples/c_abi_prune.c: include/qvk.h only, gcc -std=c99): it compiles and links against
+libqvk.so without CUDA headers (CPU), and on the GPU its prune of a small video equals the Python path's bit for bit."""
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2505_16175_b200 as qp
+
+ROOT = Path(__file__).resolve().parent.parent
+LIB = ROOT / "paper_2505_16175_b200" / "lib"
+
+
+def _compile(tmp_path):
+    if shutil.which("gcc") is None or not (LIB / "libqvk.so").exists():
+        pytest.skip("gcc or libqvk.so missing")
+    exe = tmp_path / "c_abi_prune"
+    subprocess.run(["gcc", "-std=c99", "-O2", "-Wall", "-Werror", f"-I{ROOT / 'include'}",
+                    str(ROOT / "examples" / "c_abi_prune.c"), f"-L{LIB}", "-lqvk", f"-Wl,-rpath,{LIB}", "-o",
+                    str(exe)], check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_example_compiles_and_links_without_cuda_headers(tmp_path):
+    _compile(tmp_path)
+
+
+def _lcg_bf16(n):
+    """The example's inputs: one 64-bit LCG, alternating K / V draws, uniform [-1, 1) -> fp32 -> bf16 (RNE)."""
+    s = 0x9e3779b97f4a7c15
+    a, c, m = 6364136223846793005, 1442695040888963407, (1 << 64) - 1
+    draws = np.empty(2 * n, dtype=np.float64)
+    for i in range(2 * n):
+        s = (s * a + c) & m
+        draws[i] = (s >> 11) / 9007199254740992.0 * 2.0 - 1.0
+    u = draws.astype(np.float32).view(np.uint32).astype(np.uint64)
+    b = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    return b[0::2], b[1::2]
+
+
+@pytest.mark.gpu
+def test_c_example_matches_python_path(tmp_path):
+    exe = _compile(tmp_path)
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), str(out)], capture_output=True, text=True, env=dict(os.environ))
+    assert r.returncode == 0, r.stderr
+    frames, fpg, tpf, heads, width, rho = 16, 4, 64, 2, 128, 0.5
+    plan = qp.GroupPlan.plan(frames, fpg, tpf, rho, 1)
+    T, R = plan.total_tokens, plan.total_rows
+    kb, vb = _lcg_bf16(T * heads * width)
+    dev = torch.device("cuda", 0)
+    k = torch.from_numpy(kb.view(np.int16)).view(torch.bfloat16).view(T, heads, width).to(dev)
+    v = torch.from_numpy(vb.view(np.int16)).view(torch.bfloat16).view(T, heads, width).to(dev)
+    kc, vc, origin, idx = qp.prune(k, v, plan.to(dev), heads, width, qp.Scorer.key_norm_small, rho)
+    raw = out.read_bytes()
+    c_idx = np.frombuffer(raw[:R * heads * 4], dtype=np.uint32)
+    c_kc = np.frombuffer(raw[R * heads * 4:], dtype=np.uint16)
+    assert np.array_equal(c_idx, idx[:R * heads].cpu().numpy().astype(np.uint32))
+    assert np.array_equal(c_kc, kc.view(torch.int16).cpu().numpy().view(np.uint16))
