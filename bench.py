@@ -538,7 +538,7 @@ def main():
         embed = ((torch.rand(d_model, 3, generator=torch.Generator().manual_seed(11)) * 2 - 1) / 255).to(dev)
         wqkv = (qp.synth_bf16(1, 8, 0, 0, (n_q + 2 * n_kv) * d, 1, d_model, False, dev).float()
                 * (1.0 / math.sqrt(d_model))).to(torch.bfloat16).view(-1, d_model)
-        e2e_chunks = os.environ.get("QVK_E2E_CHUNKS", "8")  # dev knob: group chunks of the pipeline (n | taper)
+        e2e_chunks = os.environ.get("QVK_E2E_CHUNKS", "4")  # dev knob: group chunks of the pipeline (n | taper)
         e2e_chunks = int(e2e_chunks) if e2e_chunks.isdigit() else e2e_chunks
         fp = qp.FramePrefill(local_plan, c["tokens_per_frame"], side, side, embed, wqkv, n_q, n_kv, d, rho, dev,
                              chunks=e2e_chunks, cache_rows=plan.total_rows, row_base=row_base)
