@@ -483,11 +483,14 @@ int launch_wc(cudaStream_t stream, const qvk_groups* g, const void* x, const dou
     return QVK_OK;
 }
 
-// Cluster size: about kRowsTarget rows per CTA, doubled (up to 16) while the grid would leave SMs idle.
+// Cluster size: about kRowsTarget rows per CTA, doubled (up to 16) while the grid would leave SMs idle: with fewer
+// segments than SMs until ~2 CTAs per SM (C2: 64 segments -> 8-CTA clusters), otherwise only until every SM has a
+// CTA (C3: 256 segments of 1024 rows stay 1 CTA each — select + gather 24.6 vs 30.7 us with 2-CTA clusters).
 int cluster_size(int64_t segs, int64_t max_tokens) {
-    // tuning knobs QVK_PRUNE_ROWS (rows per CTA), QVK_PRUNE_FILL (CTAs per SM)
+    // tuning knobs QVK_PRUNE_ROWS (rows per CTA), QVK_PRUNE_FILL (CTAs per SM when segments < SMs)
     static const int target = std::max(64, env_knob("QVK_PRUNE_ROWS", kRowsTarget));
-    static const int fill = std::max(1, env_knob("QVK_PRUNE_FILL", 2));
+    static const int fill_small = std::max(1, env_knob("QVK_PRUNE_FILL", 2));
+    const int fill = segs < kNumSms ? fill_small : 1;
     int cl = 1;
     while (cl < 16 && max_tokens > static_cast<int64_t>(cl) * target) cl *= 2;
     while (cl < 16 && segs * cl < fill * kNumSms && max_tokens >= static_cast<int64_t>(cl) * 2 * 128) cl *= 2;
