@@ -483,14 +483,17 @@ int launch_wc(cudaStream_t stream, const qvk_groups* g, const void* x, const dou
     return QVK_OK;
 }
 
-// Cluster size: about kRowsTarget rows per CTA, doubled (up to 16) while the grid would leave SMs idle: with fewer
-// segments than SMs until ~2 CTAs per SM (C2: 64 segments -> 8-CTA clusters), otherwise only until every SM has a
-// CTA (C3: 256 segments of 1024 rows stay 1 CTA each — select + gather 24.6 vs 30.7 us with 2-CTA clusters).
-int cluster_size(int64_t segs, int64_t max_tokens) {
-    // tuning knobs QVK_PRUNE_ROWS (rows per CTA), QVK_PRUNE_FILL (CTAs per SM when segments < SMs)
+// Cluster size: about kRowsTarget rows per CTA, doubled (up to 16) while the grid would leave SMs idle.  Scoring
+// launches (which stream every K row) double until ~2 CTAs per SM when there are fewer segments than SMs (C2: 64
+// segments -> 8-CTA clusters, 54 us; one CTA per SM: 56 us); otherwise — and always for select + gather on given
+// scores, where the cluster exchanges outweigh the smaller streams — only until every SM has a CTA (C3: 256
+// segments of 1024 rows stay 1 CTA each, select + gather 24.6 vs 30.7 us with 2-CTA clusters; C2 select + gather
+// 38.9 vs 49.2 us with 4- instead of 16-CTA clusters).
+int cluster_size(int64_t segs, int64_t max_tokens, bool score) {
+    // tuning knobs QVK_PRUNE_ROWS (rows per CTA), QVK_PRUNE_FILL (CTAs per SM of scoring launches, segments < SMs)
     static const int target = std::max(64, env_knob("QVK_PRUNE_ROWS", kRowsTarget));
     static const int fill_small = std::max(1, env_knob("QVK_PRUNE_FILL", 2));
-    const int fill = segs < kNumSms ? fill_small : 1;
+    const int fill = score && segs < kNumSms ? fill_small : 1;
     int cl = 1;
     while (cl < 16 && max_tokens > static_cast<int64_t>(cl) * target) cl *= 2;
     while (cl < 16 && segs * cl < fill * kNumSms && max_tokens >= static_cast<int64_t>(cl) * 2 * 128) cl *= 2;
@@ -501,7 +504,7 @@ template <int W, bool kScore>
 int launch_w(cudaStream_t stream, const qvk_groups* g, const void* x, const double* scores_in, int negate,
              const void* k, const void* v, int heads, double* scores_out, uint32_t* idx, const Dests& dst,
              int ov) {
-    switch (cluster_size(static_cast<int64_t>(g->n_groups) * heads, g->max_tokens)) {
+    switch (cluster_size(static_cast<int64_t>(g->n_groups) * heads, g->max_tokens, kScore)) {
         case 1: return launch_wc<W, 1, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
         case 2: return launch_wc<W, 2, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
         case 4: return launch_wc<W, 4, kScore>(stream, g, x, scores_in, negate, k, v, heads, scores_out, idx, dst, ov);
