@@ -39,7 +39,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     hbm = 6650.0
     cfgs = [("C2", 16, 4096, 4, 128, 0.5), ("C4-layer", 225, 4096, 4, 128, 0.5), ("C3", 64, 1024, 4, 128, 0.25),
-            ("C5-g64", 4, 16384, 4, 128, 0.125), ("C1", 4, 256, 2, 64, 0.5), ("per-token", 16, 4096, 1, 512, 0.5)]
+            ("C5-g64", 4, 16384, 4, 128, 0.125), ("C1", 4, 256, 2, 64, 0.5), ("per-token", 16, 4096, 1, 512, 0.5),
+            ("per-token-256", 16, 4096, 1, 256, 0.5), ("per-token-C4", 225, 4096, 1, 512, 0.5)]
     for name, G, N, H, D, rho in cfgs:
         if args.only and name != args.only:
             continue
