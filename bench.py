@@ -107,8 +107,9 @@ class ClockSampler:
 
 
 class NvmlSampler:
-    """SM clock and clock-event reasons polled through NVML back to back (~0.5 ms per sample) on a background
-    thread: covers a timed region too short for nvidia-smi's 200 ms sampling (a C2 step is ~1.7 ms)."""
+    """SM clock and clock-event reasons polled through NVML back to back (~0.25 ms per sample) on a background
+    thread started before the warm-up, each sample stamped with the host clock; `window(t0, t1)` keeps the samples
+    taken inside the timed region (a C2 step is ~1.7 ms — far below nvidia-smi's 200 ms sampling)."""
 
     BITS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -122,6 +123,7 @@ class NvmlSampler:
         import torch
 
         self.ok = False
+        self.err = ""
         try:
             import pynvml as N
 
@@ -148,21 +150,25 @@ class NvmlSampler:
         N, h = self.N, self.h
         while not self.stop_ev.is_set():
             try:
-                self.rows.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM),
-                                  N.nvmlDeviceGetCurrentClocksEventReasons(h)))
-            except Exception:
-                pass
+                c = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((time.perf_counter(), c, r))
+            except Exception as e:  # noqa: BLE001
+                self.err = repr(e)
             time.sleep(0.0002)  # an NVML query itself takes ~0.1-0.5 ms
 
     def stop(self):
+        if self.ok:
+            self.stop_ev.set()
+            self.th.join(timeout=5)
+
+    def window(self, t0, t1):
         if not self.ok:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + getattr(self, "err", "")],
-                    "samples": 0}
-        self.stop_ev.set()
-        self.th.join(timeout=5)
-        rows = self.rows
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable: " + self.err], "samples": 0}
+        rows = [(c, r) for t, c, r in list(self.rows) if t0 <= t <= t1]
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "note": "no NVML sample inside the timed region" + (": " + self.err if self.err else "")}
         reasons = set()
         for _, r in rows:
             for name, attr in self.BITS:
@@ -170,7 +176,7 @@ class NvmlSampler:
                     reasons.add(name)
         sm = [float(c) for c, _ in rows]
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
-                "samples": len(rows), "source": "NVML, polled back to back during the timed region"}
+                "samples": len(rows), "source": "NVML, polled back to back; samples stamped inside the timed region"}
 
 
 # ------------------------------------------------------------------------------------------------ CPU baseline
@@ -333,12 +339,13 @@ def main():
             prune_ev.append((a1, p1))
 
     sampler = ClockSampler(local)
+    nv = NvmlSampler(dev)  # polling from before the warm-up; only the samples inside the timed region are kept
     for _ in range(args.warmup):
         step()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    nv = NvmlSampler(dev)
+    h0 = time.perf_counter()
     t_start, t_end = ev(), ev()
     t_start.record(stream)
     for _ in range(args.steps):
@@ -346,7 +353,9 @@ def main():
     drain()  # the last layers' all-gathers complete inside the timed region
     t_end.record(stream)
     torch.cuda.synchronize()
-    nv_clocks = nv.stop()
+    h1 = time.perf_counter()
+    nv.stop()
+    nv_clocks = nv.window(h0, h1)
     if world > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
@@ -354,6 +363,8 @@ def main():
     if nv_clocks["samples"] >= 3:
         nv_clocks["nvidia_smi"] = clocks  # the 200 ms nvidia-smi samples over warm-up + timed steps
         clocks = nv_clocks
+    else:
+        clocks["nvml"] = nv_clocks
     # per-kernel times right after the timed region, before the clock probe below heats the GPU further
     kernel_times(max(10, args.steps))
     torch.cuda.synchronize()
@@ -364,8 +375,11 @@ def main():
             for _ in range(20):
                 step()
             torch.cuda.synchronize()
+        nvml_info = clocks.get("nvml")
         clocks = sampler.stop()
         clocks["note"] = "sampled over a 1.2 s run of the same step right after the timed region"
+        if nvml_info is not None:
+            clocks["nvml"] = nvml_info
     drain()
     # ---- N > 1: how much of the cache all-gather the overlap hides (SURVEY.md §8e "exposed vs hidden") ----
     ag_report = None
