@@ -166,10 +166,22 @@ constexpr int kSnapStages = 3;
 constexpr uint32_t kSnapChunk = 128 * 128;          // 128 rows x 128 B (one SW128 chunk of a key tile)
 constexpr uint32_t kSnapKTile = 2 * kSnapChunk;      // 128 keys x 128 d bf16
 constexpr uint32_t kSnapQChunk = 256 * 128;          // window-row operand: up to 256 rows x 128 B per d-chunk
+#ifndef QVK_SNAP_POLY
+#define QVK_SNAP_POLY 2  // share of the exponentials on the FMA pipe: 0 (none), 2 (1/4), 4 (1/2); see kSnapPolyPass1
+#endif
 constexpr int kSnapThreads = 576;
 constexpr int kSnapCompute = 512;  // compute threads (warps 0-15)
 constexpr int kSnapTmaWarp = 16, kSnapMmaWarp = 17;
 
+// Share of the exponentials computed on the FMA pipe (ex2_poly2) instead of the MUFU.  Pass 1 handles pairs c, c+1
+// (c even, 32 pairs per 64 columns); pass 2 handles groups of 4 whose first pair may go to the FMA pipe.
+//   QVK_SNAP_POLY 2: 1/4 of pass-1 pairs (c % 8 == 0) and 1/4 of pass-2 elements (e4 even) — the default.
+__host__ __device__ constexpr bool kSnapPolyPass1(int c) {
+    return QVK_SNAP_POLY == 0 ? false : QVK_SNAP_POLY == 4 ? (c & 3) == 0 : (c & 7) == 0;
+}
+__host__ __device__ constexpr bool kSnapPolyPass2(int e4) {
+    return QVK_SNAP_POLY == 0 ? false : QVK_SNAP_POLY == 4 ? true : (e4 & 1) == 0;
+}
 struct SnapShared {
     uint64_t q_full, q_empty, acc_full, acc_empty;
     uint64_t kv_full[kSnapStages], kv_empty[kSnapStages];
@@ -347,8 +359,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                     for (int c = 0; c < 64; c += 2) {
                         float e0, e1;
                         ptx::f2_split(ptx::f2_fma(ptx::f2_make(x[c], x[c + 1]), sl2x2, nmn2), e0, e1);
-                        if ((c & 7) == 0) {
-                            ptx::ex2_poly2(e0, e1);  // a quarter of the exponentials on the FMA pipe
+                        if (kSnapPolyPass1(c)) {
+                            ptx::ex2_poly2(e0, e1);  // a share of the exponentials on the FMA pipe
                         } else {
                             e0 = ptx::ex2(e0);
                             e1 = ptx::ex2(e1);
@@ -425,12 +437,12 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                         for (int e4 = 0; e4 < 8; ++e4) {
                             const int4 pp = p4[e4];
                             const int pv[4] = {pp.x, pp.y, pp.z, pp.w};
-                            column4(x + 32 * q + 4 * e4, b4[e4], pv, true, (e4 & 1) == 0);
+                            column4(x + 32 * q + 4 * e4, b4[e4], pv, true, kSnapPolyPass2(e4));
                         }
                     } else {
 #pragma unroll
                         for (int e4 = 0; e4 < 8; ++e4)
-                            column4(x + 32 * q + 4 * e4, b4[e4], nullptr, false, (e4 & 1) == 0);
+                            column4(x + 32 * q + 4 * e4, b4[e4], nullptr, false, kSnapPolyPass2(e4));
                     }
                 }
                 float a4[4];
