@@ -103,6 +103,7 @@ int launch_decode_attention(cudaStream_t, const void*, int, int, int, int, const
 int launch_prune_fused_dests(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const double*,
                              double*, uint32_t*, int, void* const*, void* const*, uint64_t* const*, int);
 bool prune_fused_supported(const qvk_groups*, int, int, const void*, const void*, const void*, const void*);
+bool prune_fused_preferred(const qvk_groups*, int);
 int launch_prune_fused(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const double*,
                        double*, uint32_t*, void*, void*, uint64_t*, int);
 
@@ -275,7 +276,7 @@ int qvk_select_gather(qvk_stream_t s, const qvk_groups* g, const double* scores,
     if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
     if (dtype != QVK_F32 && dtype != QVK_BF16) QVK_INVALID("gather: unsupported dtype");
     if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
-    if (prune_fused_supported(g, dtype, width, k, v, kc, vc))
+    if (prune_fused_supported(g, dtype, width, k, v, kc, vc) && prune_fused_preferred(g, heads))
         return launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores, nullptr, idx, kc, vc, origin, 0);
     uint32_t* ix = idx;
     if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
@@ -295,7 +296,7 @@ int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v,
     if (rho == 1.0)  // prefill.cpp:263-270: identity, no scoring, no shape check
         return gather_checked(s, g, k, v, dtype, heads, width, nullptr, kc, vc, origin, keep_full);
     if ((scorer == QVK_KEY_NORM_SMALL || scorer == QVK_VALUE_NORM) && heads > 0 && width > 0 &&
-        prune_fused_supported(g, dtype, width, k, v, kc, vc)) {
+        prune_fused_supported(g, dtype, width, k, v, kc, vc) && prune_fused_preferred(g, heads)) {
         if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
         // score -> select -> gather in one cluster launch (prune_fused.cu); workspaces receive scores / idx
         return launch_prune_fused(s, g, k, v, heads, width, scorer, nullptr, scores_ws, idx_ws, kc, vc, origin, 0);
@@ -331,7 +332,7 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
     const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
     const int64_t keep_full = static_cast<int64_t>(retained(p->rho, static_cast<size_t>(g->max_tokens)));
     if (p->rho == 1.0) return launch_gather(s, g, k, v, QVK_BF16, heads, width, nullptr, kc, vc, origin, keep_full);
-    const bool fused = prune_fused_supported(g, QVK_BF16, width, k, v, kc, vc);
+    const bool fused = prune_fused_supported(g, QVK_BF16, width, k, v, kc, vc) && prune_fused_preferred(g, heads);
     if (fused && (p->scorer == QVK_KEY_NORM_SMALL || p->scorer == QVK_VALUE_NORM))
         // overlap_prev = 1: the prune only reads K / V, so its CTAs may take the SMs the attention grid releases
         return launch_prune_fused(s, g, k, v, heads, width, p->scorer, nullptr, scores_ws, idx_ws, kc, vc, origin,

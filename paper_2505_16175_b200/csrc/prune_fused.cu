@@ -526,6 +526,14 @@ bool prune_fused_supported(const qvk_groups* g, int dtype, int width, const void
            static_cast<int64_t>(g->n_groups) * 16 < (int64_t(1) << 31) / 8;
 }
 
+// Per-token pruning (heads == 1, the reference's own semantics) of a small batch lands on 16-CTA clusters, which lose
+// to the three separate kernels (16 x 4096 tokens, width 512: 83 vs 60 us; width 256: 49 vs 42 us); from ~32
+// segments on the fused launch wins (225 x 4096, width 512: 510 vs 552 us).  Knob QVK_PRUNE_FUSED_MIN_SEGS.
+bool prune_fused_preferred(const qvk_groups* g, int heads) {
+    static const int min_segs = std::max(0, env_knob("QVK_PRUNE_FUSED_MIN_SEGS", 32));
+    return !(heads == 1 && static_cast<int64_t>(g->n_groups) < min_segs);
+}
+
 // scorer: QVK_KEY_NORM_SMALL / QVK_VALUE_NORM (scores computed here; written to scores_out when non-null) or
 // QVK_SNAPKV = any precomputed scores in scores_in (SnapKV, or the key-norm fused into the projection).
 // overlap_prev: the previous kernel on `stream` does not produce k / v (see the kernel's PDL note).

@@ -6,7 +6,9 @@ double restatement and a torch fp32 reference; SnapKV scores rel 1e-4 (fp32 math
 the oracle's boundary gap is within the stated near-tie band.
 """
 import hashlib
+import os
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -442,6 +444,35 @@ def test_prune_fused_matches_separate_kernels(cuda, sizes, heads, width, rho, ki
         R = plan.total_rows * heads
         assert torch.equal(idx[:R], idx2[:R]), scorer
         assert torch.equal(kc, kc2) and torch.equal(vc, vc2) and torch.equal(origin, origin2), scorer
+
+
+def test_small_per_token_batches_route_to_separate_kernels(cuda, tmp_path):
+    """With the default routing (QVK_PRUNE_FUSED_MIN_SEGS unset: small per-token batches take score + select +
+    gather) qvk_prune gives the same cache as the fused kernel this test process is pinned to."""
+    import subprocess
+    import sys
+    sizes, heads, width, rho = [300, 5, 1000], 1, 512, 0.5
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    k = synth_groups(sizes, heads, width, 1, True, cuda)
+    v = synth_groups(sizes, heads, width, 2, False, cuda)
+    kc, vc, origin, idx = qp.prune(k, v, plan.to(cuda), heads, width, qp.Scorer.key_norm_small, rho)
+    np.save(tmp_path / "kc.npy", kc.view(torch.int16).cpu().numpy())
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import paper_2505_16175_b200 as qp
+from test_kernels_gpu import synth_groups
+dev = torch.device('cuda', 0)
+sizes = [300, 5, 1000]
+plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+k = synth_groups(sizes, 1, 512, 1, True, dev); v = synth_groups(sizes, 1, 512, 2, False, dev)
+kc, vc, origin, idx = qp.prune(k, v, plan.to(dev), 1, 512, qp.Scorer.key_norm_small, 0.5)
+assert np.array_equal(kc.view(torch.int16).cpu().numpy(), np.load(%r))
+print("same")
+""" % (str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent), str(tmp_path / "kc.npy"))
+    env = {kk: vv for kk, vv in os.environ.items() if kk != "QVK_PRUNE_FUSED_MIN_SEGS"}
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0 and "same" in r.stdout, r.stderr[-2000:]
 
 
 def test_prune_fused_extreme_values(cuda):
