@@ -90,6 +90,22 @@ int qvk_score(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, co
               int32_t heads, int32_t width, int32_t scorer, const float* text_query_d, int64_t text_count,
               int32_t n_h, double* scores_d);
 
+/* GQA attention_score (prefill.cpp:213-230 generalised to n_q query / n_kv KV heads):
+ *   qbar[h, j] = (float) sum_t sum_{hq in group(h)} double(text_query[t, hq, j])   (t outer, hq inner)
+ *   per_head = 1: s[i, h] = (sum_{j < d_h} double(k[i, h, j]) * qbar[h, j]) / (T * n_q / n_kv)
+ *   per_head = 0: s[i]    = (sum_{j < n_kv d_h} double(k[i, :, :]) * qbar[:, :]) / (T * n_q)
+ * i.e. the reference's own attention_score applied to the ONE pre-summed text-query row qbar (sum over j in the
+ * reference's sequential double order, bit-identical to qv::score_tokens(k, v, N, n_h, d_h, attention_score, qbar)
+ * up to the divisor), an HBM-bound GEMV instead of the reference's O(N*T*D) loop.  text_query_d (text_count, n_q,
+ * d_h) fp32; k_d (tokens, n_kv, d_h) bf16; qbar_ws_d receives qbar (n_kv * d_h floats; may be NULL = scratch);
+ * scores in the qvk_score layout (heads = per_head ? n_kv : 1).  Errors: "attention_score scorer requires a text
+ * query" when text_count == 0. */
+int qvk_text_query_sum(qvk_stream_t stream, const float* text_query_d, int64_t text_count, int32_t n_q, int32_t n_kv,
+                       int32_t d_h, float* qbar_d);
+int qvk_score_text(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, int32_t n_q, int32_t n_kv,
+                   int32_t d_h, int32_t per_head, const float* text_query_d, int64_t text_count, float* qbar_ws_d,
+                   double* scores_d);
+
 /* SnapKV observation-window scores per KV head: window = the last min(window, N_g) tokens of
  * the group; s[h, j] = sum over the n_q/n_kv query heads of h and the window rows r of causal
  * softmax_j(scale * q_r . k_j); optional average pooling of odd width `pool` (1 = none).  bf16 q/k, fp32 math,
@@ -129,22 +145,27 @@ int qvk_select_gather(qvk_stream_t stream, const qvk_groups* groups, const doubl
 
 /* ---- (a4) per-group causal GQA attention ------------------------------------------------------------------------ */
 /* O[i, h, :] = sum_{j <= i, same group} softmax_j(scale * Q[i,h].K[j,h/(n_q/n_kv)]) V[j, ...]; bf16 in/out, fp32
- * accumulate.  tcgen05/TMEM/TMA kernel; d_h == 128 only (QVK_E_UNSUPPORTED otherwise). */
+ * accumulate.  tcgen05/TMEM/TMA kernel; d_h == 64 or 128 (QVK_E_UNSUPPORTED otherwise). */
 int qvk_attention(qvk_stream_t stream, const qvk_groups* groups, const void* q_d, const void* k_d,
                   const void* v_d, int32_t n_q, int32_t n_kv, int32_t d_h, float scale, void* o_d);
 
 /* ---- one full pruned-prefill layer for all groups of the batch -------------------------------------------------- */
 typedef struct {
     int32_t n_q, n_kv, d_h;   /* GQA shape; K/V rows are (tokens, n_kv, d_h) */
-    int32_t scorer;           /* QVK_KEY_NORM_SMALL / QVK_VALUE_NORM / QVK_SNAPKV */
+    int32_t scorer;           /* QVK_KEY_NORM_SMALL / QVK_VALUE_NORM / QVK_ATTENTION_SCORE / QVK_SNAPKV */
     int32_t per_head;         /* 1: prune each KV head independently (north star (4)); 0: per token (reference) */
     double rho;               /* retention ratio (0, 1] */
     float scale;              /* softmax scale, usually 1/sqrt(d_h) */
     int32_t snap_window, snap_pool;
+    /* QVK_ATTENTION_SCORE only: the text-token queries (text_count, n_q, d_h) fp32 on the device — the reference's
+     * StandInModel::text_query() (prefill.cpp:108-113) in GQA form; scored through qvk_score_text. */
+    const float* text_query_d;
+    int64_t text_count;
 } qvk_layer_params;
 
 /* attention -> score -> select -> gather for one layer.  scores_ws_d: n_kv * tok_off[G] doubles; idx_ws_d:
- * total_rows * n_kv uint32 (NULL -> stream-ordered scratch). */
+ * total_rows * n_kv uint32 (NULL -> stream-ordered scratch).  With rho == 1 (identity, prefill.cpp:263-270) idx_ws_d
+ * receives 0..keep-1 per group like every scored path. */
 int qvk_prefill_layer(qvk_stream_t stream, const qvk_groups* groups, const qvk_layer_params* p, const void* q_d,
                       const void* k_d, const void* v_d, void* o_d, double* scores_ws_d, uint32_t* idx_ws_d,
                       void* k_cache_d, void* v_cache_d, uint64_t* origin_d);
@@ -184,9 +205,49 @@ int qvk_ipc_close(void* base_d);
 int qvk_prune_dests(qvk_stream_t stream, const qvk_groups* groups, const void* k_d, const void* v_d, int32_t heads,
                     int32_t width, int32_t scorer, double rho, double* scores_ws_d, uint32_t* idx_ws_d, int32_t n_dest,
                     void* const* kc_d, void* const* vc_d, uint64_t* const* origin_d);
+/* Device-side barrier after a *_dests call (no host synchronisation): every rank adds 1 to every rank's 32-bit
+ * counter (flags_d: HOST array of the n ranks' counter addresses, own included — qvk_ipc_open mappings; zeroed once)
+ * and waits on the device until its own counter reaches epoch * n (epoch = 1, 2, ... per call); later work on
+ * `stream` then sees every peer's stores.  A rank that does not arrive within QVK_PEER_BARRIER_TIMEOUT_MS (20 s)
+ * sets *err_d to 1 instead of hanging. */
+int qvk_peer_barrier(qvk_stream_t stream, int32_t n, uint32_t* const* flags_d, int32_t self, uint32_t epoch,
+                     uint32_t* err_d);
 int qvk_prefill_layer_dests(qvk_stream_t stream, const qvk_groups* groups, const qvk_layer_params* p, const void* q_d,
                             const void* k_d, const void* v_d, void* o_d, double* scores_ws_d, uint32_t* idx_ws_d,
                             int32_t n_dest, void* const* kc_d, void* const* vc_d, uint64_t* const* origin_d);
+
+/* ---- multi-GPU: the cache all-gather as ONE NCCL collective call over NVLink / NVSwitch ------------------------ */
+/* Groups are independent and every cache offset is a pure function of (rho, N_g), so rank r writes its
+ * groups' pruned rows at their global offsets (qvk_plan_groups rank_begin) and one collective replicates the cache
+ * for the decode step — the reference's single-writer, in-order KvCache (prefill.hpp:132-133) assembled on every
+ * GPU.  NCCL has no all-gather-v, so qvk_allgather_layer issues one in-place ncclBroadcast per source rank and
+ * buffer inside ONE ncclGroupStart/End (a single fused NCCL launch); rank_row_begin (host, world + 1 entries) gives
+ * the first cache row of each rank's segment (row_off[rank_begin[r]]).  k/v caches hold heads * width bf16 per
+ * row, origin heads uint64 per row (may be NULL).  Stream-ordered on `stream`.
+ *   qvk_comm_unique_id   rank 0 creates the 128-byte ncclUniqueId; the caller ships it to the other ranks
+ *   qvk_comm_init        one rank per process on the current device (ncclCommInitRank)
+ *   qvk_comm_init_all    one process driving n_dev GPUs (ncclCommInitAll): comms_out[i] drives devices[i]; wrap
+ *                        the per-device calls in qvk_comm_group_start / qvk_comm_group_end
+ *   qvk_comm_wrap        adopt a caller's ncclComm_t (not destroyed by qvk_comm_destroy)
+ *   qvk_comm_check       ncclCommGetAsyncError: QVK_E_CUDA with NCCL's message after an asynchronous failure */
+typedef struct qvk_comm_st* qvk_comm_t;
+int qvk_comm_unique_id(void* id_out);
+int qvk_comm_init(qvk_comm_t* out, int32_t world, int32_t rank, const void* unique_id);
+int qvk_comm_init_all(qvk_comm_t* comms_out, int32_t n_dev, const int32_t* devices);
+int qvk_comm_wrap(qvk_comm_t* out, void* nccl_comm);
+int qvk_comm_rank(qvk_comm_t comm, int32_t* rank, int32_t* world);
+int qvk_comm_check(qvk_comm_t comm);
+int qvk_comm_destroy(qvk_comm_t comm);
+int qvk_comm_group_start(void);
+int qvk_comm_group_end(void);
+int qvk_allgather_layer(qvk_stream_t stream, qvk_comm_t comm, const int64_t* rank_row_begin, int32_t heads,
+                        int32_t width, void* k_cache_d, void* v_cache_d, uint64_t* origin_d);
+
+/* ---- diagnostics ------------------------------------------------------------------------------------------------ */
+/* Route the last qvk_prune / qvk_prefill_layer* call of this thread took for its prune step: 0 = fused cluster
+ * kernel (score + select + gather in one launch), 1 = separate score / select / gather kernels, 2 = rho == 1
+ * identity copy, 3 = select + gather on precomputed scores (fused), -1 = none yet. */
+int qvk_last_prune_route(void);
 
 /* ---- §8f-4: decode-step consumer of the pruned cache ------------------------------------------------------------- */
 /* O[t, h] = softmax_r(scale * q[t, h] . K[r, h / (n_q/n_kv)]) V[r, ...] over every cache row r (non-causal: the video

@@ -279,3 +279,34 @@ def attention_rows(q, k, v, n_q, n_kv, d, scale, row_begin, row_step):
     o = np.zeros(n * n_q * d, np.float64)
     rows = port.qvo_attention_rows(_np(q), _np(k), _np(v), n, n_q, n_kv, d, scale, row_begin, row_step, _np(o))
     return o.reshape(n, n_q, d), rows
+
+
+# ---------------------------------------------------------------- GQA attention_score (qvk.h qvk_score_text)
+def text_query_sum(q, n_q, n_kv, d):
+    """qbar[h, j] = float32(sum_t sum_{x < n_q/n_kv} double(q[t, h*(n_q/n_kv) + x, j])), t outer, x inner — the text
+    query pre-summed over text tokens and the query heads of each KV head (one double rounding per addition, like
+    numpy's elementwise add)."""
+    q = np.asarray(q, np.float32).reshape(-1, n_q, d)
+    gq = n_q // n_kv
+    acc = np.zeros((n_kv, d), np.float64)
+    for t in range(q.shape[0]):
+        qt = q[t].reshape(n_kv, gq, d).astype(np.float64)
+        for x in range(gq):
+            acc = acc + qt[:, x]
+    return acc.astype(np.float32)
+
+
+def score_text_ref(k, n, n_q, n_kv, d, per_head, qbar, text_count):
+    """GQA attention_score through the UNMODIFIED reference: qvref::score_tokens (prefill.cpp:213-230) on the ONE
+    pre-summed text-query row (n_h = 1, so its divisor is 1 and the result is the sequential double sum itself),
+    per KV-head slice (per_head) or on the flattened n_kv*d row; then divided by T * (n_q/n_kv) or T * n_q.
+    Returns (heads, n) float64."""
+    k = np.asarray(k, np.float32).reshape(n, n_kv, d)
+    qbar = np.asarray(qbar, np.float32).reshape(n_kv, d)
+    if per_head:
+        div = float(text_count) * float(n_q // n_kv)
+        return np.stack([ref_score_tokens(np.ascontiguousarray(k[:, h]), np.ascontiguousarray(k[:, h]), n, 1, d, 2,
+                                          qbar[h]) / div for h in range(n_kv)])
+    div = float(text_count) * float(n_q)
+    flat = np.ascontiguousarray(k.reshape(n, n_kv * d))
+    return (ref_score_tokens(flat, flat, n, 1, n_kv * d, 2, qbar.ravel()) / div)[None]

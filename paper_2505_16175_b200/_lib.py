@@ -42,6 +42,8 @@ class QvkLayerParams(C.Structure):
         ("scale", C.c_float),
         ("snap_window", C.c_int32),
         ("snap_pool", C.c_int32),
+        ("text_query_d", C.c_void_p),
+        ("text_count", C.c_int64),
     ]
 
 
@@ -63,6 +65,20 @@ _SIGS = {
     "qvk_validate_rho": (C.c_int, [F64]),
     "qvk_plan_groups": (C.c_int, [U64, U32, U32, F64, I32, C.POINTER(U64), P, P, P, P]),
     "qvk_score": (C.c_int, [P, GP, P, P, C.c_int, I32, I32, I32, P, I64, I32, P]),
+    "qvk_text_query_sum": (C.c_int, [P, P, I64, I32, I32, I32, P]),
+    "qvk_score_text": (C.c_int, [P, GP, P, I32, I32, I32, I32, P, I64, P, P]),
+    "qvk_comm_unique_id": (C.c_int, [P]),
+    "qvk_comm_init": (C.c_int, [C.POINTER(P), I32, I32, P]),
+    "qvk_comm_init_all": (C.c_int, [P, I32, P]),
+    "qvk_comm_wrap": (C.c_int, [C.POINTER(P), P]),
+    "qvk_comm_rank": (C.c_int, [P, C.POINTER(I32), C.POINTER(I32)]),
+    "qvk_comm_check": (C.c_int, [P]),
+    "qvk_comm_destroy": (C.c_int, [P]),
+    "qvk_comm_group_start": (C.c_int, []),
+    "qvk_comm_group_end": (C.c_int, []),
+    "qvk_allgather_layer": (C.c_int, [P, P, P, I32, I32, P, P, P]),
+    "qvk_last_prune_route": (C.c_int, []),
+    "qvk_peer_barrier": (C.c_int, [P, I32, P, I32, U32, P]),
     "qvk_snapkv_score": (C.c_int, [P, GP, P, P, I32, I32, I32, I32, I32, F32, P]),
     "qvk_select": (C.c_int, [P, GP, P, I32, P]),
     "qvk_gather": (C.c_int, [P, GP, P, P, C.c_int, I32, I32, P, P, P, P]),

@@ -26,9 +26,21 @@ INCLUDE = ROOT / "include"
 REF_INCLUDE = Path(os.environ.get("QV_REF_INCLUDE", "/root/reference/proj/include"))
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> Path:
+    """The NCCL torch bundles (site-packages/nvidia/nccl): linking the same runtime keeps one NCCL per process."""
+    for p in map(Path, sys.path):
+        d = p / "nvidia" / "nccl"
+        if (d / "include" / "nccl.h").exists() and (d / "lib" / "libnccl.so.2").exists():
+            return d
+    raise RuntimeError("nvidia/nccl (torch's NCCL) not found on sys.path")
+
+
+NCCL = _nccl_dir()
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = GENCODE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-                     f"-I{INCLUDE}", f"-I{CSRC}", "-ccbin", "g++"] + os.environ.get("QVK_EXTRA_NVFLAGS", "").split()
+                     f"-I{INCLUDE}", f"-I{CSRC}", f"-I{NCCL / 'include'}", "-ccbin", "g++"] + os.environ.get("QVK_EXTRA_NVFLAGS", "").split()
 CXX = "g++"  # /usr/bin/g++ (the image's CXX variable points at a toolchain without libgomp)
 
 
@@ -60,7 +72,8 @@ def build_qvk(force: bool = False) -> Path:
     out = LIB / "libqvk.so"
     objs = [OBJ / (s.stem + ".o") for s in srcs]
     if force or jobs or _stale(out, objs):
-        _run([NVCC] + GENCODE + ["-shared", "-o", str(out)] + [str(o) for o in objs] + ["-lcudart"])
+        _run([NVCC] + GENCODE + ["-shared", "-o", str(out)] + [str(o) for o in objs] + ["-lcudart", f"-L{NCCL / 'lib'}", "-l:libnccl.so.2",
+                                                                       f"-Xlinker=-rpath={NCCL / 'lib'}"])
     return out
 
 

@@ -36,23 +36,36 @@ cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value) {
 }
 
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t stream) {
+    // A private pool per device (not the device's default pool, which belongs to the whole process): its release
+    // threshold is raised once so freed scratch stays pooled across synchronisations — with the default of 0 every
+    // synchronise returns it to the driver and the next call pays a real allocation (~0.4 ms).
     static std::mutex mu;
-    static std::set<int> pooled;
+    static std::map<int, cudaMemPool_t> pools;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    cudaMemPool_t pool;
     {
         std::lock_guard<std::mutex> lk(mu);
-        if (pooled.insert(dev).second) {
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-                uint64_t keep = UINT64_MAX;
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-            }
+        auto it = pools.find(dev);
+        if (it == pools.end()) {
+            cudaMemPoolProps props = {};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            e = cudaMemPoolCreate(&pool, &props);
+            if (e != cudaSuccess) return e;
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            pools[dev] = pool;
+        } else {
+            pool = it->second;
         }
     }
-    return cudaMallocAsync(p, bytes, stream);
+    return cudaMallocFromPoolAsync(p, bytes, pool, stream);
 }
+
+thread_local int g_route = -1;
 
 int sm_count() {
     static const int n = [] {
@@ -86,7 +99,9 @@ int launch_score(cudaStream_t, const qvk_groups*, int64_t, const void*, const vo
                  const float*, int64_t, int, double*);
 int launch_select(cudaStream_t, const qvk_groups*, const double*, int, uint32_t*);
 int launch_gather(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, const uint32_t*, void*,
-                  void*, uint64_t*, int64_t);
+                  void*, uint64_t*, int64_t, uint32_t*);
+int launch_text_query_sum(cudaStream_t, const float*, int64_t, int, int, int, float*);
+int launch_score_dot(cudaStream_t, const qvk_groups*, const void*, int, int, const float*, double, double*);
 int launch_attention(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, int, float,
                      void*);
 int launch_snapkv(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, int, int, float,
@@ -141,7 +156,8 @@ using namespace qvk;
 extern "C" {
 
 const char* qvk_last_error(void) { return g_last_error.c_str(); }
-int qvk_version(void) { return 1; }
+int qvk_version(void) { return 2; }
+int qvk_last_prune_route(void) { return g_route; }
 
 int qvk_device_count(int* out) {
     QVK_CUDA_CHECK(cudaGetDeviceCount(out));
@@ -256,18 +272,102 @@ int qvk_select(qvk_stream_t s, const qvk_groups* g, const double* scores, int32_
 
 namespace {
 int gather_checked(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
-                   int32_t width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin, int64_t keep_stride) {
+                   int32_t width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin, int64_t keep_stride,
+                   uint32_t* idx_out) {
     QVK_TRY(check_groups(g));
     if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
     if (dtype != QVK_F32 && dtype != QVK_BF16) QVK_INVALID("gather: unsupported dtype");
+    return launch_gather(s, g, k, v, dtype, heads, width, idx, kc, vc, origin, keep_stride, idx_out);
+}
+
+int check_text(const float* tq, int64_t text_count) {
+    if (!tq || text_count <= 0) QVK_INVALID("attention_score scorer requires a text query");  // prefill.cpp:214-215
+    return QVK_OK;
+}
+
+// GQA attention_score (qvk_score_text): qbar = the text queries pre-summed over text tokens and the query heads of
+// each KV head, then the reference's sequential dot product per (token, head) row (score.cu).
+int score_text(cudaStream_t s, const qvk_groups* g, const void* k, int n_q, int n_kv, int d_h, int per_head,
+               const float* tq, int64_t text_count, float* qbar_ws, double* scores) {
+    QVK_TRY(check_text(tq, text_count));
+    if (n_q <= 0 || n_kv <= 0 || d_h <= 0) QVK_INVALID("model config: dimensions must be positive");
+    if (n_q % n_kv != 0) QVK_INVALID("score: n_q must be a multiple of n_kv");
+    float* qb = qbar_ws;
+    if (!qb) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&qb), sizeof(float) * n_kv * d_h, s));
+    int rc = launch_text_query_sum(s, tq, text_count, n_q, n_kv, d_h, qb);
+    // divisor = T * (query heads averaged over): the reference's double(text_count) * n_h (prefill.cpp:228)
+    const double div = static_cast<double>(text_count) * static_cast<double>(per_head ? n_q / n_kv : n_q);
+    if (rc == QVK_OK)
+        rc = per_head ? launch_score_dot(s, g, k, n_kv, d_h, qb, div, scores)
+                      : launch_score_dot(s, g, k, 1, n_kv * d_h, qb, div, scores);
+    if (!qbar_ws) cudaFreeAsync(qb, s);
+    return rc;
+}
+
+// The prune step of one layer (score -> select -> gather into the cache, prefill.cpp:255-282) for every group,
+// after the layer's attention.  pre_scores: scores already computed (the key-norm fused into the projection
+// epilogue); overlap: the previous kernel on the stream only READS k / v (the attention), so a fused launch may
+// start in its tail (PDL).
+int layer_prune(cudaStream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q, const void* k,
+                const void* v, const double* pre_scores, double* scores_ws, uint32_t* idx_ws, void* kc, void* vc,
+                uint64_t* origin, int overlap) {
+    const int heads = p->per_head ? p->n_kv : 1;
+    const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
+    const int64_t keep_full = static_cast<int64_t>(retained(p->rho, static_cast<size_t>(g->max_tokens)));
     if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
-    return launch_gather(s, g, k, v, dtype, heads, width, idx, kc, vc, origin, keep_stride);
+    if (p->rho == 1.0) {  // prefill.cpp:263-270: identity, no scoring
+        g_route = 2;
+        return launch_gather(s, g, k, v, QVK_BF16, heads, width, nullptr, kc, vc, origin, keep_full, idx_ws);
+    }
+    const bool fused = prune_fused_supported(g, QVK_BF16, width, k, v, kc, vc) && prune_fused_preferred(g, heads);
+    const bool norm = p->scorer == QVK_KEY_NORM_SMALL || p->scorer == QVK_VALUE_NORM;
+    if (!pre_scores && norm && fused) {  // score + select + gather in one cluster launch
+        g_route = 0;
+        return launch_prune_fused(s, g, k, v, heads, width, p->scorer, nullptr, scores_ws, idx_ws, kc, vc, origin,
+                                  overlap);
+    }
+    if (!pre_scores && p->scorer == QVK_SNAPKV && !p->per_head)
+        QVK_INVALID("prefill_layer: SnapKV scores are per KV head (set per_head = 1)");
+    if (!pre_scores && p->scorer == QVK_ATTENTION_SCORE) QVK_TRY(check_text(p->text_query_d, p->text_count));
+    if (!pre_scores && !norm && p->scorer != QVK_ATTENTION_SCORE && p->scorer != QVK_SNAPKV)
+        QVK_INVALID("score: unknown scorer");
+    double* sc = scores_ws;
+    uint32_t* ix = idx_ws;
+    if (!pre_scores && !sc)
+        QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&sc),
+                                     sizeof(double) * std::max<int64_t>(1, g->total_tokens * heads), s));
+    int rc = QVK_OK;
+    if (!pre_scores) {
+        if (p->scorer == QVK_SNAPKV)
+            rc = launch_snapkv(s, g, q, k, p->n_q, p->n_kv, p->d_h, p->snap_window, p->snap_pool, p->scale, sc);
+        else if (p->scorer == QVK_ATTENTION_SCORE)
+            rc = score_text(s, g, k, p->n_q, p->n_kv, p->d_h, p->per_head, p->text_query_d, p->text_count, nullptr,
+                            sc);
+        else
+            rc = launch_score(s, g, g->total_tokens, k, v, QVK_BF16, heads, width, p->scorer, nullptr, 0, 1, sc);
+    }
+    const double* scores = pre_scores ? pre_scores : sc;
+    if (rc == QVK_OK && fused) {  // select + gather fused on the given scores
+        g_route = 3;
+        rc = launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores, nullptr, idx_ws, kc, vc, origin,
+                                pre_scores ? overlap : 0);
+    } else if (rc == QVK_OK) {
+        g_route = 1;
+        if (!ix)
+            QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
+                                         sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
+        rc = launch_select(s, g, scores, heads, ix);
+        if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, keep_full, nullptr);
+        if (!idx_ws) cudaFreeAsync(ix, s);
+    }
+    if (!pre_scores && !scores_ws) cudaFreeAsync(sc, s);
+    return rc;
 }
 }  // namespace
 
 int qvk_gather(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v, int dtype, int32_t heads,
                int32_t width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin) {
-    return gather_checked(s, g, k, v, dtype, heads, width, idx, kc, vc, origin, 0);
+    return gather_checked(s, g, k, v, dtype, heads, width, idx, kc, vc, origin, 0, nullptr);
 }
 
 int qvk_select_gather(qvk_stream_t s, const qvk_groups* g, const double* scores, const void* k, const void* v,
@@ -276,13 +376,16 @@ int qvk_select_gather(qvk_stream_t s, const qvk_groups* g, const double* scores,
     if (heads <= 0 || width <= 0) QVK_INVALID("model config: dimensions must be positive");
     if (dtype != QVK_F32 && dtype != QVK_BF16) QVK_INVALID("gather: unsupported dtype");
     if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
-    if (prune_fused_supported(g, dtype, width, k, v, kc, vc) && prune_fused_preferred(g, heads))
+    if (prune_fused_supported(g, dtype, width, k, v, kc, vc) && prune_fused_preferred(g, heads)) {
+        g_route = 3;
         return launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores, nullptr, idx, kc, vc, origin, 0);
+    }
+    g_route = 1;
     uint32_t* ix = idx;
     if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
                                             sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
     int rc = launch_select(s, g, scores, heads, ix);
-    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, dtype, heads, width, ix, kc, vc, origin, 0);
+    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, dtype, heads, width, ix, kc, vc, origin, 0, nullptr);
     if (!idx) cudaFreeAsync(ix, s);
     return rc;
 }
@@ -293,14 +396,18 @@ int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v,
     QVK_TRY(check_rho(rho));  // prefill.cpp:258, validated before anything else
     QVK_TRY(check_groups(g));
     const int64_t keep_full = static_cast<int64_t>(retained(rho, static_cast<size_t>(g->max_tokens)));
-    if (rho == 1.0)  // prefill.cpp:263-270: identity, no scoring, no shape check
-        return gather_checked(s, g, k, v, dtype, heads, width, nullptr, kc, vc, origin, keep_full);
+    if (rho == 1.0) {  // prefill.cpp:263-270: identity, no scoring, no shape check
+        g_route = 2;
+        return gather_checked(s, g, k, v, dtype, heads, width, nullptr, kc, vc, origin, keep_full, idx_ws);
+    }
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
     if ((scorer == QVK_KEY_NORM_SMALL || scorer == QVK_VALUE_NORM) && heads > 0 && width > 0 &&
         prune_fused_supported(g, dtype, width, k, v, kc, vc) && prune_fused_preferred(g, heads)) {
-        if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
         // score -> select -> gather in one cluster launch (prune_fused.cu); workspaces receive scores / idx
+        g_route = 0;
         return launch_prune_fused(s, g, k, v, heads, width, scorer, nullptr, scores_ws, idx_ws, kc, vc, origin, 0);
     }
+    g_route = 1;
     double* sc = scores_ws;
     uint32_t* ix = idx_ws;
     if (!sc) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&sc),
@@ -309,10 +416,25 @@ int qvk_prune(qvk_stream_t s, const qvk_groups* g, const void* k, const void* v,
                                             sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
     int rc = qvk_score(s, g, k, v, dtype, heads, width, scorer, tq, text_count, n_h, sc);
     if (rc == QVK_OK) rc = qvk_select(s, g, sc, heads, ix);
-    if (rc == QVK_OK) rc = gather_checked(s, g, k, v, dtype, heads, width, ix, kc, vc, origin, keep_full);
+    if (rc == QVK_OK) rc = gather_checked(s, g, k, v, dtype, heads, width, ix, kc, vc, origin, keep_full, nullptr);
     if (!scores_ws) cudaFreeAsync(sc, s);
     if (!idx_ws) cudaFreeAsync(ix, s);
     return rc;
+}
+
+int qvk_text_query_sum(qvk_stream_t s, const float* tq, int64_t text_count, int32_t n_q, int32_t n_kv, int32_t d_h,
+                       float* qbar) {
+    QVK_TRY(check_text(tq, text_count));
+    if (n_q <= 0 || n_kv <= 0 || d_h <= 0) QVK_INVALID("model config: dimensions must be positive");
+    if (n_q % n_kv != 0) QVK_INVALID("score: n_q must be a multiple of n_kv");
+    if (!qbar) QVK_INVALID("score: null qbar output");
+    return launch_text_query_sum(s, tq, text_count, n_q, n_kv, d_h, qbar);
+}
+
+int qvk_score_text(qvk_stream_t s, const qvk_groups* g, const void* k, int32_t n_q, int32_t n_kv, int32_t d_h,
+                   int32_t per_head, const float* tq, int64_t text_count, float* qbar_ws, double* scores) {
+    QVK_TRY(check_groups(g));
+    return score_text(s, g, k, n_q, n_kv, d_h, per_head, tq, text_count, qbar_ws, scores);
 }
 
 int qvk_attention(qvk_stream_t s, const qvk_groups* g, const void* q, const void* k, const void* v, int32_t n_q,
@@ -327,40 +449,10 @@ int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_param
     if (!p) QVK_INVALID("prefill_layer: null params");
     QVK_TRY(check_rho(p->rho));
     QVK_TRY(check_groups(g));
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
     QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
-    const int heads = p->per_head ? p->n_kv : 1;
-    const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
-    const int64_t keep_full = static_cast<int64_t>(retained(p->rho, static_cast<size_t>(g->max_tokens)));
-    if (p->rho == 1.0) return launch_gather(s, g, k, v, QVK_BF16, heads, width, nullptr, kc, vc, origin, keep_full);
-    const bool fused = prune_fused_supported(g, QVK_BF16, width, k, v, kc, vc) && prune_fused_preferred(g, heads);
-    if (fused && (p->scorer == QVK_KEY_NORM_SMALL || p->scorer == QVK_VALUE_NORM))
-        // overlap_prev = 1: the prune only reads K / V, so its CTAs may take the SMs the attention grid releases
-        return launch_prune_fused(s, g, k, v, heads, width, p->scorer, nullptr, scores_ws, idx_ws, kc, vc, origin,
-                                  1);
-    double* sc = scores_ws;
-    uint32_t* ix = idx_ws;
-    if (!sc) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&sc),
-                                            sizeof(double) * std::max<int64_t>(1, g->total_tokens * heads), s));
-    if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
-                                            sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
-    int rc;
-    if (p->scorer == QVK_SNAPKV) {
-        rc = p->per_head ? launch_snapkv(s, g, q, k, p->n_q, p->n_kv, p->d_h, p->snap_window, p->snap_pool, p->scale,
-                                         sc)
-                         : (set_error("prefill_layer: SnapKV scores are per KV head (set per_head = 1)"),
-                            QVK_E_INVALID);
-    } else {
-        rc = qvk_score(s, g, k, v, QVK_BF16, heads, width, p->scorer, nullptr, 0, p->n_kv, sc);
-    }
-    if (rc == QVK_OK && fused && p->scorer == QVK_SNAPKV)  // select + gather fused, scores from snapkv.cu
-        rc = launch_prune_fused(s, g, k, v, heads, width, p->scorer, sc, nullptr, idx_ws, kc, vc, origin, 0);
-    else if (rc == QVK_OK) {
-        rc = launch_select(s, g, sc, heads, ix);
-        if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, keep_full);
-    }
-    if (!scores_ws) cudaFreeAsync(sc, s);
-    if (!idx_ws) cudaFreeAsync(ix, s);
-    return rc;
+    // overlap = 1: the fused prune only reads K / V, so its CTAs may take the SMs the attention grid releases
+    return layer_prune(s, g, p, q, k, v, nullptr, scores_ws, idx_ws, kc, vc, origin, 1);
 }
 
 int qvk_project_qkv(qvk_stream_t s, const void* x, int64_t tokens, int32_t d_model, const void* w, int32_t n_q,
@@ -377,22 +469,13 @@ int qvk_prefill_layer_x(qvk_stream_t s, const qvk_groups* g, const qvk_layer_par
     QVK_TRY(check_rho(p->rho));
     QVK_TRY(check_groups(g));
     if (!scores_ws) QVK_INVALID("prefill_layer_x: scores workspace required");
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
     const bool fused_norm = p->scorer == QVK_KEY_NORM_SMALL && p->per_head && p->rho != 1.0;
     QVK_TRY(launch_project_qkv(s, x, g->total_tokens, d_model, w, p->n_q, p->n_kv, p->d_h, q, k, v, g,
                                fused_norm ? scores_ws : nullptr));
-    if (!fused_norm) return qvk_prefill_layer(s, g, p, q, k, v, o, scores_ws, idx_ws, kc, vc, origin);
     QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
-    const int heads = p->n_kv, width = p->d_h;
-    if (prune_fused_supported(g, QVK_BF16, width, k, v, kc, vc))  // scores came from the projection epilogue
-        return launch_prune_fused(s, g, k, v, heads, width, QVK_SNAPKV, scores_ws, nullptr, idx_ws, kc, vc, origin,
-                                  1);
-    uint32_t* ix = idx_ws;
-    if (!ix) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&ix),
-                                            sizeof(uint32_t) * std::max<int64_t>(1, g->total_rows * heads), s));
-    int rc = launch_select(s, g, scores_ws, heads, ix);
-    if (rc == QVK_OK) rc = launch_gather(s, g, k, v, QVK_BF16, heads, width, ix, kc, vc, origin, 0);
-    if (!idx_ws) cudaFreeAsync(ix, s);
-    return rc;
+    // key-norm scores came from the projection epilogue: select + gather only, in the attention's tail
+    return layer_prune(s, g, p, q, k, v, fused_norm ? scores_ws : nullptr, scores_ws, idx_ws, kc, vc, origin, 1);
 }
 
 int qvk_decode_workspace(int32_t n_tq, int32_t n_q, int32_t n_kv, int32_t d_h, int64_t rows, size_t* bytes) {
@@ -459,6 +542,7 @@ int qvk_prune_dests(qvk_stream_t s, const qvk_groups* g, const void* k, const vo
         set_error("prune_dests: needs rho < 1, a norm scorer and bf16 rows of 64/128/256/512");
         return QVK_E_UNSUPPORTED;
     }
+    g_route = 0;
     return launch_prune_fused_dests(s, g, k, v, heads, width, scorer, nullptr, scores_ws, idx_ws, n_dest, kc, vc,
                                     origin, 0);
 }
@@ -470,6 +554,7 @@ int qvk_prefill_layer_dests(qvk_stream_t s, const qvk_groups* g, const qvk_layer
     QVK_TRY(check_rho(p->rho));
     QVK_TRY(check_groups(g));
     if (!kc || !vc || n_dest < 1) QVK_INVALID("prune: no cache destinations");
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
     const int heads = p->per_head ? p->n_kv : 1;
     const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
     if (p->rho == 1.0 || (p->scorer != QVK_KEY_NORM_SMALL && p->scorer != QVK_VALUE_NORM) ||
@@ -478,6 +563,7 @@ int qvk_prefill_layer_dests(qvk_stream_t s, const qvk_groups* g, const qvk_layer
         return QVK_E_UNSUPPORTED;
     }
     QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
+    g_route = 0;
     return launch_prune_fused_dests(s, g, k, v, heads, width, p->scorer, nullptr, scores_ws, idx_ws, n_dest, kc, vc,
                                     origin, 1);
 }

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(256) tokenize_fast_kernel(const uint8_t* __res
         uint32_t acc[3] = {0u, 0u, 0u};
         if (pl < np) {
             const uint32_t p = p0 + pl, gr = p / grid_cols, gc = p % grid_cols;
-            const bool vec = (pw % 4 == 0) && (width % 4 == 0);
+            // 32-bit loads need every row start 4-byte aligned: pw, width and the frames pointer itself
+            const bool vec = (pw % 4 == 0) && (width % 4 == 0) && (reinterpret_cast<uintptr_t>(frames) & 3) == 0;
             for (uint32_t y = part; y < ph; y += 4) {
                 const size_t row = static_cast<size_t>(gr * ph + y) * width + gc * pw;
 #pragma unroll

@@ -18,7 +18,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
                                                      const uint32_t* __restrict__ idx, int64_t total_units,
                                                      int64_t keep_stride,
                                                      uint8_t* __restrict__ kc, uint8_t* __restrict__ vc,
-                                                     uint64_t* __restrict__ origin) {
+                                                     uint64_t* __restrict__ origin, uint32_t* __restrict__ idx_out) {
     const int vec_per_unit = row_bytes / static_cast<int>(sizeof(V));
     const int64_t total = total_units * vec_per_unit;
     for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < total;
@@ -38,14 +38,18 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         *reinterpret_cast<V*>(kc + dof) = a;
         *reinterpret_cast<V*>(vc + dof) = b;
         if (origin && part == 0) origin[cu] = __ldg(first_token + g) + static_cast<uint64_t>(src_tok);
+        if (idx_out && part == 0) idx_out[cu] = static_cast<uint32_t>(src_tok);  // identity path: r = 0..keep-1
     }
 }
 
 }  // namespace
 
 // keep_stride: cache rows of a full-size group when known (rho given), else 0 = derive / binary search.
+// idx_out (identity path only, idx == NULL): receives the retained local indices 0..keep-1 like every scored path.
 int launch_gather(cudaStream_t stream, const qvk_groups* g, const void* k, const void* v, int dtype, int heads,
-                  int width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin, int64_t keep_stride) {
+                  int width, const uint32_t* idx, void* kc, void* vc, uint64_t* origin, int64_t keep_stride,
+                  uint32_t* idx_out) {
+    if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
     if (keep_stride <= 0 && g->n_groups > 0 && g->total_rows % g->n_groups == 0)
         keep_stride = g->total_rows / g->n_groups;  // equal groups
     const int elem = dtype == QVK_F32 ? 4 : 2;
@@ -64,7 +68,7 @@ int launch_gather(cudaStream_t stream, const qvk_groups* g, const void* k, const
         kern<<<blocks, 256, 0, stream>>>(static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v), row_bytes,
                                          heads, g->n_groups, g->tok_off_d, g->row_off_d, g->first_token_d, idx,
                                          units, keep_stride, static_cast<uint8_t*>(kc), static_cast<uint8_t*>(vc),
-                                         origin);
+                                         origin, idx ? nullptr : idx_out);
     };
     if (vec == 16) args(gather_kernel<uint4>);
     else if (vec == 4) args(gather_kernel<uint32_t>);

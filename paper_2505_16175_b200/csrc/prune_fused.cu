@@ -545,6 +545,9 @@ int launch_prune_fused_dests(cudaStream_t stream, const qvk_groups* g, const voi
                              int overlap_prev) {
     if (static_cast<int64_t>(g->n_groups) * heads == 0 || g->max_tokens == 0) return QVK_OK;
     if (n_dest < 1 || n_dest > kMaxDests) QVK_INVALID("prune: 1..8 cache destinations");
+    if (origin && !g->first_token_d)
+        for (int i = 0; i < n_dest; ++i)
+            if (origin[i]) QVK_INVALID("gather: origin requested without first_token");
     Dests dst{};
     dst.n = n_dest;
     for (int i = 0; i < n_dest; ++i) {

@@ -348,6 +348,139 @@ __global__ void score_attention_smem_kernel(const T* __restrict__ k, int64_t tok
     out[i0 + threadIdx.x] = __ddiv_rn(sum, divisor);
 }
 
+// ---- GQA attention_score on a pre-summed text query (qvk_score_text, include/qvk.h) ------------------------------
+// qbar[h, j] = float(sum_t sum_{hq in group(h)} double(q[t, hq, j])), t outer, hq inner — one thread per (h, j).
+__global__ void text_query_sum_kernel(const float* __restrict__ q, int64_t text_count, int n_q, int n_kv, int d_h,
+                                      float* __restrict__ qbar) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n_kv * d_h) return;
+    const int h = o / d_h, j = o - h * d_h, gq = n_q / n_kv;
+    double acc = 0.0;
+    for (int64_t t = 0; t < text_count; ++t)
+        for (int x = 0; x < gq; ++x)
+            acc = __dadd_rn(acc, static_cast<double>(__ldg(q + (t * n_q + h * gq + x) * d_h + j)));
+    qbar[o] = static_cast<float>(acc);
+}
+
+// s = (sum_j double(k_j) * double(qbar_j)) / divisor over one (token, head) row, j sequential (prefill.cpp:220-226
+// with a single text row).  bf16 x fp32 products are exact in double, so fma(k, q, acc) rounds exactly like
+// acc + k*q: bit-identical to the reference's loop on the same row.  Generic widths: the row is read straight from
+// HBM (16-byte loads when aligned).
+__device__ __forceinline__ void store_unit(double* __restrict__ out, int64_t u, int heads, int n_groups,
+                                           const int64_t* __restrict__ tok_off, int64_t stride, double s) {
+    if (heads == 1) {
+        out[u] = s;
+        return;
+    }
+    const int64_t tok = u / heads;
+    const int hh = static_cast<int>(u - tok * heads);
+    const int g = find_group_fast(tok_off, n_groups, tok, stride);
+    const int64_t t0 = __ldg(tok_off + g);
+    const int64_t n = __ldg(tok_off + g + 1) - t0;
+    out[heads * t0 + hh * n + (tok - t0)] = s;
+}
+
+__global__ void __launch_bounds__(kSeqThreads) score_dot_seq_kernel(const __nv_bfloat16* __restrict__ k,
+                                                                    int64_t units, int width, int heads,
+                                                                    const float* __restrict__ qbar, double divisor,
+                                                                    const int64_t* __restrict__ tok_off, int n_groups,
+                                                                    int64_t max_tokens, double* __restrict__ out) {
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kSeqThreads + threadIdx.x;
+    if (u >= units) return;
+    const int h = static_cast<int>(u % heads);
+    const __nv_bfloat16* row = k + u * width;
+    const float* qb = qbar + static_cast<int64_t>(h) * width;
+    double acc = 0.0;
+    if ((width & 7) == 0 && (reinterpret_cast<uintptr_t>(k) & 15) == 0) {
+        for (int c = 0; c < width / 8; ++c) {
+            const uint4 p = __ldg(reinterpret_cast<const uint4*>(row) + c);
+            const uint32_t w[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const uint32_t bits = (e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16);
+                acc = __fma_rn(static_cast<double>(__uint_as_float(bits)),
+                               static_cast<double>(__ldg(qb + c * 8 + e)), acc);
+            }
+        }
+    } else {
+        for (int j = 0; j < width; ++j)
+            acc = __fma_rn(to_double(row[j]), static_cast<double>(__ldg(qb + j)), acc);
+    }
+    store_unit(out, u, heads, n_groups, tok_off, max_tokens, __ddiv_rn(acc, divisor));
+}
+
+// Per-head rows of 64 / 128 bf16 (every GQA shape): the norm kernel's TMA ring (128-row tiles, 128-byte swizzle,
+// one producer warp) with ONE consumer thread per row walking its row j = 0..W-1 (chunk c of row r sits at
+// r*128 + ((c ^ (r & 7)) * 16): conflict-free), qbar held as doubles in shared memory with a padded per-head stride
+// (the heads of one warp's rows read distinct banks).  HBM-bound: N*W*2 bytes read, N*8 written.
+constexpr int kDotConsumers = kTmaRows;
+
+template <int NB>
+__global__ void __launch_bounds__(kDotConsumers + 32) score_dot_tma_kernel(
+    const __grid_constant__ CUtensorMap tm, int64_t units, int heads, const float* __restrict__ qbar,
+    double divisor, const int64_t* __restrict__ tok_off, int n_groups, int64_t max_tokens, double* __restrict__ out) {
+    constexpr int W = 64 * NB;
+    constexpr int kQStride = W + 1;                  // doubles per head row of qbar in smem
+    constexpr uint32_t kBox = kTmaRows * 128;
+    constexpr uint32_t kTile = NB * kBox;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    ScoreTmaShared* sh = reinterpret_cast<ScoreTmaShared*>(smem + kTmaStages * kTile);
+    double* qs = reinterpret_cast<double*>(sh + 1);  // [heads][kQStride]
+    const int warp = threadIdx.x >> 5;
+    const int64_t tiles = (units + kTmaRows - 1) / kTmaRows;
+    for (int i = threadIdx.x; i < heads * W; i += blockDim.x)
+        qs[(i / W) * kQStride + (i % W)] = static_cast<double>(__ldg(qbar + i));
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < kTmaStages; ++st) {
+            ptx::mbar_init(&sh->full[st], 1);
+            ptx::mbar_init(&sh->empty[st], kDotConsumers);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == kDotConsumers / 32) {
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tm);
+            uint32_t k = 0;
+            for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
+                const uint32_t st = k % kTmaStages;
+                ptx::mbar_wait(&sh->empty[st], ((k / kTmaStages) & 1) ^ 1);
+                ptx::mbar_arrive_expect_tx(&sh->full[st], kTile);
+#pragma unroll
+                for (int b = 0; b < NB; ++b)
+                    ptx::tma_load_2d(smem + st * kTile + b * kBox, &tm, &sh->full[st], 64 * b,
+                                     static_cast<int>(t * kTmaRows));
+            }
+        }
+        return;
+    }
+    const int r = threadIdx.x;
+    uint32_t k = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
+        const uint32_t st = k % kTmaStages;
+        ptx::mbar_wait(&sh->full[st], (k / kTmaStages) & 1);
+        const int64_t u = t * kTmaRows + r;
+        const double* q = qs + static_cast<int>(u % heads) * kQStride;
+        const uint32_t row_s = ptx::smem_u32(smem + st * kTile + r * 128);
+        double acc = 0.0;
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t w[4];
+                ptx::lds128(w, row_s + b * kBox + ((c ^ (r & 7)) << 4));
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t bits = (e & 1) ? (w[e >> 1] & 0xffff0000u) : (w[e >> 1] << 16);
+                    acc = __fma_rn(static_cast<double>(__uint_as_float(bits)), q[b * 64 + c * 8 + e], acc);
+                }
+            }
+        ptx::mbar_arrive(&sh->empty[st]);
+        if (u < units) store_unit(out, u, heads, n_groups, tok_off, max_tokens, __ddiv_rn(acc, divisor));
+    }
+}
+
 }  // namespace
 
 int launch_score(cudaStream_t stream, const qvk_groups* g, int64_t total_tokens, const void* k, const void* v,
@@ -418,6 +551,44 @@ int launch_score(cudaStream_t stream, const qvk_groups* g, int64_t total_tokens,
         return QVK_OK;
     }
     QVK_INVALID("score: unknown scorer");
+}
+
+int launch_text_query_sum(cudaStream_t stream, const float* q, int64_t text_count, int n_q, int n_kv, int d_h,
+                          float* qbar) {
+    const int n = n_kv * d_h;
+    text_query_sum_kernel<<<(n + 127) / 128, 128, 0, stream>>>(q, text_count, n_q, n_kv, d_h, qbar);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
+// Scores of every (token, head) row of k (heads x width bf16) against qbar (heads x width fp32), divided by divisor.
+int launch_score_dot(cudaStream_t stream, const qvk_groups* g, const void* k, int heads, int width,
+                     const float* qbar, double divisor, double* scores) {
+    const int64_t units = g->total_tokens * heads;
+    if (units == 0) return QVK_OK;
+    CUtensorMap tm;
+    if ((width == 64 || width == 128) && heads <= 16 && (reinterpret_cast<uintptr_t>(k) & 15) == 0 &&
+        units < (int64_t(1) << 31) && score_map(&tm, k, units, width)) {
+        auto go = [&](auto kern, int nb) -> int {
+            const size_t smem = 1024 + kTmaStages * nb * kTmaRows * 128 + sizeof(ScoreTmaShared) +
+                                static_cast<size_t>(heads) * (64 * nb + 1) * sizeof(double);
+            QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+            const int64_t tiles = (units + kTmaRows - 1) / kTmaRows;
+            const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, 2 * static_cast<int64_t>(sm_count())));
+            kern<<<grid, kDotConsumers + 32, smem, stream>>>(tm, units, heads, qbar, divisor, g->tok_off_d,
+                                                            g->n_groups, g->max_tokens, scores);
+            QVK_LAUNCH_CHECK();
+            return QVK_OK;
+        };
+        return width == 64 ? go(score_dot_tma_kernel<1>, 1) : go(score_dot_tma_kernel<2>, 2);
+    }
+    const unsigned grid = static_cast<unsigned>((units + kSeqThreads - 1) / kSeqThreads);
+    score_dot_seq_kernel<<<grid, kSeqThreads, 0, stream>>>(static_cast<const __nv_bfloat16*>(k), units, width, heads,
+                                                           qbar, divisor, g->tok_off_d, g->n_groups, g->max_tokens,
+                                                           scores);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
 }
 
 }  // namespace qvk

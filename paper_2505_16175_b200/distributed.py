@@ -47,6 +47,45 @@ def allgather_cache(tensors: list[torch.Tensor], bounds: list[tuple[int, int]], 
     return []
 
 
+class NcclComm:
+    """The C ABI's NCCL communicator (qvk_comm_*, include/qvk.h) bootstrapped over torch.distributed: rank 0 creates
+    the ncclUniqueId, the process group ships it, every rank joins on its current device.  `allgather` replicates a
+    layer's pruned cache with ONE grouped NCCL call (qvk_allgather_layer: an in-place broadcast per source rank and
+    buffer inside one ncclGroupStart/End) on the given stream."""
+
+    def __init__(self, group=None):
+        import ctypes as C
+
+        from ._lib import check, lib
+
+        self._C, self._lib, self._check = C, lib, check
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            check(lib.qvk_comm_unique_id(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        self.comm = C.c_void_p(0)
+        check(lib.qvk_comm_init(C.byref(self.comm), self.world, self.rank, C.create_string_buffer(box[0], 128)))
+
+    def allgather(self, k_cache: torch.Tensor, v_cache: torch.Tensor, origin: torch.Tensor | None,
+                  bounds: list[tuple[int, int]], heads: int, width: int, stream=None) -> None:
+        C = self._C
+        rb = (C.c_int64 * (self.world + 1))(*([b for b, _ in bounds] + [bounds[-1][1]]))
+        s = (stream or torch.cuda.current_stream()).cuda_stream
+        self._check(self._lib.qvk_allgather_layer(s, self.comm, rb, heads, width, k_cache.data_ptr(),
+                                                  v_cache.data_ptr(), None if origin is None else origin.data_ptr()))
+
+    def check(self) -> None:
+        self._check(self._lib.qvk_comm_check(self.comm))
+
+    def close(self) -> None:
+        if self.comm:
+            self._check(self._lib.qvk_comm_destroy(self.comm))
+            self.comm = self._C.c_void_p(0)
+
+
 class PeerCache:
     """The cache all-gather fused into the compaction: every rank maps the other ranks' cache buffers into its address
     space (CUDA IPC over NVLink; qvk_ipc_*) and the fused prune kernel stores each retained row into ALL ranks' caches
@@ -90,13 +129,45 @@ class PeerCache:
                 row.append(base.value + off)
             self.ptrs.append(row)
         self.arrays = [(C.c_void_p * len(row))(*row) for row in self.ptrs]
+        # device-side barrier state: one 32-bit counter per rank (IPC-mapped by the others) and an error word
+        dev = tensors[0].device
+        self.flag = torch.zeros(64, dtype=torch.int32, device=dev)  # own 256-byte slot, counter at [0]
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        h = (C.c_char * 64)()
+        off = C.c_uint64(0)
+        torch.cuda.synchronize(dev)
+        check(lib.qvk_ipc_get_handle(self.flag.data_ptr(), h, C.byref(off)))
+        fl = [None] * self.world
+        dist.all_gather_object(fl, (bytes(h), off.value), group=group)
+        flags = []
+        for r in range(self.world):
+            if r == self.rank:
+                flags.append(self.flag.data_ptr())
+                continue
+            base = C.c_void_p(0)
+            check(lib.qvk_ipc_open(C.create_string_buffer(fl[r][0], 64), C.byref(base)))
+            self._bases.append(base.value)
+            flags.append(base.value + fl[r][1])
+        self._flags = (C.c_void_p * self.world)(*flags)
+        self.epoch = 0
+        dist.barrier(group=group)  # every rank mapped every counter before the first fence
 
-    def fence(self, device):
-        """Cross-rank barrier after this step's kernels: every peer's stores into our cache have completed."""
-        torch.cuda.current_stream(device).synchronize()
-        dist.barrier(group=self.group)
+    def fence(self, device=None):
+        """Cross-rank barrier after this step's kernels, ON THE DEVICE (qvk_peer_barrier): stream-ordered after the
+        prune, so later work on the stream sees every peer's stores into our cache; no host synchronisation."""
+        self.epoch += 1
+        s = torch.cuda.current_stream(device).cuda_stream
+        self._check(self._lib.qvk_peer_barrier(s, self.world, self._flags, self.rank, self.epoch,
+                                               self.err.data_ptr()))
+
+    def check(self) -> None:
+        """Raise if a device barrier timed out (a peer never arrived)."""
+        if int(self.err.item()):
+            raise RuntimeError("PeerCache: a peer did not reach the device barrier (timeout)")
 
     def close(self):
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # no peer still stores into our buffers when they are unmapped
         for b in self._bases:
             self._check(self._lib.qvk_ipc_close(b))
         self._bases = []

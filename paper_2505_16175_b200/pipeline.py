@@ -88,11 +88,14 @@ class _Pipeline:
             if out_k is not None:
                 self.d2h.wait_event(self._consumed[c])
                 a, b = self.row_base + r0, self.row_base + r1
+                L_ = self.k_cache.shape[0]
+                ok, ov, oo = out_k.view(L_, -1), out_v.view(L_, -1), out_o.view(L_, -1)
                 with torch.cuda.stream(self.d2h):
-                    out_k[a * unit:b * unit].copy_(self.k_cache[a * unit:b * unit], non_blocking=True)
-                    out_v[a * unit:b * unit].copy_(self.v_cache[a * unit:b * unit], non_blocking=True)
-                    out_o[a * self.n_kv:b * self.n_kv].copy_(self.origin[a * self.n_kv:b * self.n_kv],
-                                                             non_blocking=True)
+                    for l in range(L_):  # the chunk's rows of every layer's cache
+                        ok[l, a * unit:b * unit].copy_(self.k_cache[l, a * unit:b * unit], non_blocking=True)
+                        ov[l, a * unit:b * unit].copy_(self.v_cache[l, a * unit:b * unit], non_blocking=True)
+                        oo[l, a * self.n_kv:b * self.n_kv].copy_(self.origin[l, a * self.n_kv:b * self.n_kv],
+                                                                 non_blocking=True)
                     self._read[c] = torch.cuda.Event()
                     self._read[c].record(self.d2h)
         if after_compute is not None:
@@ -132,9 +135,9 @@ class HostPrefill(_Pipeline):
         self.scores = torch.empty(max(1, T * n_kv), dtype=torch.float64, device=self.dev)
         self.idx = torch.empty(max(1, R * n_kv), dtype=torch.int32, device=self.dev)
         rows = R if cache_rows is None else cache_rows
-        self.k_cache = torch.empty(rows * n_kv * d_h, dtype=bf, device=self.dev)
+        self.k_cache = torch.empty(1, rows * n_kv * d_h, dtype=bf, device=self.dev)  # (layers = 1, cache)
         self.v_cache = torch.empty_like(self.k_cache)
-        self.origin = torch.empty(rows * n_kv, dtype=torch.int64, device=self.dev)
+        self.origin = torch.empty(1, rows * n_kv, dtype=torch.int64, device=self.dev)
         self.row_base = row_base
         self.prm = L.QvkLayerParams(n_q, n_kv, d_h, int(scorer), 1, rho, 1.0 / math.sqrt(d_h), 32, 1)
         self._init_pipeline()
@@ -146,8 +149,8 @@ class HostPrefill(_Pipeline):
         check(lib.qvk_prefill_layer(stream.cuda_stream, g.ref, C.byref(self.prm), self.q[t0:t1].data_ptr(),
                                     self.k[t0:t1].data_ptr(), self.v[t0:t1].data_ptr(), self.o[t0:t1].data_ptr(),
                                     self.scores[t0 * self.n_kv:].data_ptr(), self.idx[r0 * self.n_kv:].data_ptr(),
-                                    self.k_cache[cr * unit:].data_ptr(), self.v_cache[cr * unit:].data_ptr(),
-                                    self.origin[cr * self.n_kv:].data_ptr()))
+                                    self.k_cache[0, cr * unit:].data_ptr(), self.v_cache[0, cr * unit:].data_ptr(),
+                                    self.origin[0, cr * self.n_kv:].data_ptr()))
 
     def run(self, hq, hk, hv, out_k=None, out_v=None, out_o=None, after_compute=None, join=True):
         """One pruned-prefill layer from host Q/K/V (pinned, (T, heads, d) bf16) into the device cache; optional
@@ -166,21 +169,26 @@ class HostPrefill(_Pipeline):
 
 
 class FramePrefill(_Pipeline):
-    """Video frames in host memory -> one layer's pruned KV cache: the end-to-end path of the reference's
+    """Video frames in host memory -> the pruned KV cache of every layer: the end-to-end path of the reference's
     `prefill(model, tokenize(frames), prune)` (prefill.hpp:86-87, 137-138; prefill.cpp:170-183, 293-323) on the GPU.
 
     Per chunk of groups (contiguous frames): pinned host frames -> HBM on a copy stream; GPU tokenizer (bf16 tokens,
-    qvk_tokenize_bf16); QKV projection with the key-norm fused (qvk_project_qkv); attention; fused select + gather
-    (qvk_prefill_layer_x); the chunk's pruned cache rows -> pinned host on a second copy stream.  Chunk c+1's frames
-    upload and chunk c-1's cache readback overlap chunk c's kernels.  Frames are (F, 3, H, W) uint8 (decode.hpp:27-55
-    FrameBuffer slots), H and W divisible by the patch grid of tokens_per_frame (prefill.cpp:116-121)."""
+    qvk_tokenize_bf16) ONCE; then for every layer l — the stand-in projects the same tokens in every layer
+    (prefill.cpp:188-189, 298-308) — QKV projection with W_l and the key-norm fused (qvk_project_qkv), attention,
+    fused select + gather into layer l's cache (qvk_prefill_layer_x); the chunk's pruned rows of every layer ->
+    pinned host on a second copy stream.  Chunk c+1's frames upload and chunk c-1's cache readback overlap chunk c's
+    kernels.  Frames are (F, 3, H, W) uint8 (decode.hpp:27-55 FrameBuffer slots), H and W divisible by the patch grid
+    of tokens_per_frame (prefill.cpp:116-121).  w_qkv: ((n_q + 2 n_kv) d_h, d_model) for one layer or
+    (layers, (n_q + 2 n_kv) d_h, d_model); caches are (layers, rows * n_kv * d_h)."""
 
     def __init__(self, plan: GroupPlan, tokens_per_frame: int, height: int, width: int, embed, w_qkv, n_q: int,
                  n_kv: int, d_h: int, rho: float, device, chunks: int = 4, cache_rows: int | None = None,
                  row_base: int = 0):
         self.plan, self.tpf, self.n_q, self.n_kv, self.d, self.rho = plan, tokens_per_frame, n_q, n_kv, d_h, rho
         self.dev = torch.device(device)
-        self.embed, self.w = embed, w_qkv
+        self.embed = embed
+        self.w = w_qkv if w_qkv.dim() == 3 else w_qkv.unsqueeze(0)
+        self.layers = int(self.w.shape[0])
         self.d_model = int(embed.shape[0])
         G = plan.n_groups
         bounds = chunk_bounds(G, chunks)
@@ -205,9 +213,9 @@ class FramePrefill(_Pipeline):
         self.scores = torch.empty(max(1, T * n_kv), dtype=torch.float64, device=self.dev)
         self.idx = torch.empty(max(1, R * n_kv), dtype=torch.int32, device=self.dev)
         rows = R if cache_rows is None else cache_rows
-        self.k_cache = torch.empty(rows * n_kv * d_h, dtype=bf, device=self.dev)
+        self.k_cache = torch.empty(self.layers, rows * n_kv * d_h, dtype=bf, device=self.dev)
         self.v_cache = torch.empty_like(self.k_cache)
-        self.origin = torch.empty(rows * n_kv, dtype=torch.int64, device=self.dev)
+        self.origin = torch.empty(self.layers, rows * n_kv, dtype=torch.int64, device=self.dev)
         self.row_base = row_base
         self.prm = L.QvkLayerParams(n_q, n_kv, d_h, int(Scorer.key_norm_small), 1, rho, 1.0 / math.sqrt(d_h), 32, 1)
         self._init_pipeline()
@@ -220,12 +228,14 @@ class FramePrefill(_Pipeline):
                                     self.embed.data_ptr(), self.d_model, self.x[t0:t1].data_ptr()))
         unit = self.n_kv * self.d
         cr = self.row_base + r0
-        check(lib.qvk_prefill_layer_x(stream.cuda_stream, g.ref, C.byref(self.prm), self.x[t0:t1].data_ptr(),
-                                      self.d_model, self.w.data_ptr(), self.q[t0:t1].data_ptr(),
-                                      self.k[t0:t1].data_ptr(), self.v[t0:t1].data_ptr(), self.o[t0:t1].data_ptr(),
-                                      self.scores[t0 * self.n_kv:].data_ptr(), self.idx[r0 * self.n_kv:].data_ptr(),
-                                      self.k_cache[cr * unit:].data_ptr(), self.v_cache[cr * unit:].data_ptr(),
-                                      self.origin[cr * self.n_kv:].data_ptr()))
+        for l in range(self.layers):
+            check(lib.qvk_prefill_layer_x(stream.cuda_stream, g.ref, C.byref(self.prm), self.x[t0:t1].data_ptr(),
+                                          self.d_model, self.w[l].data_ptr(), self.q[t0:t1].data_ptr(),
+                                          self.k[t0:t1].data_ptr(), self.v[t0:t1].data_ptr(),
+                                          self.o[t0:t1].data_ptr(), self.scores[t0 * self.n_kv:].data_ptr(),
+                                          self.idx[r0 * self.n_kv:].data_ptr(), self.k_cache[l, cr * unit:].data_ptr(),
+                                          self.v_cache[l, cr * unit:].data_ptr(),
+                                          self.origin[l, cr * self.n_kv:].data_ptr()))
 
     def run(self, hframes, out_k=None, out_v=None, out_o=None, after_compute=None, join=True):
         """One layer from pinned host frames (F, 3, H, W) uint8 into the device cache; optional pinned host outputs
@@ -284,8 +294,8 @@ class StreamingPrefill(FramePrefill):
         if len(self.submitted) != len(self.parts):
             raise ValueError("not every group was submitted")
         if out_k is not None:
-            out_k.copy_(self.k_cache, non_blocking=True)
-            out_v.copy_(self.v_cache, non_blocking=True)
-            out_o.copy_(self.origin, non_blocking=True)
+            out_k.view(-1).copy_(self.k_cache.view(-1), non_blocking=True)
+            out_v.view(-1).copy_(self.v_cache.view(-1), non_blocking=True)
+            out_o.view(-1).copy_(self.origin.view(-1), non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
         self.submitted = set()

@@ -243,6 +243,42 @@ def snapkv_scores(q, k, groups: DeviceGroups, n_q: int, n_kv: int, window: int =
     return out
 
 
+def text_query_sum(text_query, n_q: int, n_kv: int, out=None) -> torch.Tensor:
+    """qbar (n_kv, d_h) fp32: the text queries (T, n_q, d_h) pre-summed over text tokens and the query heads of each KV
+    head in double, rounded once (qvk_text_query_sum)."""
+    T, d = text_query.shape[0], text_query.shape[-1]
+    out = out if out is not None else torch.empty(n_kv, d, dtype=torch.float32, device=text_query.device)
+    check(lib.qvk_text_query_sum(_stream(), _ptr(text_query), T, n_q, n_kv, d, _ptr(out)))
+    return out
+
+
+def score_text(k, groups: DeviceGroups, text_query, n_q: int, n_kv: int, per_head: bool = True, qbar=None,
+               out=None) -> torch.Tensor:
+    """GQA attention_score (prefill.cpp:213-230 on the pre-summed text query, qvk_score_text): float64 scores in the
+    (group, head, token) layout; text_query (T, n_q, d_h) fp32 on the device (None -> the reference's error)."""
+    d = k.shape[-1]
+    heads = n_kv if per_head else 1
+    T = 0 if text_query is None else text_query.shape[0]
+    out = out if out is not None else torch.empty(max(1, groups.plan.total_tokens * heads), dtype=torch.float64,
+                                                  device=k.device)
+    check(lib.qvk_score_text(_stream(), groups.ref, _ptr(k), n_q, n_kv, d, int(per_head), _ptr(text_query), T,
+                             _ptr(qbar), _ptr(out)))
+    return out
+
+
+def last_prune_route() -> int:
+    """Route of this thread's last prune step: 0 fused, 1 separate kernels, 2 rho = 1 identity, 3 select + gather on
+    precomputed scores (qvk_last_prune_route)."""
+    return int(lib.qvk_last_prune_route())
+
+
+def _layer_params(n_q, n_kv, d, scorer, per_head, rho, scale, snap_window, snap_pool, text_query):
+    tq_count = 0 if text_query is None else int(text_query.shape[0])
+    return L.QvkLayerParams(n_q, n_kv, d, int(scorer), int(per_head), rho,
+                            1.0 / math.sqrt(d) if scale is None else scale, snap_window, snap_pool,
+                            _ptr(text_query), tq_count)
+
+
 @dataclass
 class LayerBuffers:
     """Preallocated outputs/workspace of prefill_layer (reused across steps; no allocation on the hot path)."""
@@ -271,14 +307,14 @@ class LayerBuffers:
 def prefill_layer(q, k, v, groups: DeviceGroups, n_q: int, n_kv: int, rho: float,
                   scorer: Scorer = Scorer.key_norm_small, per_head: bool = True, scale: float | None = None,
                   snap_window: int = 32, snap_pool: int = 1, buffers: LayerBuffers | None = None,
-                  cache_row_offset: int = 0) -> LayerBuffers:
-    """attention -> score -> select -> gather for one layer and every group of the plan (one qvk call)."""
+                  cache_row_offset: int = 0, text_query=None) -> LayerBuffers:
+    """attention -> score -> select -> gather for one layer and every group of the plan (one qvk call).
+    text_query: (T, n_q, d_h) fp32 on the device, for Scorer.attention_score."""
     d = q.shape[-1]
     buf = buffers or LayerBuffers.allocate(groups.plan, n_q, n_kv, d, per_head, q.device)
     heads = n_kv if per_head else 1
     width = d if per_head else n_kv * d
-    prm = L.QvkLayerParams(n_q, n_kv, d, int(scorer), int(per_head), rho,
-                           1.0 / math.sqrt(d) if scale is None else scale, snap_window, snap_pool)
+    prm = _layer_params(n_q, n_kv, d, scorer, per_head, rho, scale, snap_window, snap_pool, text_query)
     off = cache_row_offset * heads
     kc = buf.k_cache.data_ptr() + off * width * 2
     vc = buf.v_cache.data_ptr() + off * width * 2
@@ -307,7 +343,7 @@ def project_qkv(x, w, n_q: int, n_kv: int, d_h: int, groups: DeviceGroups | None
 def prefill_layer_x(x, w, groups: DeviceGroups, n_q: int, n_kv: int, d_h: int, rho: float,
                     scorer: Scorer = Scorer.key_norm_small, per_head: bool = True, scale: float | None = None,
                     snap_window: int = 32, snap_pool: int = 1, buffers: LayerBuffers | None = None,
-                    qkv=None, cache_row_offset: int = 0):
+                    qkv=None, cache_row_offset: int = 0, text_query=None):
     """Projection -> attention -> prune for one layer from hidden states X (qvk_prefill_layer_x)."""
     T, d_model = x.shape[0], x.shape[-1]
     dev = x.device
@@ -318,8 +354,7 @@ def prefill_layer_x(x, w, groups: DeviceGroups, n_q: int, n_kv: int, d_h: int, r
                torch.empty(T, n_kv, d_h, dtype=torch.bfloat16, device=dev))
     heads = n_kv if per_head else 1
     width = d_h if per_head else n_kv * d_h
-    prm = L.QvkLayerParams(n_q, n_kv, d_h, int(scorer), int(per_head), rho,
-                           1.0 / math.sqrt(d_h) if scale is None else scale, snap_window, snap_pool)
+    prm = _layer_params(n_q, n_kv, d_h, scorer, per_head, rho, scale, snap_window, snap_pool, text_query)
     off = cache_row_offset * heads
     kc = buf.k_cache.data_ptr() + off * width * 2
     vc = buf.v_cache.data_ptr() + off * width * 2
@@ -365,7 +400,7 @@ def prefill_layer_dests(q, k, v, groups: DeviceGroups, n_q: int, n_kv: int, rho:
     """prefill_layer whose compaction writes every retained row into this rank's cache AND every peer's
     (distributed.PeerCache over buffers.k_cache / v_cache / origin) — the all-gather fused into the kernel."""
     d = q.shape[-1]
-    prm = L.QvkLayerParams(n_q, n_kv, d, int(scorer), 1, rho, 1.0 / math.sqrt(d) if scale is None else scale, 32, 1)
+    prm = _layer_params(n_q, n_kv, d, scorer, True, rho, scale, 32, 1, None)
     off = cache_row_offset * n_kv
     n = len(peers.ptrs[0])
     kcs = (C.c_void_p * n)(*[p + off * d * 2 for p in peers.ptrs[0]])

@@ -237,9 +237,13 @@ def test_identity_rho_one(cuda):
     g = plan.to(cuda)
     k = synth_groups(sizes, 2, 64, 1, True, cuda)
     v = synth_groups(sizes, 2, 64, 2, False, cuda)
-    kc, vc, origin, _ = qp.prune(k, v, g, 2, 64, qp.Scorer.key_norm_small, 1.0)
+    kc, vc, origin, idx = qp.prune(k, v, g, 2, 64, qp.Scorer.key_norm_small, 1.0)
+    assert qp.last_prune_route() == 2
     assert torch.equal(kc.view_as(k), k) and torch.equal(vc.view_as(v), v)
     assert origin.view(-1, 2)[:, 0].tolist() == list(range(137))
+    # the identity path fills idx like every scored path: 0..keep-1 per group and head
+    want = torch.cat([torch.arange(n, device=cuda) for n in sizes]).view(-1, 1).expand(-1, 2)
+    assert torch.equal(idx.view(-1, 2).long(), want)
 
 
 # ------------------------------------------------------------------------------------------------ attention
@@ -446,33 +450,51 @@ def test_prune_fused_matches_separate_kernels(cuda, sizes, heads, width, rho, ki
         assert torch.equal(kc, kc2) and torch.equal(vc, vc2) and torch.equal(origin, origin2), scorer
 
 
-def test_small_per_token_batches_route_to_separate_kernels(cuda, tmp_path):
-    """With the default routing (QVK_PRUNE_FUSED_MIN_SEGS unset: small per-token batches take score + select +
-    gather) qvk_prune gives the same cache as the fused kernel this test process is pinned to."""
+@pytest.mark.parametrize("entry", ["prune", "prefill_layer"])
+@pytest.mark.parametrize("scorer", [qp.Scorer.key_norm_small, qp.Scorer.value_norm])
+def test_small_per_token_batches_route_to_separate_kernels(cuda, tmp_path, entry, scorer):
+    """Default routing (QVK_PRUNE_FUSED_MIN_SEGS unset): a small per-token batch takes score + select + gather
+    (qvk_last_prune_route() == 1) and yields the same cache as the fused kernel this test process is pinned to
+    (route 0) — for qvk_prune and qvk_prefill_layer (per_head = 0), both norm scorers."""
     import subprocess
     import sys
-    sizes, heads, width, rho = [300, 5, 1000], 1, 512, 0.5
-    plan = qp.GroupPlan.from_sizes(sizes, rho)
-    k = synth_groups(sizes, heads, width, 1, True, cuda)
-    v = synth_groups(sizes, heads, width, 2, False, cuda)
-    kc, vc, origin, idx = qp.prune(k, v, plan.to(cuda), heads, width, qp.Scorer.key_norm_small, rho)
-    np.save(tmp_path / "kc.npy", kc.view(torch.int16).cpu().numpy())
+    sizes, n_q, n_kv, d, rho = [300, 5, 1000], 8, 4, 128, 0.5
     code = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, %r); sys.path.insert(0, %r)
 import paper_2505_16175_b200 as qp
 from test_kernels_gpu import synth_groups
 dev = torch.device('cuda', 0)
-sizes = [300, 5, 1000]
-plan = qp.GroupPlan.from_sizes(sizes, 0.5)
-k = synth_groups(sizes, 1, 512, 1, True, dev); v = synth_groups(sizes, 1, 512, 2, False, dev)
-kc, vc, origin, idx = qp.prune(k, v, plan.to(dev), 1, 512, qp.Scorer.key_norm_small, 0.5)
-assert np.array_equal(kc.view(torch.int16).cpu().numpy(), np.load(%r))
-print("same")
-""" % (str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent), str(tmp_path / "kc.npy"))
-    env = {kk: vv for kk, vv in os.environ.items() if kk != "QVK_PRUNE_FUSED_MIN_SEGS"}
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
-    assert r.returncode == 0 and "same" in r.stdout, r.stderr[-2000:]
+sizes, n_q, n_kv, d, rho, entry, scorer = %r, %d, %d, %d, %r, %r, qp.Scorer(%d)
+plan = qp.GroupPlan.from_sizes(sizes, rho)
+g = plan.to(dev)
+k = synth_groups(sizes, n_kv, d, 1, True, dev); v = synth_groups(sizes, n_kv, d, 2, False, dev)
+if entry == "prune":
+    kc, vc, origin, idx = qp.prune(k.view(-1, 1, n_kv * d), v.view(-1, 1, n_kv * d), g, 1, n_kv * d, scorer, rho)
+else:
+    q = synth_groups(sizes, n_q, d, 3, False, dev)
+    buf = qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, scorer, False)
+    kc, vc, origin = buf.k_cache, buf.v_cache, buf.origin
+torch.cuda.synchronize()
+print("route", qp.last_prune_route())
+np.save(sys.argv[1], np.concatenate([kc.view(torch.int16).cpu().numpy().ravel().astype(np.int64),
+                                     vc.view(torch.int16).cpu().numpy().ravel().astype(np.int64),
+                                     origin.cpu().numpy().ravel()]))
+""" % (str(Path(__file__).resolve().parent.parent), str(Path(__file__).resolve().parent), sizes, n_q, n_kv, d, rho,
+       entry, int(scorer))
+    outs = {}
+    for mode, env_min in (("default", None), ("fused", "0")):
+        env = {kk: vv for kk, vv in os.environ.items() if kk != "QVK_PRUNE_FUSED_MIN_SEGS"}
+        if env_min is not None:
+            env["QVK_PRUNE_FUSED_MIN_SEGS"] = env_min
+        out = tmp_path / f"{mode}.npy"
+        r = subprocess.run([sys.executable, "-c", code, str(out)], capture_output=True, text=True, env=env,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        route = int(r.stdout.split("route")[1].split()[0])
+        assert route == (1 if mode == "default" else 0), (mode, route)
+        outs[mode] = np.load(out)
+    assert np.array_equal(outs["default"], outs["fused"])
 
 
 def test_prune_fused_extreme_values(cuda):
@@ -670,7 +692,7 @@ def test_frame_prefill_after_compute_hook(cuda):
     out_o = torch.empty(fp.origin.numel(), dtype=torch.int64).pin_memory()
     fp.run(fr.cpu().pin_memory(), out_k, out_v, out_o, after_compute=lambda: seen.copy_(fp.k_cache))
     torch.cuda.synchronize()
-    assert torch.equal(seen.cpu(), buf.k_cache.cpu())
+    assert torch.equal(seen.view(-1).cpu(), buf.k_cache.cpu())
     assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
     assert torch.equal(out_o, buf.origin.cpu())
 
