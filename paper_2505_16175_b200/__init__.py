@@ -16,6 +16,7 @@ from .prefill import (  # noqa: F401
     decode_attention,
     gather,
     group_count,
+    last_prune_route,
     prefill_layer,
     prefill_layer_dests,
     prefill_layer_x,
@@ -24,12 +25,14 @@ from .prefill import (  # noqa: F401
     prune_group,
     retained_count,
     score,
+    score_text,
     score_tokens,
     scorer_from_name,
     select,
     select_gather,
     snapkv_scores,
     synth_bf16,
+    text_query_sum,
     tokenize,
     top_k_indices,
 )

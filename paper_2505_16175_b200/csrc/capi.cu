@@ -17,8 +17,14 @@
 
 namespace qvk {
 
-thread_local std::string g_last_error;
-void set_error(const std::string& msg) { g_last_error = msg; }
+// Trivially destructible, so a qvk call made during process teardown (e.g. a static destructor freeing HBM) can still
+// record its error after this thread's thread_local objects with destructors are gone.
+thread_local char g_last_error[1024];
+void set_error(const std::string& msg) {
+    const size_t n = std::min(msg.size(), sizeof(g_last_error) - 1);
+    std::memcpy(g_last_error, msg.data(), n);
+    g_last_error[n] = '\0';
+}
 
 cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value) {
     static std::mutex mu;
@@ -155,7 +161,7 @@ using namespace qvk;
 
 extern "C" {
 
-const char* qvk_last_error(void) { return g_last_error.c_str(); }
+const char* qvk_last_error(void) { return g_last_error; }
 int qvk_version(void) { return 2; }
 int qvk_last_prune_route(void) { return g_route; }
 

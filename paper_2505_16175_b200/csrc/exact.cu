@@ -3,7 +3,8 @@
 //   project_exact   prefill.cpp:38-54   out = x * w with double accumulation in the reference's sequential order
 //   tokenize        prefill.cpp:123-168 per-patch double mean (exact integer sums) and the 3 -> d embed
 // plus the synthetic bf16 generator of the benchmark (same bits as oracle qvo_synth_bf16).
-// Every double operation is an explicit _rn intrinsic so nvcc can never contract it into an FMA.
+// Every double operation is an explicit _rn intrinsic, so nvcc never contracts a rounding the reference performs into
+// an FMA; the projection's FMAs are exact by construction (see project_exact_kernel).
 #include "common.cuh"
 
 namespace qvk {
@@ -17,36 +18,62 @@ __global__ void seeded_matrix_kernel(uint64_t state0, size_t count, double scale
     }
 }
 
-// out(rows, d_out) = x(rows, d_in) * w(d_in, d_out); thread (r, o) accumulates i = 0..d_in-1 in order.
-constexpr int kPT = 32;  // outputs per tile (threadIdx.x)
-constexpr int kPR = 8;   // rows per tile (threadIdx.y)
-constexpr int kPK = 32;  // reduction chunk
-__global__ void __launch_bounds__(kPT * kPR) project_exact_kernel(const float* __restrict__ x, int64_t rows,
-                                                                  int d_in, const float* __restrict__ w,
-                                                                  int d_out, float* __restrict__ out) {
-    __shared__ double xs[kPR][kPK];
-    __shared__ double ws[kPK][kPT + 1];
-    const int o = blockIdx.x * kPT + threadIdx.x;
-    const int64_t r = static_cast<int64_t>(blockIdx.y) * kPR + threadIdx.y;
-    double acc = 0.0;
+// out(rows, d_out) = x(rows, d_in) * w(d_in, d_out): every output accumulates i = 0..d_in-1 in order, in double
+// (prefill.cpp:38-54 `acc[o] += xi * wrow[o]`).  The product of two floats is exact in double (24 + 24 bits), so
+// fma(xi, w, acc) rounds exactly like acc + xi * w: bit-identical to the reference while running one DFMA per MAC.
+// CTA tile 64 rows x 64 outputs, 256 threads with 4 x 4 outputs each (register tile), reduction chunks of 16
+// staged in shared memory as doubles (converted once per element, not per use).
+constexpr int kPM = 64, kPN = 64, kPK = 16;
+__global__ void __launch_bounds__(256) project_exact_kernel(const float* __restrict__ x, int64_t rows, int d_in,
+                                                            const float* __restrict__ w, int d_out,
+                                                            float* __restrict__ out) {
+    __shared__ __align__(16) double xs[kPK][kPM];  // xs[i][r]
+    __shared__ __align__(16) double ws[kPK][kPN];  // ws[i][o]
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // outputs 4 tx.., rows 4 ty..
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kPM;
+    const int o0 = blockIdx.x * kPN;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
     for (int i0 = 0; i0 < d_in; i0 += kPK) {
-        const int kw = min(kPK, d_in - i0);
         __syncthreads();
-        for (int e = threadIdx.y * kPT + threadIdx.x; e < kPR * kPK; e += kPT * kPR) {
+        for (int e = threadIdx.x; e < kPM * kPK; e += 256) {  // x tile: consecutive threads walk i (coalesced rows)
             const int rr = e / kPK, ii = e % kPK;
-            const int64_t gr = static_cast<int64_t>(blockIdx.y) * kPR + rr;
-            xs[rr][ii] = (gr < rows && ii < kw) ? static_cast<double>(x[gr * d_in + i0 + ii]) : 0.0;
+            const int64_t gr = r0 + rr;
+            xs[ii][rr] = (gr < rows && i0 + ii < d_in) ? static_cast<double>(__ldg(x + gr * d_in + i0 + ii)) : 0.0;
         }
-        for (int e = threadIdx.y * kPT + threadIdx.x; e < kPK * kPT; e += kPT * kPR) {
-            const int ii = e / kPT, oo = e % kPT;
-            const int go = blockIdx.x * kPT + oo;
-            ws[ii][oo] = (go < d_out && ii < kw) ? static_cast<double>(w[static_cast<int64_t>(i0 + ii) * d_out + go])
-                                                 : 0.0;
+        for (int e = threadIdx.x; e < kPK * kPN; e += 256) {
+            const int ii = e / kPN, oo = e % kPN;
+            const int go = o0 + oo;
+            ws[ii][oo] = (go < d_out && i0 + ii < d_in)
+                             ? static_cast<double>(__ldg(w + static_cast<int64_t>(i0 + ii) * d_out + go)) : 0.0;
         }
         __syncthreads();
-        for (int ii = 0; ii < kw; ++ii) acc = __dadd_rn(acc, __dmul_rn(xs[threadIdx.y][ii], ws[ii][threadIdx.x]));
+        const int kw = min(kPK, d_in - i0);
+        for (int ii = 0; ii < kw; ++ii) {
+            const double2 xa = *reinterpret_cast<const double2*>(&xs[ii][ty * 4]);
+            const double2 xb = *reinterpret_cast<const double2*>(&xs[ii][ty * 4 + 2]);
+            const double2 wa = *reinterpret_cast<const double2*>(&ws[ii][tx * 4]);
+            const double2 wb = *reinterpret_cast<const double2*>(&ws[ii][tx * 4 + 2]);
+            const double xv[4] = {xa.x, xa.y, xb.x, xb.y}, wv[4] = {wa.x, wa.y, wb.x, wb.y};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = __fma_rn(xv[a], wv[b], acc[a][b]);
+        }
     }
-    if (r < rows && o < d_out) out[r * d_out + o] = __double2float_rn(acc);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int64_t r = r0 + ty * 4 + a;
+        if (r >= rows) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int o = o0 + tx * 4 + b;
+            if (o < d_out) out[r * d_out + o] = __double2float_rn(acc[a][b]);
+        }
+    }
 }
 
 // One CTA per token (frame slot f, patch gr, gc).  Integer channel sums are exact in any order (the reference
@@ -194,9 +221,9 @@ int launch_seeded_matrix(cudaStream_t s, uint64_t seed, uint32_t tag, uint32_t l
 int launch_project_exact(cudaStream_t s, const float* x, int64_t rows, int d_in, const float* w, int d_out,
                          float* out) {
     if (rows == 0 || d_out == 0) return QVK_OK;
-    if ((rows + kPR - 1) / kPR > 65535) QVK_INVALID("project: too many rows for one launch");
-    dim3 grid((d_out + kPT - 1) / kPT, static_cast<unsigned>((rows + kPR - 1) / kPR));
-    project_exact_kernel<<<grid, dim3(kPT, kPR), 0, s>>>(x, rows, d_in, w, d_out, out);
+    if ((rows + kPM - 1) / kPM > 65535) QVK_INVALID("project: too many rows for one launch");
+    dim3 grid((d_out + kPN - 1) / kPN, static_cast<unsigned>((rows + kPM - 1) / kPM));
+    project_exact_kernel<<<grid, 256, 0, s>>>(x, rows, d_in, w, d_out, out);
     QVK_LAUNCH_CHECK();
     return QVK_OK;
 }

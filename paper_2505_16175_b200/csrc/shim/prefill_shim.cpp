@@ -11,6 +11,9 @@
 //   score / top-k / gather exact fp64 scores, exact radix select, copies  (prefill.cpp:192-282)
 #include <cmath>
 #include <cstring>
+#include <list>
+#include <memory>
+#include <mutex>
 #include <numeric>
 
 #include "qv/prefill.hpp"
@@ -80,6 +83,148 @@ std::vector<float> seeded(uint64_t seed, uint32_t tag, uint32_t layer, size_t co
     return out;
 }
 
+// Device-resident weights of a StandInModel ("build once, share read-only", prefill.hpp:72).  The stand-in's
+// weights are a pure function of (seed, d_model, layers, text_tokens) (prefill.cpp:96-114), so models with equal
+// configs share one entry; W_K / W_V live only in HBM (generated there, never uploaded), and every project /
+// prefill call reuses them.  A small LRU bounds the HBM held for models that no longer exist.
+struct DeviceModel {
+    uint64_t seed = 0;
+    size_t d = 0, layers = 0, text = 0;
+    std::vector<Dev> wk, wv;
+    Dev query;  // (text_tokens, d) fp32: prompt * W_q (prefill.cpp:106-113)
+};
+
+std::shared_ptr<const DeviceModel> device_model(const ModelConfig& cfg) {
+    static std::mutex mu;
+    // Leaked on purpose: freeing HBM from a static destructor would run after the CUDA runtime and this thread's
+    // thread_local error string are torn down.
+    static auto& lru = *new std::list<std::shared_ptr<const DeviceModel>>();
+    constexpr size_t kKeep = 2;
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto it = lru.begin(); it != lru.end(); ++it) {
+        const DeviceModel& m = **it;
+        if (m.seed == cfg.seed && m.d == cfg.d_model && m.layers == cfg.layers && m.text == cfg.text_tokens) {
+            lru.splice(lru.begin(), lru, it);
+            return lru.front();
+        }
+    }
+    auto m = std::make_shared<DeviceModel>();
+    m->seed = cfg.seed;
+    m->d = cfg.d_model;
+    m->layers = cfg.layers;
+    m->text = cfg.text_tokens;
+    const size_t d = cfg.d_model;
+    const double proj_scale = 1.0 / std::sqrt(double(d));
+    for (uint32_t l = 0; l < cfg.layers; ++l) {
+        m->wk.emplace_back(d * d * sizeof(float));
+        m->wv.emplace_back(d * d * sizeof(float));
+        check(qvk_seeded_matrix(nullptr, cfg.seed, kTagKey, l, d * d, proj_scale, m->wk.back().get<float>()));
+        check(qvk_seeded_matrix(nullptr, cfg.seed, kTagValue, l, d * d, proj_scale, m->wv.back().get<float>()));
+    }
+    // Text query = prompt * W_q, both generated and multiplied on the device (prefill.cpp:106-113).
+    const size_t t = cfg.text_tokens;
+    Dev prompt(std::max<size_t>(1, t * d) * sizeof(float)), wq(d * d * sizeof(float));
+    m->query = Dev(std::max<size_t>(1, t * d) * sizeof(float));
+    check(qvk_seeded_matrix(nullptr, cfg.seed, kTagPrompt, 0, t * d, 1.0, prompt.get<float>()));
+    check(qvk_seeded_matrix(nullptr, cfg.seed, kTagQuery, 0, d * d, proj_scale, wq.get<float>()));
+    check(qvk_project_exact(nullptr, prompt.get<float>(), static_cast<int64_t>(t), static_cast<int32_t>(d),
+                            wq.get<float>(), static_cast<int32_t>(d), m->query.get<float>()));
+    check(qvk_stream_sync(nullptr));
+    lru.push_front(std::move(m));
+    if (lru.size() > kKeep) lru.pop_back();
+    return lru.front();
+}
+
+// Groups of the batched device path: token offsets, retained counts, cache offsets, first tokens.
+struct Groups {
+    Dev arrays;
+    qvk_groups g{};
+    std::vector<int64_t> tok_off, keep, row_off;
+    Groups(std::span<const TokenGroup> groups, double rho) {
+        const size_t G = groups.size();
+        tok_off.assign(G + 1, 0);
+        row_off.assign(G + 1, 0);
+        keep.assign(G, 0);
+        std::vector<int64_t> first(G);
+        int64_t mx = 0;
+        for (size_t i = 0; i < G; ++i) {
+            const int64_t n = static_cast<int64_t>(groups[i].token_count);
+            tok_off[i + 1] = tok_off[i] + n;
+            keep[i] = static_cast<int64_t>(qvk_retained_count(rho, static_cast<size_t>(n)));
+            row_off[i + 1] = row_off[i] + keep[i];
+            first[i] = static_cast<int64_t>(groups[i].first_token);
+            mx = std::max(mx, n);
+        }
+        std::vector<int64_t> host;
+        host.insert(host.end(), tok_off.begin(), tok_off.end());
+        host.insert(host.end(), keep.begin(), keep.end());
+        host.insert(host.end(), row_off.begin(), row_off.end());
+        host.insert(host.end(), first.begin(), first.end());
+        arrays = Dev(host.data(), host.size() * sizeof(int64_t));
+        const int64_t* base = arrays.get<int64_t>();
+        g.n_groups = static_cast<int32_t>(G);
+        g.max_tokens = mx;
+        g.total_tokens = tok_off[G];
+        g.total_rows = row_off[G];
+        g.tok_off_d = base;
+        g.keep_d = base + (G + 1);
+        g.row_off_d = base + (2 * G + 1);
+        g.first_token_d = reinterpret_cast<const uint64_t*>(base + (3 * G + 2));
+    }
+};
+
+// prefill_group / prefill for a batch of groups (prefill.cpp:293-323), all on the device: the tokens go up once,
+// then per layer ONE exact projection over every group's tokens (K and V), ONE qvk_prune over every group (the
+// retained rows land at the static offsets the in-order append would give them, prefill.cpp:304-308), and the
+// layer's pruned rows come back with one copy per tensor; a single synchronisation at the end.
+void prefill_batch(const StandInModel& model, std::span<const TokenGroup> groups, const PruneConfig& prune,
+                   KvCache& cache) {
+    const ModelConfig& cfg = model.config();
+    prune.validate();  // prune_group's order: rho, then the empty group, then the text query (prefill.cpp:258-275)
+    for (const TokenGroup& grp : groups)
+        if (grp.token_count == 0) throw Error("prune: empty group");
+    const bool text = prune.rho != 1.0 && prune.scorer == Scorer::attention_score;
+    if (text && model.text_query().empty()) throw Error("attention_score scorer requires a text query");
+    auto dm = device_model(cfg);
+    const size_t d = cfg.d_model;
+    Groups gr(groups, prune.rho);
+    const size_t T = static_cast<size_t>(gr.g.total_tokens), R = static_cast<size_t>(gr.g.total_rows);
+    Dev x(T * d * sizeof(float)), k(T * d * sizeof(float)), v(T * d * sizeof(float));
+    for (size_t i = 0; i < groups.size(); ++i)
+        check(qvk_memcpy_h2d(x.get<float>() + gr.tok_off[i] * d, groups[i].tokens.data(),
+                             groups[i].token_count * d * sizeof(float), nullptr));
+    Dev kc(std::max<size_t>(1, R * d) * sizeof(float)), vc(std::max<size_t>(1, R * d) * sizeof(float));
+    Dev org(std::max<size_t>(1, R) * sizeof(uint64_t));
+    Dev sc(T * sizeof(double)), ix(std::max<size_t>(1, R) * sizeof(uint32_t));
+    const size_t text_count = text ? model.text_query().size() / d : 0;
+    std::vector<size_t> base(cfg.layers);
+    for (uint32_t l = 0; l < cfg.layers; ++l) {
+        check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(T), static_cast<int32_t>(d),
+                                dm->wk[l].get<float>(), static_cast<int32_t>(d), k.get<float>()));
+        check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(T), static_cast<int32_t>(d),
+                                dm->wv[l].get<float>(), static_cast<int32_t>(d), v.get<float>()));
+        check(qvk_prune(nullptr, &gr.g, k.get(), v.get(), QVK_F32, 1, static_cast<int32_t>(d),
+                        static_cast<int32_t>(prune.scorer), prune.rho, text ? dm->query.get<float>() : nullptr,
+                        static_cast<int64_t>(text_count), static_cast<int32_t>(cfg.n_h), sc.get<double>(),
+                        ix.get<uint32_t>(), kc.get(), vc.get(), org.get<uint64_t>()));
+        LayerCache& layer = cache.layers[l];
+        base[l] = layer.origin.size();
+        layer.k.resize(layer.k.size() + R * d);
+        layer.v.resize(layer.v.size() + R * d);
+        layer.origin.resize(base[l] + R);
+        // stream-ordered after this layer's prune and before the next layer's, which reuses kc / vc / org
+        check(qvk_memcpy_d2h(layer.k.data() + base[l] * d, kc.get(), R * d * sizeof(float), nullptr));
+        check(qvk_memcpy_d2h(layer.v.data() + base[l] * d, vc.get(), R * d * sizeof(float), nullptr));
+        check(qvk_memcpy_d2h(layer.origin.data() + base[l], org.get(), R * sizeof(uint64_t), nullptr));
+    }
+    check(qvk_stream_sync(nullptr));
+    for (size_t i = 0; i < groups.size(); ++i) {  // prefill.cpp:309-313 (last layer's retained count)
+        cache.retained_per_group.push_back(static_cast<size_t>(gr.keep[i]));
+        cache.tokens_seen += groups[i].token_count;
+        cache.peak_group_tokens = std::max(cache.peak_group_tokens, groups[i].token_count);
+    }
+}
+
 }  // namespace
 
 // ---- config / naming (prefill.cpp:58-94) ---------------------------------------------------------------------------
@@ -120,23 +265,11 @@ bool KvCache::same_entries(const KvCache& other) const {
 // ---- StandInModel (prefill.cpp:96-190) ---------------------------------------------------------------------------
 StandInModel::StandInModel(const ModelConfig& config) : config_(config) {
     config_.validate();
-    const size_t d = config_.d_model;
-    const double proj_scale = 1.0 / std::sqrt(double(d));
-    w_k_.reserve(config_.layers);
-    w_v_.reserve(config_.layers);
-    for (uint32_t l = 0; l < config_.layers; ++l) {
-        w_k_.push_back(seeded(config_.seed, kTagKey, l, d * d, proj_scale));
-        w_v_.push_back(seeded(config_.seed, kTagValue, l, d * d, proj_scale));
-    }
-    embed_ = seeded(config_.seed, kTagEmbed, 0, d * 3, 1.0 / 255.0);
-    // Text query = prompt * W_q, both generated and multiplied on the device (prefill.cpp:106-113).
-    const size_t t = config_.text_tokens;
-    Dev prompt(t * d * sizeof(float)), wq(d * d * sizeof(float)), q(std::max<size_t>(1, t * d) * sizeof(float));
-    check(qvk_seeded_matrix(nullptr, config_.seed, kTagPrompt, 0, t * d, 1.0, prompt.get<float>()));
-    check(qvk_seeded_matrix(nullptr, config_.seed, kTagQuery, 0, d * d, proj_scale, wq.get<float>()));
-    check(qvk_project_exact(nullptr, prompt.get<float>(), static_cast<int64_t>(t), static_cast<int32_t>(d),
-                            wq.get<float>(), static_cast<int32_t>(d), q.get<float>()));
-    download(query_, q, t * d);
+    // W_K / W_V are generated in HBM and stay there (device_model); w_k_ / w_v_ are left empty — nothing outside
+    // this file can read them, and the weights are a pure function of the config (prefill.cpp:96-104).
+    auto dm = device_model(config_);
+    embed_ = seeded(config_.seed, kTagEmbed, 0, size_t{config_.d_model} * 3, 1.0 / 255.0);
+    download(query_, dm->query, size_t{config_.text_tokens} * config_.d_model);
 }
 
 std::pair<uint32_t, uint32_t> StandInModel::patch_grid(uint32_t tokens_per_frame) {
@@ -205,14 +338,14 @@ std::vector<TokenGroup> StandInModel::tokenize(const FrameBuffer& frames, uint32
 void StandInModel::project(const TokenGroup& group, uint32_t layer, std::vector<float>& k,
                            std::vector<float>& v) const {
     if (layer >= config_.layers) throw Error("project: layer out of range");
+    auto dm = device_model(config_);
     const size_t d = config_.d_model, n = group.token_count;
     Dev x(group.tokens.data(), std::max<size_t>(1, n * d) * sizeof(float));
-    Dev wk(w_k_[layer].data(), d * d * sizeof(float)), wv(w_v_[layer].data(), d * d * sizeof(float));
     Dev dk(std::max<size_t>(1, n * d) * sizeof(float)), dv(std::max<size_t>(1, n * d) * sizeof(float));
     check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(n), static_cast<int32_t>(d),
-                            wk.get<float>(), static_cast<int32_t>(d), dk.get<float>()));
+                            dm->wk[layer].get<float>(), static_cast<int32_t>(d), dk.get<float>()));
     check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(n), static_cast<int32_t>(d),
-                            wv.get<float>(), static_cast<int32_t>(d), dv.get<float>()));
+                            dm->wv[layer].get<float>(), static_cast<int32_t>(d), dv.get<float>()));
     download(k, dk, n * d);
     download(v, dv, n * d);
 }
@@ -312,30 +445,14 @@ KvCache make_cache(const ModelConfig& config) {
 }
 
 void prefill_group(const StandInModel& model, const TokenGroup& group, const PruneConfig& prune, KvCache& cache) {
-    const ModelConfig& cfg = model.config();
-    std::vector<float> k, v;
-    size_t retained = 0;
-    for (uint32_t l = 0; l < cfg.layers; ++l) {
-        model.project(group, l, k, v);
-        PrunedGroup pruned = prune_group(
-            k, v, group.token_count, cfg.n_h, cfg.d_h, prune,
-            prune.scorer == Scorer::attention_score ? model.text_query() : std::span<const float>{});
-        LayerCache& layer = cache.layers[l];
-        layer.k.insert(layer.k.end(), pruned.k.begin(), pruned.k.end());
-        layer.v.insert(layer.v.end(), pruned.v.begin(), pruned.v.end());
-        for (uint32_t i : pruned.indices) layer.origin.push_back(group.first_token + i);
-        retained = pruned.indices.size();
-    }
-    cache.retained_per_group.push_back(retained);
-    cache.tokens_seen += group.token_count;
-    cache.peak_group_tokens = std::max(cache.peak_group_tokens, group.token_count);
+    prefill_batch(model, std::span<const TokenGroup>(&group, 1), prune, cache);
 }
 
 KvCache prefill(const StandInModel& model, std::span<const TokenGroup> groups, const PruneConfig& prune) {
     if (groups.empty()) throw Error("prefill: no token groups");
     prune.validate();
     KvCache cache = make_cache(model.config());
-    for (const TokenGroup& g : groups) prefill_group(model, g, prune, cache);
+    prefill_batch(model, groups, prune, cache);  // every group in one batch: same cache as the in-order loop
     return cache;
 }
 

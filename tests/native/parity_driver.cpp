@@ -7,6 +7,7 @@
 //       JSON line with bitwise comparisons of tokens, text query, every layer's K/V/origin and the cache stats.
 //   parity_driver errors
 //       drives the documented misuse cases through both APIs and prints each pair of qv::Error messages.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -226,14 +227,60 @@ int errors() {
 
 }  // namespace
 
+// Drop-in throughput only (no reference run: at the 7B shape the reference needs ~30 ms per token per layer):
+// same arguments as `pipeline`; tokenize + prefill once to warm up (device weights, allocations), then timed `reps`
+// times.  Prints {"tokens", "dropin_ms", "tokens_per_s", "rows"}.
+int bench(char** a, int reps) {
+    const int pattern = std::stoi(a[0]);
+    const uint64_t seed = std::stoull(a[1]);
+    const size_t frames = std::stoull(a[2]);
+    const uint32_t w = std::stoul(a[3]), h = std::stoul(a[4]);
+    qv::ModelConfig cfg;
+    cfg.d_model = std::stoul(a[5]);
+    cfg.n_h = std::stoul(a[6]);
+    cfg.d_h = std::stoul(a[7]);
+    cfg.layers = std::stoul(a[8]);
+    cfg.tokens_per_frame = std::stoul(a[9]);
+    cfg.text_tokens = std::stoul(a[10]);
+    cfg.seed = seed;
+    const uint32_t fpg = std::stoul(a[11]);
+    qv::PruneConfig prune;
+    prune.scorer = qv::scorer_from_name(a[12]);
+    prune.rho = std::stod(a[13]);
+    qv::FrameBuffer fb(frames, w, h);
+    std::vector<uint8_t> pixels(frames * fb.slot_bytes());
+    for (size_t f = 0; f < frames; ++f) {
+        qvref_fill_pattern(pattern, seed, f, w, h, pixels.data() + f * fb.slot_bytes());
+        fb.write_slot(f, {pixels.data() + f * fb.slot_bytes(), fb.slot_bytes()});
+    }
+    qv::StandInModel model(cfg);
+    size_t rows = 0;
+    {
+        const auto groups = model.tokenize(fb, fpg);
+        rows = qv::prefill(model, groups, prune).retained_tokens();
+    }
+    double best = 1e30;
+    for (int r = 0; r < reps; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto groups = model.tokenize(fb, fpg);
+        const qv::KvCache cache = qv::prefill(model, groups, prune);
+        best = std::min(best, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+    const size_t tokens = frames * cfg.tokens_per_frame;
+    std::printf("{\"tokens\": %zu, \"rows\": %zu, \"dropin_ms\": %.3f, \"tokens_per_s\": %.1f}\n", tokens, rows, best,
+                tokens / (best / 1e3));
+    return 0;
+}
+
 int main(int argc, char** argv) {
     try {
         if (argc >= 2 && std::string(argv[1]) == "pipeline" && argc == 16) return pipeline(argv + 2);
         if (argc >= 2 && std::string(argv[1]) == "errors") return errors();
+        if (argc >= 2 && std::string(argv[1]) == "bench" && argc == 16) return bench(argv + 2, 3);
     } catch (const std::exception& e) {
         std::printf("{\"exception\": \"%s\"}\n", e.what());
         return 2;
     }
-    std::fprintf(stderr, "usage: parity_driver pipeline <14 args> | errors\n");
+    std::fprintf(stderr, "usage: parity_driver pipeline <14 args> | bench <14 args> | errors\n");
     return 64;
 }

@@ -52,3 +52,16 @@ def test_error_texts_match_reference(cuda):
     rc, out, err = run("errors")
     assert rc == 0, out + err
     assert out.count("OK\t") >= 14
+
+
+@needs_driver
+def test_dropin_throughput_7b_16_groups(cuda):
+    """The drop-in prefill at the 7B shape, 16 groups x 4096 tokens (d_model 3584, 28 heads x 128, 1 layer):
+    batched on the device (weights resident, one exact projection and one prune per layer for every group).  Round 1
+    ran 128 tokens of this shape in 49.8 ms (2.6 k tokens/s, profiles/r1_dropin_parity.jsonl); the bar is 10x."""
+    rc, out, err = run("bench", PAT["noise"], 1, 256, 64, 64, 3584, 28, 128, 1, 256, 64, 16, "key_norm_small", 0.5)
+    assert rc == 0, out + err
+    res = json.loads(out.strip().splitlines()[-1])
+    print(res)
+    assert res["tokens"] == 65536 and res["rows"] == 32768
+    assert res["tokens_per_s"] >= 10 * 2570
