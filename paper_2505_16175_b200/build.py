@@ -89,6 +89,19 @@ def build_shim(force: bool = False) -> Path | None:
     return out
 
 
+def build_pipeline(force: bool = False) -> Path | None:
+    """The overlap pipeline (include/qv_pipeline.hpp) over the drop-in; its producer is the reference's unchanged
+    video side, resolved at link time of the application (as qv::decode_intervals would be)."""
+    out = LIB / "libqv_pipeline.so"
+    if not (REF_INCLUDE / "qv" / "decode.hpp").exists():
+        return out if out.exists() else None
+    src = CSRC / "shim" / "pipeline.cpp"
+    if force or _stale(out, [src, INCLUDE / "qv_pipeline.hpp", LIB / "libqv_prefill.so"]):
+        _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-pthread", "-Wall", "-Wextra", f"-I{REF_INCLUDE}",
+              f"-I{INCLUDE}", str(src), "-o", str(out), f"-L{LIB}", "-lqv_prefill", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_oracle() -> None:
     """Test infrastructure: the reference (when /root/reference is present) and the C restatement."""
     _run(["make", "-s", "-C", str(ROOT / "oracle")])
@@ -103,9 +116,9 @@ def build_native_tests(force: bool = False) -> Path | None:
     if not (REF_INCLUDE / "qv" / "prefill.hpp").exists() or not shim.exists():
         return out if out.exists() else None
     out.parent.mkdir(parents=True, exist_ok=True)
-    if force or _stale(out, [src, shim]):
-        _run([CXX, "-std=c++20", "-O2", "-Wall", f"-I{REF_INCLUDE}", str(src), "-o", str(out),
-              f"-L{LIB}", "-lqv_prefill", "-lqvk", f"-L{ref_lib}", "-lqv_video", "-lqvref_capi", "-lqvref",
+    if force or _stale(out, [src, shim, LIB / "libqv_pipeline.so"]):
+        _run([CXX, "-std=c++20", "-O2", "-Wall", "-pthread", f"-I{REF_INCLUDE}", f"-I{INCLUDE}", str(src), "-o",
+              str(out), f"-L{LIB}", "-lqv_pipeline", "-lqv_prefill", "-lqvk", f"-L{ref_lib}", "-lqv_video", "-lqvref_capi", "-lqvref",
               "-Wl,-rpath,$ORIGIN/../../../paper_2505_16175_b200/lib:$ORIGIN/../../../oracle/_ref", "-fopenmp"])
     return out
 
@@ -113,6 +126,7 @@ def build_native_tests(force: bool = False) -> Path | None:
 def build_all(force: bool = False) -> None:
     build_qvk(force)
     build_shim(force)
+    build_pipeline(force)
     build_oracle()
     build_native_tests(force)
 

@@ -16,6 +16,8 @@
 #include <vector>
 
 #include "qv/prefill.hpp"
+#include "qv/synthetic.hpp"
+#include "qv_pipeline.hpp"
 
 extern "C" {
 const char* qvref_last_error(void);
@@ -272,15 +274,100 @@ int bench(char** a, int reps) {
     return 0;
 }
 
+// The overlap pipeline (qvx::run_pipeline, include/qv_pipeline.hpp) on a synthetic QVS video encoded by the
+// reference: its frame buffer must equal the reference decoder's, its cache the UNMODIFIED reference's prefill of
+// those frames (bit for bit); prints the PipelineReport (predicted vs measured t_total) and the sequential
+// decode-then-prefill time of the same drop-in calls.
+// args: pattern seed frames w h d_model n_h d_h layers tpf text fpg scorer rho cores intervals keyframe_period gap
+//       check (0: skip the reference prefill — minutes per 1k tokens at the 7B shape)
+int overlap(char** a) {
+    const int pattern = std::stoi(a[0]);
+    const uint64_t seed = std::stoull(a[1]);
+    const size_t frames = std::stoull(a[2]);
+    const uint32_t w = std::stoul(a[3]), h = std::stoul(a[4]);
+    qv::ModelConfig cfg;
+    cfg.d_model = std::stoul(a[5]);
+    cfg.n_h = std::stoul(a[6]);
+    cfg.d_h = std::stoul(a[7]);
+    cfg.layers = std::stoul(a[8]);
+    cfg.tokens_per_frame = std::stoul(a[9]);
+    cfg.text_tokens = std::stoul(a[10]);
+    cfg.seed = seed;
+    qvx::PipelineConfig pc;
+    pc.frames_per_group = std::stoul(a[11]);
+    pc.prune.scorer = qv::scorer_from_name(a[12]);
+    pc.prune.rho = std::stod(a[13]);
+    pc.cores = std::stoul(a[14]);
+    pc.intervals = std::stoul(a[15]);
+    qv::EncodeConfig ec;
+    ec.keyframe_period = std::stoul(a[16]);
+    const uint64_t gap = std::stoull(a[17]);
+    const bool check = std::stoi(a[18]) != 0;
+    const qv::VideoFile file = qv::synth_video(static_cast<qv::Pattern>(pattern), seed, frames, w, h, ec);
+    qv::SampleSpec spec;
+    spec.indices = qv::sample_indices_gap(frames, gap);
+    qv::StandInModel model(cfg);
+    {  // warm-up: device weights, allocations, kernels loaded
+        qv::FrameBuffer warm(std::min<size_t>(spec.indices.size(), pc.frames_per_group), w, h);
+        qv::prefill(model, model.tokenize(warm, pc.frames_per_group), pc.prune);
+    }
+    qvx::PipelineReport rep;
+    qv::FrameBuffer fb;
+    const qv::KvCache cache = qvx::run_pipeline(file, spec, model, pc, &rep, &fb);
+
+    // the sequential composition with the same calls: decode everything, then tokenize + prefill
+    const auto s0 = std::chrono::steady_clock::now();
+    qv::IntervalSet plan = qv::keyframe_intervals(file, pc.intervals ? pc.intervals : 4 * pc.cores);
+    qv::DecodeResult dec = qv::decode_intervals(file, spec, plan, pc.cores);
+    const auto s1 = std::chrono::steady_clock::now();
+    const qv::KvCache seq = qv::prefill(model, model.tokenize(dec.buffer, pc.frames_per_group), pc.prune);
+    const auto s2 = std::chrono::steady_clock::now();
+    const bool frames_equal = fb.same_pixels(dec.buffer);
+
+    void* ref = check ? qvref_model_create(cfg.d_model, cfg.n_h, cfg.d_h, cfg.layers, cfg.tokens_per_frame,
+                                           cfg.text_tokens, seed)
+                      : nullptr;
+    void* rc = check ? qvref_prefill_frames(ref, dec.buffer.bytes().data(), dec.buffer.slots(), w, h,
+                                            pc.frames_per_group, static_cast<int>(pc.prune.scorer), pc.prune.rho)
+                     : nullptr;
+    // without the reference: the pipeline's cache must still equal the sequential drop-in composition
+    bool cache_equal = cache.layers == seq.layers && (!check || (rc && qvref_cache_layers(rc) == cache.layers.size()));
+    for (size_t l = 0; check && cache_equal && l < cache.layers.size(); ++l) {
+        const size_t r = qvref_cache_rows(rc, l), d = cfg.d_model;
+        std::vector<float> k(r * d), v(r * d);
+        std::vector<uint64_t> o(r);
+        qvref_cache_copy_layer(rc, l, k.data(), v.data(), o.data());
+        cache_equal = same_bits(cache.layers[l].k, k.data(), r * d) && same_bits(cache.layers[l].v, v.data(), r * d) &&
+                      same_bits(cache.layers[l].origin, o.data(), r);
+    }
+    const bool stats_equal = (!check || (rc && cache.tokens_seen == qvref_cache_tokens_seen(rc))) &&
+                             cache.tokens_seen == seq.tokens_seen && cache.retained_per_group == seq.retained_per_group;
+    const double ms_dec = std::chrono::duration<double, std::milli>(s1 - s0).count();
+    const double ms_pre = std::chrono::duration<double, std::milli>(s2 - s1).count();
+    std::printf(
+        "{\"frames_equal\": %s, \"cache_equal\": %s, \"stats_equal\": %s, \"slots\": %zu, \"groups\": %zu, "
+        "\"intervals\": %zu, \"cores\": %zu, \"t_dec_ms\": %.3f, \"t_prefill_ms\": %.3f, \"t_g_dec_ms\": %.3f, "
+        "\"t_g_prefill_ms\": %.3f, \"delta_ms\": %.3f, \"t_total_measured_ms\": %.3f, "
+        "\"t_total_predicted_ms\": %.3f, \"sequential_decode_ms\": %.3f, \"sequential_prefill_ms\": %.3f, "
+        "\"sequential_total_ms\": %.3f}\n",
+        frames_equal ? "true" : "false", cache_equal ? "true" : "false", stats_equal ? "true" : "false",
+        spec.indices.size(), rep.groups.size(), rep.intervals, pc.cores, rep.t_dec, rep.t_prefill, rep.t_g_dec,
+        rep.t_g_prefill, rep.delta, rep.t_total_measured, rep.t_total_predicted, ms_dec, ms_pre, ms_dec + ms_pre);
+    if (rc) qvref_cache_destroy(rc);
+    if (ref) qvref_model_destroy(ref);
+    return frames_equal && cache_equal && stats_equal ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
     try {
         if (argc >= 2 && std::string(argv[1]) == "pipeline" && argc == 16) return pipeline(argv + 2);
         if (argc >= 2 && std::string(argv[1]) == "errors") return errors();
         if (argc >= 2 && std::string(argv[1]) == "bench" && argc == 16) return bench(argv + 2, 3);
+        if (argc >= 2 && std::string(argv[1]) == "overlap" && argc == 21) return overlap(argv + 2);
     } catch (const std::exception& e) {
         std::printf("{\"exception\": \"%s\"}\n", e.what());
         return 2;
     }
-    std::fprintf(stderr, "usage: parity_driver pipeline <14 args> | bench <14 args> | errors\n");
+    std::fprintf(stderr, "usage: parity_driver pipeline <14 args> | bench <14 args> | overlap <19 args> | errors\n");
     return 64;
 }
