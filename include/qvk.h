@@ -65,6 +65,12 @@ int qvk_free(void* p_d);
 int qvk_memcpy_h2d(void* dst_d, const void* src, size_t bytes, qvk_stream_t stream);
 int qvk_memcpy_d2h(void* dst, const void* src_d, size_t bytes, qvk_stream_t stream);
 int qvk_stream_sync(qvk_stream_t stream);
+/* Synchronous copies between PAGEABLE host memory (e.g. the std::vectors of the reference's API) and the device,
+ * ordered after the work already on `stream`: staged through pinned double buffers, the DMA of one chunk overlapping
+ * the multi-threaded host copy of the previous one (plain cudaMemcpy from pageable memory runs at ~2 GB/s D2H on the
+ * B200 box, the staged copy at several times that). */
+int qvk_memcpy_d2h_pageable(void* dst, const void* src_d, size_t bytes, qvk_stream_t stream);
+int qvk_memcpy_h2d_pageable(void* dst_d, const void* src, size_t bytes, qvk_stream_t stream);
 
 /* ---- (a1) group scheduler, host side ------------------------------------------------------------------------- */
 /* prefill.cpp:325-328 group_count; "frames_per_group must be >= 1" on fpg == 0. */

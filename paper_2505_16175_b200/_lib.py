@@ -60,6 +60,8 @@ _SIGS = {
     "qvk_memcpy_h2d": (C.c_int, [P, P, SZ, P]),
     "qvk_memcpy_d2h": (C.c_int, [P, P, SZ, P]),
     "qvk_stream_sync": (C.c_int, [P]),
+    "qvk_memcpy_d2h_pageable": (C.c_int, [P, P, SZ, P]),
+    "qvk_memcpy_h2d_pageable": (C.c_int, [P, P, SZ, P]),
     "qvk_group_count": (C.c_int, [U64, U32, C.POINTER(U64)]),
     "qvk_retained_count": (SZ, [F64, SZ]),
     "qvk_validate_rho": (C.c_int, [F64]),

@@ -7,8 +7,8 @@
 // which is exactly what the overlap must avoid.  Consumer (the calling thread): group g (frame slots
 // [g*fpg, min((g+1)*fpg, F)), prefill.cpp:170-183) becomes ready once every interval whose pts range can hold one
 // of its frames has finished (and every one of its slots has been written); it is then tokenized and prefilled on
-// the GPU through the drop-in API — tokenize_group + prefill_group, bit-identical to the reference — strictly in
-// group order (the cache's append order, prefill.hpp:132-133), while the CPU keeps decoding later intervals.
+// the GPU through the drop-in's exact kernels — tokenize_group + prefill_group with the tokens kept in HBM,
+// bit-identical to the reference — strictly in group order (the cache's append order, prefill.hpp:132-133), while the CPU keeps decoding later intervals.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
@@ -25,6 +25,12 @@ void decode_one_interval(const VideoFile& file, const ScanResult& scan, const Of
                          uint64_t interval_start, uint64_t interval_end, bool last_interval, FrameBuffer& out,
                          const IntervalHooks* hooks, size_t index);
 }  // namespace qv::detail
+
+namespace qv::internal {
+// prefill_shim.cpp: tokenize the frames on the device and prefill them as one group (tokens stay in HBM).
+void prefill_frames_group(const StandInModel& model, const FrameBuffer& frames, size_t frame_begin, size_t frame_end,
+                          const PruneConfig& prune, KvCache& cache);
+}  // namespace qv::internal
 
 namespace qvx {
 namespace {
@@ -146,8 +152,7 @@ qv::KvCache run_pipeline(const qv::VideoFile& file, const qv::SampleSpec& spec, 
             }
             times[g].ready_ms = ms(t0, Clock::now());
             const auto a = Clock::now();
-            const qv::TokenGroup group = model.tokenize_group(buffer, f0, f1, g);
-            qv::prefill_group(model, group, cfg.prune, cache);
+            qv::internal::prefill_frames_group(model, buffer, f0, f1, cfg.prune, cache);
             const auto b = Clock::now();
             times[g].start_ms = ms(t0, a);
             times[g].done_ms = ms(t0, b);

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <list>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -28,12 +29,52 @@ void check(int rc) {
     if (rc != QVK_OK) throw Error(qvk_last_error());
 }
 
-// Owning device allocation.
+// Device blocks are recycled through a process-wide free list (cudaMalloc / cudaFree cost milliseconds and cudaFree
+// synchronises the device — per call, that was most of a small group's prefill time).  A block is reused for any
+// request it covers by at most 2x; the list is leaked at exit (no HBM freed from static destructors).
+class Pool {
+public:
+    static void* acquire(size_t bytes) {
+        auto& p = inst();
+        {
+            std::lock_guard<std::mutex> lk(p.mu);
+            auto it = p.free.lower_bound(bytes);
+            if (it != p.free.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+                void* q = it->second;
+                p.size[q] = it->first;
+                p.free.erase(it);
+                return q;
+            }
+        }
+        void* q = nullptr;
+        check(qvk_malloc(&q, bytes));
+        std::lock_guard<std::mutex> lk(p.mu);
+        p.size[q] = bytes;
+        return q;
+    }
+    static void release(void* q) {
+        if (!q) return;
+        auto& p = inst();
+        std::lock_guard<std::mutex> lk(p.mu);
+        p.free.emplace(p.size[q], q);
+    }
+
+private:
+    std::mutex mu;
+    std::multimap<size_t, void*> free;
+    std::map<void*, size_t> size;
+    static Pool& inst() {
+        static auto* p = new Pool();
+        return *p;
+    }
+};
+
+// Owning device allocation (from the pool).
 class Dev {
 public:
     Dev() = default;
-    explicit Dev(size_t bytes) { check(qvk_malloc(&p_, bytes)); }
-    Dev(const void* host, size_t bytes) : Dev(bytes) { check(qvk_memcpy_h2d(p_, host, bytes, nullptr)); }
+    explicit Dev(size_t bytes) : p_(Pool::acquire(std::max<size_t>(bytes, 256))) {}
+    Dev(const void* host, size_t bytes) : Dev(bytes) { check(qvk_memcpy_h2d_pageable(p_, host, bytes, nullptr)); }
     Dev(const Dev&) = delete;
     Dev& operator=(const Dev&) = delete;
     Dev(Dev&& o) noexcept : p_(o.p_) { o.p_ = nullptr; }
@@ -41,7 +82,7 @@ public:
         std::swap(p_, o.p_);
         return *this;
     }
-    ~Dev() { qvk_free(p_); }
+    ~Dev() { Pool::release(p_); }
     template <class T = void>
     T* get() const { return static_cast<T*>(p_); }
 
@@ -52,8 +93,7 @@ private:
 template <class T>
 void download(std::vector<T>& out, const Dev& d, size_t count) {
     out.resize(count);
-    check(qvk_memcpy_d2h(out.data(), d.get(), count * sizeof(T), nullptr));
-    check(qvk_stream_sync(nullptr));
+    check(qvk_memcpy_d2h_pageable(out.data(), d.get(), count * sizeof(T), nullptr));
 }
 
 // Device group descriptor for one group of `n` tokens keeping `keep` of them.
@@ -91,6 +131,7 @@ struct DeviceModel {
     uint64_t seed = 0;
     size_t d = 0, layers = 0, text = 0;
     std::vector<Dev> wk, wv;
+    Dev embed;  // (d, 3) fp32 (prefill.cpp:105)
     Dev query;  // (text_tokens, d) fp32: prompt * W_q (prefill.cpp:106-113)
 };
 
@@ -121,6 +162,8 @@ std::shared_ptr<const DeviceModel> device_model(const ModelConfig& cfg) {
         check(qvk_seeded_matrix(nullptr, cfg.seed, kTagKey, l, d * d, proj_scale, m->wk.back().get<float>()));
         check(qvk_seeded_matrix(nullptr, cfg.seed, kTagValue, l, d * d, proj_scale, m->wv.back().get<float>()));
     }
+    m->embed = Dev(d * 3 * sizeof(float));
+    check(qvk_seeded_matrix(nullptr, cfg.seed, kTagEmbed, 0, d * 3, 1.0 / 255.0, m->embed.get<float>()));
     // Text query = prompt * W_q, both generated and multiplied on the device (prefill.cpp:106-113).
     const size_t t = cfg.text_tokens;
     Dev prompt(std::max<size_t>(1, t * d) * sizeof(float)), wq(d * d * sizeof(float));
@@ -173,56 +216,70 @@ struct Groups {
     }
 };
 
-// prefill_group / prefill for a batch of groups (prefill.cpp:293-323), all on the device: the tokens go up once,
-// then per layer ONE exact projection over every group's tokens (K and V), ONE qvk_prune over every group (the
-// retained rows land at the static offsets the in-order append would give them, prefill.cpp:304-308), and the
-// layer's pruned rows come back with one copy per tensor; a single synchronisation at the end.
-void prefill_batch(const StandInModel& model, std::span<const TokenGroup> groups, const PruneConfig& prune,
-                   KvCache& cache) {
-    const ModelConfig& cfg = model.config();
-    prune.validate();  // prune_group's order: rho, then the empty group, then the text query (prefill.cpp:258-275)
+// Checks of prune_group in the reference's order (prefill.cpp:258-275): rho, the empty group, the text query.
+void check_prune(const StandInModel& model, std::span<const TokenGroup> groups, const PruneConfig& prune) {
+    prune.validate();
     for (const TokenGroup& grp : groups)
         if (grp.token_count == 0) throw Error("prune: empty group");
+    if (prune.rho != 1.0 && prune.scorer == Scorer::attention_score && model.text_query().empty())
+        throw Error("attention_score scorer requires a text query");
+}
+
+// prefill_group / prefill for a batch of groups (prefill.cpp:293-323) whose fp32 tokens (T x d_model) are already in
+// HBM: per layer ONE exact projection over every group's tokens (K and V), ONE qvk_prune over every group (the
+// retained rows land at the static offsets the in-order append would give them, prefill.cpp:304-308), and the
+// layer's pruned rows come back with one staged copy per tensor.
+void prefill_device(const StandInModel& model, const float* x_d, const Groups& gr, const PruneConfig& prune,
+                    KvCache& cache, std::span<const size_t> token_counts) {
+    const ModelConfig& cfg = model.config();
     const bool text = prune.rho != 1.0 && prune.scorer == Scorer::attention_score;
-    if (text && model.text_query().empty()) throw Error("attention_score scorer requires a text query");
     auto dm = device_model(cfg);
     const size_t d = cfg.d_model;
-    Groups gr(groups, prune.rho);
     const size_t T = static_cast<size_t>(gr.g.total_tokens), R = static_cast<size_t>(gr.g.total_rows);
-    Dev x(T * d * sizeof(float)), k(T * d * sizeof(float)), v(T * d * sizeof(float));
-    for (size_t i = 0; i < groups.size(); ++i)
-        check(qvk_memcpy_h2d(x.get<float>() + gr.tok_off[i] * d, groups[i].tokens.data(),
-                             groups[i].token_count * d * sizeof(float), nullptr));
+    Dev k(T * d * sizeof(float)), v(T * d * sizeof(float));
     Dev kc(std::max<size_t>(1, R * d) * sizeof(float)), vc(std::max<size_t>(1, R * d) * sizeof(float));
     Dev org(std::max<size_t>(1, R) * sizeof(uint64_t));
     Dev sc(T * sizeof(double)), ix(std::max<size_t>(1, R) * sizeof(uint32_t));
     const size_t text_count = text ? model.text_query().size() / d : 0;
-    std::vector<size_t> base(cfg.layers);
     for (uint32_t l = 0; l < cfg.layers; ++l) {
-        check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(T), static_cast<int32_t>(d),
+        check(qvk_project_exact(nullptr, x_d, static_cast<int64_t>(T), static_cast<int32_t>(d),
                                 dm->wk[l].get<float>(), static_cast<int32_t>(d), k.get<float>()));
-        check(qvk_project_exact(nullptr, x.get<float>(), static_cast<int64_t>(T), static_cast<int32_t>(d),
+        check(qvk_project_exact(nullptr, x_d, static_cast<int64_t>(T), static_cast<int32_t>(d),
                                 dm->wv[l].get<float>(), static_cast<int32_t>(d), v.get<float>()));
         check(qvk_prune(nullptr, &gr.g, k.get(), v.get(), QVK_F32, 1, static_cast<int32_t>(d),
                         static_cast<int32_t>(prune.scorer), prune.rho, text ? dm->query.get<float>() : nullptr,
                         static_cast<int64_t>(text_count), static_cast<int32_t>(cfg.n_h), sc.get<double>(),
                         ix.get<uint32_t>(), kc.get(), vc.get(), org.get<uint64_t>()));
         LayerCache& layer = cache.layers[l];
-        base[l] = layer.origin.size();
+        const size_t base = layer.origin.size();
         layer.k.resize(layer.k.size() + R * d);
         layer.v.resize(layer.v.size() + R * d);
-        layer.origin.resize(base[l] + R);
-        // stream-ordered after this layer's prune and before the next layer's, which reuses kc / vc / org
-        check(qvk_memcpy_d2h(layer.k.data() + base[l] * d, kc.get(), R * d * sizeof(float), nullptr));
-        check(qvk_memcpy_d2h(layer.v.data() + base[l] * d, vc.get(), R * d * sizeof(float), nullptr));
-        check(qvk_memcpy_d2h(layer.origin.data() + base[l], org.get(), R * sizeof(uint64_t), nullptr));
+        layer.origin.resize(base + R);
+        // synchronous, stream-ordered after this layer's prune and before the next layer's (which reuses kc / vc)
+        check(qvk_memcpy_d2h_pageable(layer.k.data() + base * d, kc.get(), R * d * sizeof(float), nullptr));
+        check(qvk_memcpy_d2h_pageable(layer.v.data() + base * d, vc.get(), R * d * sizeof(float), nullptr));
+        check(qvk_memcpy_d2h_pageable(layer.origin.data() + base, org.get(), R * sizeof(uint64_t), nullptr));
     }
-    check(qvk_stream_sync(nullptr));
-    for (size_t i = 0; i < groups.size(); ++i) {  // prefill.cpp:309-313 (last layer's retained count)
+    for (size_t i = 0; i < token_counts.size(); ++i) {  // prefill.cpp:309-313 (last layer's retained count)
         cache.retained_per_group.push_back(static_cast<size_t>(gr.keep[i]));
-        cache.tokens_seen += groups[i].token_count;
-        cache.peak_group_tokens = std::max(cache.peak_group_tokens, groups[i].token_count);
+        cache.tokens_seen += token_counts[i];
+        cache.peak_group_tokens = std::max(cache.peak_group_tokens, token_counts[i]);
     }
+}
+
+void prefill_batch(const StandInModel& model, std::span<const TokenGroup> groups, const PruneConfig& prune,
+                   KvCache& cache) {
+    check_prune(model, groups, prune);
+    const size_t d = model.config().d_model;
+    Groups gr(groups, prune.rho);
+    Dev x(static_cast<size_t>(gr.g.total_tokens) * d * sizeof(float));
+    std::vector<size_t> counts;
+    for (size_t i = 0; i < groups.size(); ++i) {
+        check(qvk_memcpy_h2d_pageable(x.get<float>() + gr.tok_off[i] * d, groups[i].tokens.data(),
+                                      groups[i].token_count * d * sizeof(float), nullptr));
+        counts.push_back(groups[i].token_count);
+    }
+    prefill_device(model, x.get<float>(), gr, prune, cache, counts);
 }
 
 }  // namespace
@@ -455,6 +512,30 @@ KvCache prefill(const StandInModel& model, std::span<const TokenGroup> groups, c
     prefill_batch(model, groups, prune, cache);  // every group in one batch: same cache as the in-order loop
     return cache;
 }
+
+namespace internal {
+// The overlap pipeline's consumer step (csrc/shim/pipeline.cpp): frames (n_frames slots of the caller's buffer) ->
+// exact tokens in HBM (the reference's tokenize_group, prefill.cpp:123-168) -> prefill_group on those tokens, the
+// tokens never leaving the device.  Same cache rows as tokenize_group + prefill_group.
+void prefill_frames_group(const StandInModel& model, const FrameBuffer& frames, size_t frame_begin, size_t frame_end,
+                          const PruneConfig& prune, KvCache& cache) {
+    const ModelConfig& cfg = model.config();
+    TokenGroup meta;  // token_count / first_token of the group (prefill.cpp:170-183), no tokens
+    meta.first_token = uint64_t(frame_begin) * cfg.tokens_per_frame;
+    meta.token_count = (frame_end - frame_begin) * size_t{cfg.tokens_per_frame};
+    check_prune(model, std::span<const TokenGroup>(&meta, 1), prune);
+    const size_t n_frames = frame_end - frame_begin, d = cfg.d_model;
+    auto dm = device_model(cfg);
+    Dev pixels(frames.slot(frame_begin).data(), n_frames * frames.slot_bytes());
+    Dev x(std::max<size_t>(1, meta.token_count * d) * sizeof(float));
+    check(qvk_tokenize(nullptr, pixels.get<uint8_t>(), static_cast<int64_t>(n_frames), frames.width(),
+                       frames.height(), cfg.tokens_per_frame, dm->embed.get<float>(), static_cast<int32_t>(d),
+                       x.get<float>()));
+    Groups gr(std::span<const TokenGroup>(&meta, 1), prune.rho);
+    const size_t count = meta.token_count;
+    prefill_device(model, x.get<float>(), gr, prune, cache, std::span<const size_t>(&count, 1));
+}
+}  // namespace internal
 
 uint64_t group_count(uint64_t total_frames, uint32_t frames_per_group) {
     uint64_t out = 0;
