@@ -206,3 +206,30 @@ def test_synth_is_deterministic_and_normalish():
     assert abs(x.mean()) < 0.02 and abs(x.std() - 1.0) < 0.02
     c = O.synth_bf16(1, 1, 0, 1, 512, 2, 64, False)
     assert a.tobytes() != c.tobytes()
+
+
+@pytest.mark.skipif(O.ref is None, reason="reference oracle not built")
+def test_gqa_attention_score_oracle_pinned():
+    """The GQA attention_score oracle (oracle.text_query_sum + score_text_ref, the checker of qvk_score_text): the
+    pre-summed query equals a pure-Python loop in the stated order, and the scores through the unmodified reference
+    equal the C restatement's attention_score on the same single row, divided by the same divisor."""
+    rng = np.random.default_rng(3)
+    T, n_q, n_kv, d, n = 3, 4, 2, 8, 17
+    q = rng.standard_normal((T, n_q, d)).astype(np.float32)
+    k = O.bf16_to_f32(O.synth_bf16(2, 1, 0, 0, n, n_kv, d, True)).reshape(n, n_kv, d)
+    qbar = O.text_query_sum(q, n_q, n_kv, d)
+    gq = n_q // n_kv
+    for h in range(n_kv):
+        for j in range(d):
+            acc = 0.0
+            for t in range(T):
+                for x in range(gq):
+                    acc += float(q[t, h * gq + x, j])
+            assert np.float32(acc) == qbar[h, j]
+    per_head = O.score_text_ref(k, n, n_q, n_kv, d, True, qbar, T)
+    for h in range(n_kv):
+        port = O.score_attention(np.ascontiguousarray(k[:, h]), n, 1, d, qbar[h], 1)
+        assert np.array_equal(per_head[h], port / (T * gq))
+    per_tok = O.score_text_ref(k, n, n_q, n_kv, d, False, qbar, T)
+    port = O.score_attention(k.reshape(n, -1), n, 1, n_kv * d, qbar.ravel(), 1)
+    assert np.array_equal(per_tok[0], port / (T * n_q))

@@ -26,5 +26,9 @@ ncu)
      $B > "$OUT/ncu_attn.log" 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:prune_fused -s 2 -c 1 -f -o "$OUT/prune" \
      $B > "$OUT/ncu_prune.log" 2>&1 ;;
+snapncu)
+  timeout 300 python tools/snapkv_bench.py > "$OUT/snapkv_bench.jsonl" 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:snapkv_tc -s 1 -c 1 -f -o "$OUT/snap" \
+     python tools/snapkv_bench.py > "$OUT/ncu_snap.log" 2>&1 ;;
 esac; done
 ls -la "$OUT"
