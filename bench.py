@@ -300,11 +300,15 @@ def main():
     # over gloo, so the multi-rank path (sharding, cache all-gather, max-over-ranks timing) can be exercised on a
     # 1-GPU box; NCCL refuses two ranks on one device, so there the all-gather is torch's (gloo) broadcasts.
     share = os.environ.get("QVK_BENCH_SHARE_GPU") == "1"
+    # Test hook (not used by the driver): QVK_BENCH_FORCE_COMM=1 under torchrun with one rank runs the N > 1 code path
+    # (process group, the C ABI's NCCL communicator, per-layer all-gathers on the comm stream, the all-gather report)
+    # on a single GPU, where NCCL's collectives degenerate to one rank.
+    multi = world > 1 or os.environ.get("QVK_BENCH_FORCE_COMM") == "1"
     if share:
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if multi:
         if share:
             dist.init_process_group("gloo")
         else:
@@ -342,9 +346,9 @@ def main():
     bufs = [qp.LayerBuffers(o, scores, idx, k_cache[l], v_cache[l], origin[l]) for l in range(L)]
 
     comm = None
-    if world > 1 and not share:
+    if multi and not share:
         comm = NcclComm()  # the C ABI's communicator (qvk_comm_init over the torch process group's bootstrap)
-    comm_stream = torch.cuda.Stream(dev) if world > 1 else None
+    comm_stream = torch.cuda.Stream(dev) if multi else None
 
     def gather_layer(l):
         """Layer l's all-gather on the comm stream, after the layer's kernels (overlaps the next layer)."""
@@ -363,9 +367,9 @@ def main():
             # one pruned-prefill layer through the C ABI (qvk_prefill_layer): attention, then the fused prune
             # launched with PDL so its CTAs take the SMs the persistent attention grid releases in its tail
             qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, buffers=bufs[l], cache_row_offset=row_base)
-            if world > 1 and do_gather:
+            if multi and do_gather:
                 gather_layer(l)
-        if world > 1 and do_gather:
+        if multi and do_gather:
             e = torch.cuda.Event()
             e.record(comm_stream)
             stream.wait_event(e)  # the step ends when the replicated cache is complete
@@ -374,7 +378,7 @@ def main():
     nv = NvmlSampler(dev)  # polling from before the warm-up; only the samples inside the timed region are kept
     for _ in range(args.warmup):
         step()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     h0 = time.perf_counter()
@@ -387,7 +391,7 @@ def main():
     h1 = time.perf_counter()
     nv.stop()
     nv_clocks = nv.window(h0, h1)
-    if world > 1:
+    if multi:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     clocks = sampler.stop()
@@ -419,7 +423,7 @@ def main():
 
     # ---- N > 1: how much of the per-layer all-gather the overlap hides (SURVEY.md §8e "exposed vs hidden") ----
     ag_report = None
-    if world > 1:
+    if multi:
         def timed(fn, reps):
             fn()
             torch.cuda.synchronize()
@@ -457,7 +461,7 @@ def main():
     attn_ms = [a.elapsed_time(b) for a, b in attn_ev]
     prune_ms = [a.elapsed_time(b) for a, b in prune_ev]
     el = torch.tensor([elapsed_ms, statistics.mean(attn_ms), statistics.mean(prune_ms)], device=dev)
-    if world > 1:
+    if multi:
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
     elapsed_ms, attn_avg, prune_avg = el.tolist()
     total_tokens = plan.total_tokens
@@ -484,9 +488,9 @@ def main():
             for l in range(L):
                 qp.prefill_layer_x(x, wqkv[l], g, n_q, n_kv, d, rho, buffers=bufs[l], qkv=qkv,
                                    cache_row_offset=row_base)
-                if world > 1:
+                if multi:
                     gather_layer(l)
-            if world > 1:
+            if multi:
                 e = torch.cuda.Event()
                 e.record(comm_stream)
                 stream.wait_event(e)
@@ -495,7 +499,7 @@ def main():
         for _ in range(max(1, min(args.warmup, 2))):
             full_step()
         torch.cuda.synchronize()
-        if world > 1:
+        if multi:
             dist.barrier()
         f0, f1 = ev(), ev()
         f0.record(stream)
@@ -512,7 +516,7 @@ def main():
             pj.append((a0, a1))
         torch.cuda.synchronize()
         t = torch.tensor([f0.elapsed_time(f1), statistics.mean(a.elapsed_time(b) for a, b in pj)], device=dev)
-        if world > 1:
+        if multi:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         full_ms, proj_ms = t.tolist()
         proj_fl = 2.0 * local_plan.total_tokens * d_model * (n_q + 2 * n_kv) * d
@@ -541,13 +545,15 @@ def main():
         fp = qp.FramePrefill(local_plan, c["tokens_per_frame"], side, side, embed, wqkv, n_q, n_kv, d, rho, dev,
                              chunks=chunks, cache_rows=R, row_base=row_base)
         # each rank reads back the pruned rows it computed, of every layer (the device all-gather replicates the
-        # cache on the GPUs, where the decode step consumes it)
-        out_k = torch.empty(fp.k_cache.numel(), dtype=torch.bfloat16, pin_memory=True)
-        out_v = torch.empty(fp.v_cache.numel(), dtype=torch.bfloat16, pin_memory=True)
-        out_o = torch.empty(fp.origin.numel(), dtype=torch.int64, pin_memory=True)
+        # cache on the GPUs, where the decode step consumes it): pinned host buffers of this rank's rows only (8 ranks
+        # x the whole 26.8 GB cache would not fit the host)
+        lr = local_plan.total_rows
+        out_k = torch.empty(L * lr * unit, dtype=torch.bfloat16, pin_memory=True)
+        out_v = torch.empty(L * lr * unit, dtype=torch.bfloat16, pin_memory=True)
+        out_o = torch.empty(L * lr * n_kv, dtype=torch.int64, pin_memory=True)
 
         def gather_f():
-            if world > 1:
+            if multi:
                 for l in range(L):
                     if comm is not None:
                         comm.allgather(fp.k_cache[l], fp.v_cache[l], fp.origin[l], bounds, n_kv, d, stream)
@@ -556,20 +562,20 @@ def main():
 
         e_steps = args.steps
         for _ in range(max(1, min(args.warmup, 2))):
-            fp.run(hframes, out_k, out_v, out_o, after_compute=gather_f, join=False)
+            fp.run(hframes, out_k, out_v, out_o, after_compute=gather_f, join=False, out_local=True)
         fp.join()
         torch.cuda.synchronize()
-        if world > 1:
+        if multi:
             dist.barrier()
         e0, e1 = ev(), ev()
         e0.record(stream)
         for _ in range(e_steps):
-            fp.run(hframes, out_k, out_v, out_o, after_compute=gather_f, join=False)
+            fp.run(hframes, out_k, out_v, out_o, after_compute=gather_f, join=False, out_local=True)
         fp.join()  # the last step's readback is inside the timed region
         e1.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], device=dev)
-        if world > 1:
+        if multi:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_f = t.item()
         d2h = local_plan.total_rows * n_kv * (2 * d * 2 + 8) * L
@@ -631,7 +637,7 @@ def main():
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
     return 0
 

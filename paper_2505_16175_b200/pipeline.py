@@ -63,7 +63,7 @@ class _Pipeline:
             s.wait_event(e)
         self._tail = []
 
-    def _pipeline(self, upload, out_k, out_v, out_o, unit, after_compute, join):
+    def _pipeline(self, upload, out_k, out_v, out_o, unit, after_compute, join, out_local=False):
         main = torch.cuda.current_stream(self.dev)
         start = torch.cuda.Event()
         start.record(main)  # inputs / outputs the caller prepared on its stream before this call
@@ -87,7 +87,8 @@ class _Pipeline:
             self._consumed[c].record(main)
             if out_k is not None:
                 self.d2h.wait_event(self._consumed[c])
-                a, b = self.row_base + r0, self.row_base + r1
+                base = 0 if out_local else self.row_base  # host outputs sized for this rank's rows only, or global
+                a, b = base + r0, base + r1
                 L_ = self.k_cache.shape[0]
                 ok, ov, oo = out_k.view(L_, -1), out_v.view(L_, -1), out_o.view(L_, -1)
                 with torch.cuda.stream(self.d2h):
@@ -237,15 +238,16 @@ class FramePrefill(_Pipeline):
                                           self.v_cache[l, cr * unit:].data_ptr(),
                                           self.origin[l, cr * self.n_kv:].data_ptr()))
 
-    def run(self, hframes, out_k=None, out_v=None, out_o=None, after_compute=None, join=True):
-        """One layer from pinned host frames (F, 3, H, W) uint8 into the device cache; optional pinned host outputs
-        receive this rank's pruned rows chunk by chunk; `after_compute` (e.g. the multi-GPU all-gather) runs on the
-        device after the last chunk's kernels.  join=False: see `_Pipeline.join`."""
+    def run(self, hframes, out_k=None, out_v=None, out_o=None, after_compute=None, join=True, out_local=False):
+        """Every layer from pinned host frames (F, 3, H, W) uint8 into the device caches; optional pinned host outputs
+        (layers x rows) receive this rank's pruned rows chunk by chunk — at their global cache rows, or from row 0 with
+        out_local=True (host buffers sized for this rank's rows only); `after_compute` (e.g. the multi-GPU
+        all-gather) runs on the device after the last chunk's kernels.  join=False: see `_Pipeline.join`."""
         def upload(part):
             f0, f1 = part[0] // self.tpf, part[1] // self.tpf
             self.frames[f0:f1].copy_(hframes[f0:f1], non_blocking=True)
 
-        self._pipeline(upload, out_k, out_v, out_o, self.n_kv * self.d, after_compute, join)
+        self._pipeline(upload, out_k, out_v, out_o, self.n_kv * self.d, after_compute, join, out_local)
 
 
 class StreamingPrefill(FramePrefill):

@@ -31,4 +31,7 @@ for G, N in ((64, 1024), (64, 4096)):
         ts.append(a.elapsed_time(b))
     ms = statistics.median(ts)
     byt = G * N * 4 * 128 * 2 + G * 32 * 28 * 128 * 2 + G * N * 4 * 8
-    print(json.dumps({"groups": G, "tokens": N, "ms": ms, "bytes": byt, "gbs": byt / ms / 1e6}), flush=True)
+    exps = G * 4 * 7 * 32 * N  # exponentials of ONE pass (window rows x keys)
+    floor_ms = 2 * exps / (16 * 148 * 1.965e9) * 1e3  # the MUFU floor of the two-exponential formulation
+    print(json.dumps({"groups": G, "tokens": N, "ms": ms, "bytes": byt, "gbs": byt / ms / 1e6,
+                      "mufu_floor_2exp_ms": floor_ms, "frac_of_mufu_floor": floor_ms / ms}), flush=True)
