@@ -63,6 +63,7 @@ def test_c_example_matches_python_path(tmp_path):
     assert np.array_equal(c_kc, kc.view(torch.int16).cpu().numpy().view(np.uint16))
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("nbytes", [1, 4 << 20, (4 << 20) + 1, (32 << 20) + 12345, (100 << 20) + 7])
 def test_pageable_staged_copies(cuda, nbytes):
     """qvk_memcpy_{h2d,d2h}_pageable: pageable host buffers through the pinned double-buffered staging, every chunk
