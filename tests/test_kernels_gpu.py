@@ -347,13 +347,19 @@ def test_snapkv_vs_oracle(cuda, sizes, window, pool):
                                1 / math.sqrt(128))
         seg = got[n_kv * t0: n_kv * (t0 + n)].reshape(n_kv, n)
         np.testing.assert_allclose(seg, want, rtol=1e-4, atol=1e-6)
-        # index sets: exact unless the oracle boundary gap is inside the near-tie band (tau = 1e-4 relative)
+        # index sets, barring near-ties: an index may be in one set and not the other only if its oracle score lies
+        # within tau = 1e-4 (relative, the fp32 scores' tolerance) of the oracle's k-th score; the count is reported
         kk = plan.keep[gi]
         for h in range(n_kv):
+            got_set = set(O.top_k(seg[h], kk).tolist())
             order = np.argsort(-want[h], kind="stable")
-            gap = want[h][order[kk - 1]] - want[h][order[kk]] if kk < n else np.inf
-            if gap > 1e-4 * abs(want[h][order[kk - 1]]):
-                assert set(O.top_k(seg[h], kk).tolist()) == set(O.top_k(want[h], kk).tolist())
+            want_set = set(order[:kk].tolist())
+            kth = want[h][order[kk - 1]]
+            diff = got_set ^ want_set
+            near = [i for i in diff if abs(want[h][i] - kth) <= 1e-4 * abs(kth)]
+            assert len(diff) == len(near), f"group {gi} head {h}: index differences outside the near-tie band"
+            if diff:
+                print(f"snapkv group {gi} head {h}: {len(diff)} near-tie index differences")
         t0 += n
 
 
