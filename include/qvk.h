@@ -176,6 +176,26 @@ int qvk_prefill_layer(qvk_stream_t stream, const qvk_groups* groups, const qvk_l
                       const void* k_d, const void* v_d, void* o_d, double* scores_ws_d, uint32_t* idx_ws_d,
                       void* k_cache_d, void* v_cache_d, uint64_t* origin_d);
 
+/* ---- per-model / per-video context: the plan on the device and every workspace, allocated once -------------------- */
+/* The reference builds its StandInModel once and shares it read-only (prefill.hpp:72); a serving loop over the layers
+ * of a video (and over consecutive videos of the same shape) should likewise pay allocation, plan upload and
+ * workspace sizing once.  qvk_ctx_create takes the group plan on the HOST (tok_off: n_groups + 1 token offsets,
+ * first_token: n_groups global token ids, NULL = tok_off) and the layer parameters; it computes keep / row_off
+ * (retained_count, prefill.cpp:235-238), uploads them, and allocates the scores / idx / text-query workspaces on the
+ * current device.  qvk_ctx_groups returns the device descriptor (valid until qvk_ctx_destroy) for the other entry
+ * points; qvk_ctx_prefill_layer(_x) run one layer with the context's plan, parameters and workspaces (no allocation,
+ * no host synchronisation).  A context may be used from one stream at a time. */
+typedef struct qvk_ctx_st* qvk_ctx_t;
+int qvk_ctx_create(qvk_ctx_t* out, const qvk_layer_params* p, int32_t n_groups, const int64_t* tok_off,
+                   const uint64_t* first_token);
+int qvk_ctx_groups(qvk_ctx_t ctx, qvk_groups* out);
+int qvk_ctx_prefill_layer(qvk_ctx_t ctx, qvk_stream_t stream, const void* q_d, const void* k_d, const void* v_d,
+                          void* o_d, void* k_cache_d, void* v_cache_d, uint64_t* origin_d);
+int qvk_ctx_prefill_layer_x(qvk_ctx_t ctx, qvk_stream_t stream, const void* x_d, int32_t d_model, const void* w_d,
+                            void* q_ws_d, void* k_ws_d, void* v_ws_d, void* o_d, void* k_cache_d, void* v_cache_d,
+                            uint64_t* origin_d);
+int qvk_ctx_destroy(qvk_ctx_t ctx);
+
 /* ---- §8f-1: QKV projection (tcgen05 GEMM) with the key-norm score fused into its epilogue ------------------------ */
 /* [Q | K | V] = X . W^T: x_d (tokens, d_model) bf16, w_d ((n_q + 2 n_kv) d_h, d_model) bf16 row-major (the
  * nn.Linear layout of the stacked q/k/v projection weights); outputs q_d (tokens, n_q, d_h), k_d / v_d

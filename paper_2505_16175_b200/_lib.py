@@ -80,6 +80,11 @@ _SIGS = {
     "qvk_comm_group_end": (C.c_int, []),
     "qvk_allgather_layer": (C.c_int, [P, P, P, I32, I32, P, P, P]),
     "qvk_last_prune_route": (C.c_int, []),
+    "qvk_ctx_create": (C.c_int, [C.POINTER(P), C.POINTER(QvkLayerParams), I32, P, P]),
+    "qvk_ctx_groups": (C.c_int, [P, GP]),
+    "qvk_ctx_prefill_layer": (C.c_int, [P, P, P, P, P, P, P, P, P]),
+    "qvk_ctx_prefill_layer_x": (C.c_int, [P, P, P, I32, P, P, P, P, P, P, P, P]),
+    "qvk_ctx_destroy": (C.c_int, [P]),
     "qvk_peer_barrier": (C.c_int, [P, I32, P, I32, U32, P]),
     "qvk_snapkv_score": (C.c_int, [P, GP, P, P, I32, I32, I32, I32, I32, F32, P]),
     "qvk_select": (C.c_int, [P, GP, P, I32, P]),

@@ -620,3 +620,112 @@ int qvk_synth_bf16(qvk_stream_t s, uint64_t seed, uint32_t tag, uint32_t layer, 
 }
 
 }  // extern "C"
+
+// ---- per-model / per-video context (include/qvk.h qvk_ctx_*) ------------------------------------------------------
+struct qvk_ctx_st {
+    qvk_layer_params p{};
+    qvk_groups g{};
+    int device = 0;
+    void* arrays = nullptr;   // tok_off | keep | row_off | first_token (int64 / uint64)
+    double* scores = nullptr; // n_kv * total_tokens
+    uint32_t* idx = nullptr;  // total_rows * n_kv
+};
+
+extern "C" {
+
+int qvk_ctx_create(qvk_ctx_t* out, const qvk_layer_params* p, int32_t n_groups, const int64_t* tok_off,
+                   const uint64_t* first_token) {
+    if (!out || !p || !tok_off) QVK_INVALID("ctx: null argument");
+    *out = nullptr;
+    if (n_groups <= 0) QVK_INVALID("prefill: no token groups");  // prefill.cpp:317
+    QVK_TRY(check_rho(p->rho));
+    if (p->n_q <= 0 || p->n_kv <= 0 || p->d_h <= 0) QVK_INVALID("model config: dimensions must be positive");
+    const int G = n_groups;
+    std::vector<int64_t> host(4 * static_cast<size_t>(G) + 2);
+    int64_t* h_tok = host.data();
+    int64_t* h_keep = h_tok + G + 1;
+    int64_t* h_row = h_keep + G;
+    int64_t* h_first = h_row + G + 1;
+    int64_t mx = 0;
+    h_row[0] = 0;
+    for (int i = 0; i <= G; ++i) h_tok[i] = tok_off[i];
+    for (int i = 0; i < G; ++i) {
+        const int64_t n = tok_off[i + 1] - tok_off[i];
+        if (n < 0) QVK_INVALID("ctx: token offsets must be ascending");
+        h_keep[i] = static_cast<int64_t>(retained(p->rho, static_cast<size_t>(n)));
+        h_row[i + 1] = h_row[i] + h_keep[i];
+        h_first[i] = first_token ? static_cast<int64_t>(first_token[i]) : tok_off[i];
+        mx = std::max(mx, n);
+    }
+    auto* c = new qvk_ctx_st;
+    c->p = *p;
+    cudaGetDevice(&c->device);
+    const int heads = p->per_head ? p->n_kv : 1;
+    const int64_t T = h_tok[G] - h_tok[0], R = h_row[G];
+    if (h_tok[0] != 0) {
+        delete c;
+        QVK_INVALID("ctx: tok_off[0] must be 0");
+    }
+    auto fail = [&](cudaError_t e) {
+        set_error(std::string("CUDA error: ") + cudaGetErrorString(e) + " in qvk_ctx_create");
+        cudaFree(c->arrays);
+        cudaFree(c->scores);
+        cudaFree(c->idx);
+        delete c;
+        return QVK_E_CUDA;
+    };
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->arrays, host.size() * sizeof(int64_t))) != cudaSuccess) return fail(e);
+    if ((e = cudaMemcpy(c->arrays, host.data(), host.size() * sizeof(int64_t), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(e);
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&c->scores), sizeof(double) * std::max<int64_t>(1, T * heads))) !=
+        cudaSuccess)
+        return fail(e);
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&c->idx), sizeof(uint32_t) * std::max<int64_t>(1, R * heads))) !=
+        cudaSuccess)
+        return fail(e);
+    const int64_t* base = static_cast<const int64_t*>(c->arrays);
+    c->g.n_groups = G;
+    c->g.max_tokens = mx;
+    c->g.total_tokens = T;
+    c->g.total_rows = R;
+    c->g.tok_off_d = base;
+    c->g.keep_d = base + G + 1;
+    c->g.row_off_d = base + 2 * G + 1;
+    c->g.first_token_d = reinterpret_cast<const uint64_t*>(base + 3 * G + 2);
+    *out = c;
+    return QVK_OK;
+}
+
+int qvk_ctx_groups(qvk_ctx_t c, qvk_groups* out) {
+    if (!c || !out) QVK_INVALID("ctx: null argument");
+    *out = c->g;
+    return QVK_OK;
+}
+
+int qvk_ctx_prefill_layer(qvk_ctx_t c, qvk_stream_t s, const void* q, const void* k, const void* v, void* o,
+                          void* kc, void* vc, uint64_t* origin) {
+    if (!c) QVK_INVALID("ctx: null argument");
+    return qvk_prefill_layer(s, &c->g, &c->p, q, k, v, o, c->scores, c->idx, kc, vc, origin);
+}
+
+int qvk_ctx_prefill_layer_x(qvk_ctx_t c, qvk_stream_t s, const void* x, int32_t d_model, const void* w, void* q,
+                            void* k, void* v, void* o, void* kc, void* vc, uint64_t* origin) {
+    if (!c) QVK_INVALID("ctx: null argument");
+    return qvk_prefill_layer_x(s, &c->g, &c->p, x, d_model, w, q, k, v, o, c->scores, c->idx, kc, vc, origin);
+}
+
+int qvk_ctx_destroy(qvk_ctx_t c) {
+    if (!c) return QVK_OK;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(c->device);
+    cudaFree(c->arrays);
+    cudaFree(c->scores);
+    cudaFree(c->idx);
+    cudaSetDevice(cur);
+    delete c;
+    return QVK_OK;
+}
+
+}  // extern "C"

@@ -81,3 +81,59 @@ def test_pageable_staged_copies(cuda, nbytes):
     out = np.zeros(nbytes, np.uint8)
     check(qp.lib.qvk_memcpy_d2h_pageable(out.ctypes.data, dev.data_ptr(), nbytes, None))
     assert np.array_equal(out, src)
+
+
+@pytest.mark.gpu
+def test_context_api_matches_prefill_layer(cuda):
+    """qvk_ctx_create / qvk_ctx_prefill_layer(_x): the plan and workspaces allocated once from HOST offsets give the
+    same attention output and pruned cache as qvk_prefill_layer with caller-provided descriptors, layer after layer."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2505_16175_b200 as qp
+    from paper_2505_16175_b200 import _lib as L
+    from paper_2505_16175_b200._lib import check
+
+    sizes, n_q, n_kv, d, rho = [1024, 300, 2048], 28, 4, 128, 0.25
+    plan = qp.GroupPlan.from_sizes(sizes, rho, first_tokens=[5, 2000, 9000])
+    prm = L.QvkLayerParams(n_q, n_kv, d, int(qp.Scorer.key_norm_small), 1, rho, 1.0 / d ** 0.5, 32, 1, None, 0)
+    ctx = C.c_void_p(0)
+    tok = np.ascontiguousarray(plan.tok_off, np.int64)
+    ft = np.ascontiguousarray(plan.first_token, np.uint64)
+    check(qp.lib.qvk_ctx_create(C.byref(ctx), C.byref(prm), len(sizes), tok.ctypes.data, ft.ctypes.data))
+    try:
+        desc = L.QvkGroups()
+        check(qp.lib.qvk_ctx_groups(ctx, C.byref(desc)))
+        assert (desc.n_groups, desc.total_tokens, desc.total_rows) == (3, plan.total_tokens, plan.total_rows)
+        s = torch.cuda.current_stream().cuda_stream
+        for layer in range(2):
+            q = torch.cat([qp.synth_bf16(1, 3, layer, i, n, n_q, d, False, cuda) for i, n in enumerate(sizes)])
+            k = torch.cat([qp.synth_bf16(1, 1, layer, i, n, n_kv, d, True, cuda) for i, n in enumerate(sizes)])
+            v = torch.cat([qp.synth_bf16(1, 2, layer, i, n, n_kv, d, False, cuda) for i, n in enumerate(sizes)])
+            ref = qp.prefill_layer(q, k, v, plan.to(cuda), n_q, n_kv, rho)
+            o = torch.empty_like(q)
+            kc, vc = torch.empty_like(ref.k_cache), torch.empty_like(ref.v_cache)
+            og = torch.empty_like(ref.origin)
+            check(qp.lib.qvk_ctx_prefill_layer(ctx, s, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                               kc.data_ptr(), vc.data_ptr(), og.data_ptr()))
+            torch.cuda.synchronize()
+            assert torch.equal(o, ref.o) and torch.equal(kc, ref.k_cache) and torch.equal(vc, ref.v_cache)
+            assert torch.equal(og, ref.origin)
+        # from hidden states
+        d_model = n_q * d
+        x = torch.cat([qp.synth_bf16(1, 7, 0, i, n, 1, d_model, False, cuda) for i, n in enumerate(sizes)]).view(-1, d_model)
+        w = (qp.synth_bf16(1, 8, 0, 0, (n_q + 2 * n_kv) * d, 1, d_model, False, cuda).float() / d_model ** 0.5
+             ).to(torch.bfloat16).view(-1, d_model)
+        ref, _ = qp.prefill_layer_x(x, w, plan.to(cuda), n_q, n_kv, d, rho)
+        T = plan.total_tokens
+        qw, kw, vw = (torch.empty(T, h, d, dtype=torch.bfloat16, device=cuda) for h in (n_q, n_kv, n_kv))
+        o = torch.empty(T, n_q, d, dtype=torch.bfloat16, device=cuda)
+        kc, vc, og = torch.empty_like(ref.k_cache), torch.empty_like(ref.v_cache), torch.empty_like(ref.origin)
+        check(qp.lib.qvk_ctx_prefill_layer_x(ctx, s, x.data_ptr(), d_model, w.data_ptr(), qw.data_ptr(), kw.data_ptr(),
+                                             vw.data_ptr(), o.data_ptr(), kc.data_ptr(), vc.data_ptr(), og.data_ptr()))
+        torch.cuda.synchronize()
+        assert torch.equal(o, ref.o) and torch.equal(kc, ref.k_cache) and torch.equal(og, ref.origin)
+    finally:
+        check(qp.lib.qvk_ctx_destroy(ctx))
