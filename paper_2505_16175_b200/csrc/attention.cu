@@ -606,6 +606,8 @@ int launch_attention_d(cudaStream_t stream, const CUtensorMap& mq, const CUtenso
 
 }  // namespace
 
+int launch_attention2(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, float, void*);
+
 int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, const void* v, int n_q,
                      int n_kv, int d_h, float scale, void* o) {
     if (d_h != 128 && d_h != 64) {
@@ -618,6 +620,8 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
         QVK_INVALID("attention: q/k/v/o must be 16-byte aligned");
     if (g->total_tokens == 0 || g->max_tokens == 0) return QVK_OK;
     if (g->total_tokens > 0x7fffffff) QVK_INVALID("attention: more than 2^31 token rows");
+    if (d_h == 128 && env_knob("QVK_ATTN_2CTA", 0))  // CTA-pair variant (attention2.cu), opt-in while evaluated
+        return launch_attention2(stream, g, q, k, v, n_q, n_kv, scale, o);
     CUtensorMap mq, mk, mv;
     if (!make_map(&mq, q, n_q, g->total_tokens, d_h) || !make_map(&mk, k, n_kv, g->total_tokens, d_h) ||
         !make_map(&mv, v, n_kv, g->total_tokens, d_h)) {

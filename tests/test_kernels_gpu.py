@@ -284,6 +284,24 @@ def test_attention_vs_torch_fp32(cuda, sizes, n_q, n_kv, d):
     check_tol(o, want, f"attention {sizes} d={d}")
 
 
+@pytest.mark.parametrize("sizes,n_q,n_kv", [([256], 2, 1), ([384, 100, 1, 129], 28, 4), ([4096, 1000], 28, 4),
+                                            ([255, 257, 513], 8, 2)])
+def test_attention_cta_pair_variant_vs_torch_fp32(cuda, sizes, n_q, n_kv):
+    """The experimental CTA-pair attention (attention2.cu, QVK_ATTN_2CTA=1: M = 256 pair MMAs, double-buffered S,
+    column-split softmax) against torch fp32 — ragged groups, 1-token groups, long groups with lazy O rescales."""
+    q = synth_groups(sizes, n_q, 128, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, 128, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, 128, 2, False, cuda)
+    g = qp.GroupPlan.from_sizes(sizes, 0.5).to(cuda)
+    os.environ["QVK_ATTN_2CTA"] = "1"
+    try:
+        o = qp.attention(q, k, v, g, n_q, n_kv)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["QVK_ATTN_2CTA"]
+    check_tol(o, torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(128)), "cta-pair attention")
+
+
 def test_attention_one_step_units_no_deadlock(cuda):
     """C3 shape (1024-token groups): thousands of 1-step head-pair units per launch.  The softmax warps must not run
     two units ahead of the epilogue (mbarrier phase aliasing deadlocked this shape once)."""
