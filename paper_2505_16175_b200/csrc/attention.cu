@@ -74,6 +74,23 @@ __device__ long long g_attn_trace[1024];
     } while (0)
 #endif
 
+#ifdef QVK_ATTN_UNITLOG
+// Debug per-unit log (tools/attn_unitlog.cu): the MMA thread of every CTA stamps clock64 at the top of each of its
+// first 128 valid units (and once after the last), with the unit's K/V step count.
+__device__ long long g_attn_unitlog[1024][129][2];
+#define QVK_ULOG(i, nkv)                                                                  \
+    do {                                                                                  \
+        if (blockIdx.x < 1024 && (i) < 129) {                                             \
+            g_attn_unitlog[blockIdx.x][(i)][0] = clock64();                               \
+            g_attn_unitlog[blockIdx.x][(i)][1] = (nkv);                                   \
+        }                                                                                 \
+    } while (0)
+#else
+#define QVK_ULOG(i, nkv) \
+    do {                 \
+    } while (0)
+#endif
+
 #ifdef QVK_ATTN_STALLS
 // Debug stall accounting (tools/attn_stalls.cu): clock64 cycles per CTA spent in each barrier wait category.
 //   0 MMA: q_full  1 MMA: kv_full  2 MMA: o_free  3 MMA: p_full  4 MMA: loop total  5 units (MMA)
@@ -307,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 QVK_TRACE(39);  // unit loop top
                 const Unit w = decode_unit(p, u);
                 if (!w.valid) continue;
+                QVK_ULOG(unit_iter, w.nkv);
                 QVK_TRACE(23);  // decoded
                 const int nt[2] = {w.n0, w.n1};
                 const int qb = unit_iter & 1;
@@ -395,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 s0_pre = next_pre;
                 QVK_STALL_ADD(5, 1);
             }
+            QVK_ULOG(unit_iter, 0);
 #ifdef QVK_ATTN_STALLS
             QVK_STALL_ADD(4, clock64() - loop0);
 #endif

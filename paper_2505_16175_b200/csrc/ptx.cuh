@@ -193,6 +193,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
           "=f"(r[30]), "=f"(r[31])                                                                                \
         : "r"(taddr))
 
+#define QVK_TMEM_LD8F(taddr, r)                                                                                   \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                        \
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])  \
+                 : "r"(taddr))
+
 #define QVK_TMEM_ST32(taddr, r)                                                                                   \
     asm volatile(                                                                                                 \
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"   \

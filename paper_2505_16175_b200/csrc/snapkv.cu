@@ -159,31 +159,28 @@ __global__ void snap_pool_kernel(const float* __restrict__ raw, const int64_t* _
 // latency), warp 16 TMA, warp 17 MMA.  Pass 1: set s takes M-tile s & 1 (window rows 0-127 / 128-255) and key
 // columns 64 (s >> 1) .. +63 of every key tile, each keeping its own running (max, sum) per row, merged once per
 // item; pass 2: set s takes window columns 64 s .. 64 s + 63, the four partial per-key sums combined through smem.
-// TMEM: pass-1 S_A | S_B (256 columns), pass-2 S' (<= 256 columns).
+// TMEM: two accumulator buffers of 256 columns (pass 1: S_A | S_B, pass 2: S' of <= 256 columns), so the MMAs of
+// key tile t + 1 run while the compute warps work on tile t (single-buffered, every tile waited for the slowest warp's
+// release, then the MMA issue and execution: ~2400 cycles per tile against ~1900 of math, tools/snap_trace.cu).
 // Algorithmic bytes per (group, layer): K read once from HBM (pass 2 re-reads it from L2) + the window Q rows +
 // n_kv * N * 8 score bytes.
 constexpr int kSnapStages = 3;
 constexpr uint32_t kSnapChunk = 128 * 128;          // 128 rows x 128 B (one SW128 chunk of a key tile)
 constexpr uint32_t kSnapKTile = 2 * kSnapChunk;      // 128 keys x 128 d bf16
 constexpr uint32_t kSnapQChunk = 256 * 128;          // window-row operand: up to 256 rows x 128 B per d-chunk
-#ifndef QVK_SNAP_POLY
-#define QVK_SNAP_POLY 2  // share of the exponentials on the FMA pipe: 0 (none), 2 (1/4), 4 (1/2); see kSnapPolyPass1
+#ifndef QVK_SNAP_POLY8
+#define QVK_SNAP_POLY8 2  // exponential pairs of every 8 computed on the FMA pipe instead of the MUFU (0..8)
 #endif
 constexpr int kSnapThreads = 576;
 constexpr int kSnapCompute = 512;  // compute threads (warps 0-15)
 constexpr int kSnapTmaWarp = 16, kSnapMmaWarp = 17;
 
-// Share of the exponentials computed on the FMA pipe (ex2_poly2) instead of the MUFU.  Pass 1 handles pairs c, c+1
-// (c even, 32 pairs per 64 columns); pass 2 handles groups of 4 whose first pair may go to the FMA pipe.
-//   QVK_SNAP_POLY 2: 1/4 of pass-1 pairs (c % 8 == 0) and 1/4 of pass-2 elements (e4 even) — the default.
-__host__ __device__ constexpr bool kSnapPolyPass1(int c) {
-    return QVK_SNAP_POLY == 0 ? false : QVK_SNAP_POLY == 4 ? (c & 3) == 0 : (c & 7) == 0;
-}
-__host__ __device__ constexpr bool kSnapPolyPass2(int e4) {
-    return QVK_SNAP_POLY == 0 ? false : QVK_SNAP_POLY == 4 ? true : (e4 & 1) == 0;
-}
+// Exponential pair pi (two adjacent columns) goes to the FMA pipe (ptx::ex2_poly2) for QVK_SNAP_POLY8 of every 8
+// pairs, spread evenly (e.g. 3 -> pairs 0, 3, 6 of each 8).  The MUFU does 16 ex2/clk/SM; the polynomial costs
+// 8 FMA-pipe cycles per element per SM sub-partition, so the pipes balance near 3/8 with the other per-element work.
+__host__ __device__ constexpr bool kSnapPoly(int pi) { return (pi * QVK_SNAP_POLY8) % 8 < QVK_SNAP_POLY8; }
 struct SnapShared {
-    uint64_t q_full, q_empty, acc_full, acc_empty;
+    uint64_t q_full, q_empty, acc_full[2], acc_empty[2];
     uint64_t kv_full[kSnapStages], kv_empty[kSnapStages];
     uint32_t tmem_base;
     alignas(16) float bias[256];  // per window column: m + log2(l) (log2 domain); +inf for invalid rows
@@ -193,11 +190,29 @@ struct SnapShared {
 };
 constexpr size_t kSnapSmem = 1024 + 2 * kSnapQChunk + kSnapStages * kSnapKTile + sizeof(SnapShared);
 
+#ifdef QVK_SNAP_TRACE
+// Developer timeline (tools/snap_trace.cu): clock64 per key tile of CTA 0's first two items.
+//   [item][tile][0] MMA thread starts waiting acc_empty, [1] issues, [2] issued + committed
+//   [3..5] warp 0 (set 0, quarter 0) lane 0: acc_full seen, accumulator released, tile's math done
+//   [6..8] the same for warp 13 (set 3, quarter 1)
+__device__ long long g_snap_trace[2][64][10];
+#define QVK_ST(item_no, tile, slot)                                                       \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && (item_no) < 2 && (tile) < 64)                              \
+            g_snap_trace[(item_no)][(tile)][(slot)] = clock64();                          \
+    } while (0)
+#else
+#define QVK_ST(item_no, tile, slot) \
+    do {                            \
+    } while (0)
+#endif
+
 struct SnapParams {
     const int64_t* tok_off;
     int n_groups, n_kv, gq, window, rows, rows_pad;
     float sl2;
-    float* raw;  // (group, head, token) layout
+    float* raw;   // (group, head, token) layout, when pooling follows
+    double* out;  // pool == 1: the double scores written directly (same value as the pool kernel's float -> double)
 };
 
 __device__ __forceinline__ uint64_t snap_desc(uint32_t chunk_addr, uint32_t chunk_stride, int kk) {
@@ -205,6 +220,8 @@ __device__ __forceinline__ uint64_t snap_desc(uint32_t chunk_addr, uint32_t chun
     return ptx::umma_desc_sw128(chunk_addr + (kk >> 2) * chunk_stride + (kk & 3) * 32, 16, 1024);
 }
 
+// kN8: 8-column chunks of the pass-2 window columns per compute set (rows_pad = 32 kN8).
+template <int kN8>
 __global__ void __launch_bounds__(kSnapThreads, 1)
     snapkv_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const SnapParams p) {
@@ -219,8 +236,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     if (threadIdx.x == 0) {
         ptx::mbar_init(&sh->q_full, 1);
         ptx::mbar_init(&sh->q_empty, 1);
-        ptx::mbar_init(&sh->acc_full, 1);
-        ptx::mbar_init(&sh->acc_empty, kSnapCompute);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&sh->acc_full[b], 1);
+            ptx::mbar_init(&sh->acc_empty[b], kSnapCompute);
+        }
         for (int st = 0; st < kSnapStages; ++st) {
             ptx::mbar_init(&sh->kv_full[st], 1);
             ptx::mbar_init(&sh->kv_empty[st], 1);
@@ -284,27 +303,34 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 for (int pass = 0; pass < 2; ++pass)
                     for (int jt = 0; jt < nt; ++jt, ++tile_no, ++acc_no) {
                         const uint32_t st = tile_no % kSnapStages;
+#ifdef QVK_SNAP_TRACE
+                        const int tr_tile = pass * nt + jt;
+#endif
                         ptx::mbar_wait(&sh->kv_full[st], (tile_no / kSnapStages) & 1);
-                        ptx::mbar_wait(&sh->acc_empty, (acc_no & 1) ^ 1);
+                        QVK_ST(item_no, tr_tile, 0);
+                        const uint32_t ab = acc_no & 1, acol = tmem + 256 * ab;  // accumulator buffer
+                        ptx::mbar_wait(&sh->acc_empty[ab], ((acc_no >> 1) & 1) ^ 1);
+                        QVK_ST(item_no, tr_tile, 1);
                         ptx::tc_fence_after();
                         const uint32_t ka = k_base + st * kSnapKTile;
                         if (pass == 0) {
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk) {
                                 const uint64_t bk = snap_desc(ka, kSnapChunk, kk);
-                                ptx::mma_ss(tmem, snap_desc(q_addr, kSnapQChunk, kk), bk, id1, kk > 0);
-                                ptx::mma_ss(tmem + 128, snap_desc(q_addr + 128 * 128, kSnapQChunk, kk), bk, id1,
+                                ptx::mma_ss(acol, snap_desc(q_addr, kSnapQChunk, kk), bk, id1, kk > 0);
+                                ptx::mma_ss(acol + 128, snap_desc(q_addr + 128 * 128, kSnapQChunk, kk), bk, id1,
                                             kk > 0);
                             }
                         } else {
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk)
-                                ptx::mma_ss(tmem + 256, snap_desc(ka, kSnapChunk, kk),
+                                ptx::mma_ss(acol, snap_desc(ka, kSnapChunk, kk),
                                             snap_desc(q_addr, kSnapQChunk, kk), id2, kk > 0);
                         }
                         ptx::mma_commit(&sh->kv_empty[st]);
-                        ptx::mma_commit(&sh->acc_full);
+                        ptx::mma_commit(&sh->acc_full[ab]);
                         if (pass == 1 && jt == nt - 1) ptx::mma_commit(&sh->q_empty);
+                        QVK_ST(item_no, tr_tile, 2);
                     }
             }
         }
@@ -315,9 +341,28 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = p.sl2;
         uint32_t acc_no = 0;
+#ifdef QVK_SNAP_TRACE
+        const bool tr = (warp == 0 || warp == 13) && lane == 0;
+        const int tr_o = warp == 0 ? 3 : 6;
+        int tr_item = 0;
+#define QVK_STC(tile, k) \
+    do {                 \
+        if (tr) QVK_ST(tr_item, (tile), tr_o + (k)); \
+    } while (0)
+#else
+#define QVK_STC(tile, k) \
+    do {                 \
+    } while (0)
+#endif
         const int mt = set & 1, ch = set >> 1;  // pass 1: M-tile (window rows 128 mt ..) and key-column half
-        const int c_lo = 2 * set;               // pass 2: window columns [64 set, 64 set + 64) = 32-col chunks c_lo, +1
-        const int nch = min(2, max(0, (p.rows - 64 * set + 31) / 32));  // chunks holding window rows
+        // pass 2: window columns [col0, col0 + 8 n8) — rows_pad split evenly over the four sets in 8-column chunks
+        // (224 columns: 56 each; a 64 / 64 / 64 / 32 split left one set idle for a quarter of every tile)
+#ifdef QVK_SNAP_OLDSPLIT
+        const int col0 = 64 * set;
+        const int nch = min(2, max(0, (p.rows - 64 * set + 31) / 32));
+#else
+        const int col0 = set * 8 * kN8;
+#endif
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
             const int g = it / p.n_kv, hk = it - g * p.n_kv;
             const int64_t t0 = __ldg(p.tok_off + g);
@@ -329,15 +374,17 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             // ---- pass 1: running max / sum of window row c_row over key columns [64 ch, 64 ch + 64) of each tile ----
             float m = -INFINITY, l = 0.f;
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
-                ptx::mbar_wait(&sh->acc_full, acc_no & 1);
+                ptx::mbar_wait(&sh->acc_full[acc_no & 1], (acc_no >> 1) & 1);
+                QVK_STC(jt, 0);
                 ptx::tc_fence_after();
                 float x[64];
-                const uint32_t col = tmem + lane_off + mt * 128 + ch * 64;
+                const uint32_t col = tmem + lane_off + 256 * (acc_no & 1) + mt * 128 + ch * 64;
                 QVK_TMEM_LD32F(col + 0, (x + 0));
                 QVK_TMEM_LD32F(col + 32, (x + 32));
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&sh->acc_empty);
+                ptx::mbar_arrive(&sh->acc_empty[acc_no & 1]);
+                QVK_STC(jt, 1);
                 if (my_pos >= 0) {
                     const int j0 = jt * 128 + ch * 64;
                     if (j0 > my_pos) continue;  // every key of this half lies after the row: all masked
@@ -359,7 +406,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                     for (int c = 0; c < 64; c += 2) {
                         float e0, e1;
                         ptx::f2_split(ptx::f2_fma(ptx::f2_make(x[c], x[c + 1]), sl2x2, nmn2), e0, e1);
-                        if (kSnapPolyPass1(c)) {
+                        if (kSnapPoly(c >> 1)) {
                             ptx::ex2_poly2(e0, e1);  // a share of the exponentials on the FMA pipe
                         } else {
                             e0 = ptx::ex2(e0);
@@ -375,6 +422,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                     l = (m == -INFINITY ? 0.f : l * ptx::ex2(m - mn)) + sum;
                     m = mn;
                 }
+#ifdef QVK_SNAP_TRACE
+                if (tr) asm volatile("" ::"f"(l));
+#endif
+                QVK_STC(jt, 2);
             }
             // merge the two key-column halves of every row: half 1 publishes (m, l), half 0 combines
             if (ch == 1) sh->stat[c_row] = make_float2(m, l);
@@ -387,26 +438,37 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 sh->pos[c_row] = my_pos;
             }
             ptx::named_bar_sync(1, kSnapCompute);
-            // ---- pass 2: key j = jt*128 + i, window columns [64 set, 64 set + 64) ----
+            // ---- pass 2: key j = jt*128 + i, window columns [col0, col0 + 8 n8) ----
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
-                ptx::mbar_wait(&sh->acc_full, acc_no & 1);
+                ptx::mbar_wait(&sh->acc_full[acc_no & 1], (acc_no >> 1) & 1);
+                QVK_STC(nt + jt, 0);
                 ptx::tc_fence_after();
                 const int j = jt * 128 + i;
                 const bool edge = jt * 128 + 127 > n - p.window;  // some window rows precede some keys
-                // load this set's two 32-column chunks and release the accumulator BEFORE the exponentials, so the
-                // next key tile's MMAs overlap them.  Columns past the window rows (beyond rows_pad, inside the 512
-                // allocated) have bias +inf: they add exp2(-inf) = 0.
+                // load this set's 8-column chunks and release the accumulator BEFORE the exponentials, so the next key
+                // tile's MMAs overlap them.  Columns past the window rows (up to rows_pad) have bias -inf: they add
+                // exp2(-inf) = 0.
+#ifdef QVK_SNAP_OLDSPLIT
                 float x[64];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) QVK_TMEM_LD32F(tmem + lane_off + 256 + 32 * (c_lo + q), (x + 32 * q));
+                for (int q = 0; q < 2; ++q)
+                    QVK_TMEM_LD32F(tmem + lane_off + 256 * (acc_no & 1) + col0 + 32 * q, (x + 32 * q));
+#else
+                float x[8 * kN8];
+#pragma unroll
+                for (int c8 = 0; c8 < kN8; ++c8)
+                    QVK_TMEM_LD8F(tmem + lane_off + 256 * (acc_no & 1) + col0 + 8 * c8, (x + 8 * c8));
+#endif
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(&sh->acc_empty);
+                ptx::mbar_arrive(&sh->acc_empty[acc_no & 1]);
+                QVK_STC(nt + jt, 1);
                 const ptx::f2 sl2x2 = ptx::f2_make(sl2, sl2);
                 ptx::f2 a01 = ptx::f2_make(0.f, 0.f), a23 = a01;  // (a4[0], a4[1]), (a4[2], a4[3])
                 // y = x * scale - (m + log2 l) of the column's window row, masked where the row precedes the key
                 // (only on `edge` tiles: a warp-uniform branch keeps the compare off the other tiles)
-                auto column4 = [&](const float* xq, const float4 bb, const int* pv, bool masked, bool poly) {
+                auto column4 = [&](const float* xq, const float4 bb, const int* pv, bool masked, bool poly01,
+                                   bool poly23) {
                     float y0, y1, y2, y3;
                     ptx::f2_split(ptx::f2_fma(ptx::f2_make(xq[0], xq[1]), sl2x2, ptx::f2_make(bb.x, bb.y)), y0, y1);
                     ptx::f2_split(ptx::f2_fma(ptx::f2_make(xq[2], xq[3]), sl2x2, ptx::f2_make(bb.z, bb.w)), y2, y3);
@@ -416,46 +478,75 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                         if (j > pv[2]) y2 = -INFINITY;
                         if (j > pv[3]) y3 = -INFINITY;
                     }
-                    if (poly) {  // a quarter of the exponentials on the FMA pipe
+                    if (poly01) {  // a share of the exponentials on the FMA pipe
                         ptx::ex2_poly2(y0, y1);
                     } else {
                         y0 = ptx::ex2(y0);
                         y1 = ptx::ex2(y1);
                     }
-                    y2 = ptx::ex2(y2);
-                    y3 = ptx::ex2(y3);
+                    if (poly23) {
+                        ptx::ex2_poly2(y2, y3);
+                    } else {
+                        y2 = ptx::ex2(y2);
+                        y3 = ptx::ex2(y3);
+                    }
                     a01 = ptx::f2_add(a01, ptx::f2_make(y0, y1));
                     a23 = ptx::f2_add(a23, ptx::f2_make(y2, y3));
                 };
+#ifdef QVK_SNAP_OLDSPLIT
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    if (q >= nch) continue;  // warp-uniform: no window rows in this chunk (exp2(-inf) terms)
-                    const float4* b4 = reinterpret_cast<const float4*>(sh->bias + 32 * (c_lo + q));
-                    const int4* p4 = reinterpret_cast<const int4*>(sh->pos + 32 * (c_lo + q));
+                    if (q >= nch) continue;
+                    const float4* b4 = reinterpret_cast<const float4*>(sh->bias + col0 + 32 * q);
+                    const int4* p4 = reinterpret_cast<const int4*>(sh->pos + col0 + 32 * q);
                     if (edge) {
 #pragma unroll
                         for (int e4 = 0; e4 < 8; ++e4) {
                             const int4 pp = p4[e4];
                             const int pv[4] = {pp.x, pp.y, pp.z, pp.w};
-                            column4(x + 32 * q + 4 * e4, b4[e4], pv, true, kSnapPolyPass2(e4));
+                            column4(x + 32 * q + 4 * e4, b4[e4], pv, true, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
                         }
                     } else {
 #pragma unroll
                         for (int e4 = 0; e4 < 8; ++e4)
-                            column4(x + 32 * q + 4 * e4, b4[e4], nullptr, false, kSnapPolyPass2(e4));
+                            column4(x + 32 * q + 4 * e4, b4[e4], nullptr, false, kSnapPoly(2 * e4),
+                                    kSnapPoly(2 * e4 + 1));
                     }
                 }
+#else
+                const float4* b4 = reinterpret_cast<const float4*>(sh->bias + col0);
+                const int4* p4 = reinterpret_cast<const int4*>(sh->pos + col0);
+                if (edge) {  // one warp-uniform branch around the whole unrolled loop keeps it one basic block
+#pragma unroll
+                    for (int e4 = 0; e4 < 2 * kN8; ++e4) {
+                        const int4 pp = p4[e4];
+                        const int pv[4] = {pp.x, pp.y, pp.z, pp.w};
+                        column4(x + 4 * e4, b4[e4], pv, true, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
+                    }
+                } else {
+#pragma unroll
+                    for (int e4 = 0; e4 < 2 * kN8; ++e4)
+                        column4(x + 4 * e4, b4[e4], nullptr, false, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
+                }
+#endif
                 float a4[4];
                 ptx::f2_split(a01, a4[0], a4[1]);
                 ptx::f2_split(a23, a4[2], a4[3]);
                 const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+                QVK_STC(nt + jt, 2);
                 if (set) sh->part[jt & 1][set - 1][i] = acc;
                 ptx::named_bar_sync(2 + quarter, 128);  // the four sets of this lane quarter
-                if (!set && j < n)
-                    p.raw[p.n_kv * t0 + static_cast<int64_t>(hk) * n + j] =
-                        acc + ((sh->part[jt & 1][0][i] + sh->part[jt & 1][1][i]) + sh->part[jt & 1][2][i]);
+                if (!set && j < n) {
+                    const float tot = acc + ((sh->part[jt & 1][0][i] + sh->part[jt & 1][1][i]) + sh->part[jt & 1][2][i]);
+                    const int64_t e = p.n_kv * t0 + static_cast<int64_t>(hk) * n + j;
+                    if (p.out) p.out[e] = static_cast<double>(tot);
+                    else p.raw[e] = tot;
+                }
             }
             ptx::named_bar_sync(1, kSnapCompute);  // bias / pos / stat reused by the next item
+#ifdef QVK_SNAP_TRACE
+            ++tr_item;
+#endif
         }
     }
     ptx::tc_fence_before();
@@ -478,6 +569,16 @@ bool snap_map(CUtensorMap* m, const void* base, int heads, int64_t tokens, uint3
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int kN8>
+int launch_snap_tc(cudaStream_t stream, const CUtensorMap& mq, const CUtensorMap& mk, const SnapParams& sp,
+                   unsigned grid) {
+    QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(snapkv_tc_kernel<kN8>),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSnapSmem)));
+    snapkv_tc_kernel<kN8><<<grid, kSnapThreads, kSnapSmem, stream>>>(mq, mk, sp);
+    QVK_LAUNCH_CHECK();
+    return QVK_OK;
+}
+
 }  // namespace
 
 int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, int n_q, int n_kv,
@@ -494,18 +595,19 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
     float2* stats = nullptr;
     float* raw = nullptr;
     const int64_t total = g->total_tokens * n_kv;
-    QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
     const int gq = n_q / n_kv;
-    if (gq * window <= 256 && window <= 256 && !env_knob("QVK_SNAPKV_SIMT", 0)) {
+    const bool tc = gq * window <= 256 && window <= 256 && !env_knob("QVK_SNAPKV_SIMT", 0);
+    const bool direct = tc && pool == 1;  // the tcgen05 kernel writes the double scores itself: no pool pass
+    if (!direct) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
+    if (tc) {
         CUtensorMap mq, mk;
         if (!snap_map(&mq, q, n_q, g->total_tokens, static_cast<uint32_t>(gq), static_cast<uint32_t>(window)) ||
             !snap_map(&mk, k, n_kv, g->total_tokens, 1, 128)) {
-            cudaFreeAsync(raw, stream);
+            if (raw) cudaFreeAsync(raw, stream);
             set_error("snapkv: cuTensorMapEncodeTiled failed");
             return QVK_E_CUDA;
         }
-        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(snapkv_tc_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSnapSmem)));
+
         SnapParams sp;
         sp.tok_off = g->tok_off_d;
         sp.n_groups = g->n_groups;
@@ -516,10 +618,25 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         sp.rows_pad = (sp.rows + 31) / 32 * 32;
         sp.sl2 = sl2;
         sp.raw = raw;
+        sp.out = direct ? scores : nullptr;
         const int sms = sm_count();
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(static_cast<int64_t>(g->n_groups) * n_kv, sms));
-        snapkv_tc_kernel<<<grid, kSnapThreads, kSnapSmem, stream>>>(mq, mk, sp);
-        QVK_LAUNCH_CHECK();
+        int rc = QVK_OK;
+        switch (sp.rows_pad / 32) {
+            case 1: rc = launch_snap_tc<1>(stream, mq, mk, sp, grid); break;
+            case 2: rc = launch_snap_tc<2>(stream, mq, mk, sp, grid); break;
+            case 3: rc = launch_snap_tc<3>(stream, mq, mk, sp, grid); break;
+            case 4: rc = launch_snap_tc<4>(stream, mq, mk, sp, grid); break;
+            case 5: rc = launch_snap_tc<5>(stream, mq, mk, sp, grid); break;
+            case 6: rc = launch_snap_tc<6>(stream, mq, mk, sp, grid); break;
+            case 7: rc = launch_snap_tc<7>(stream, mq, mk, sp, grid); break;
+            default: rc = launch_snap_tc<8>(stream, mq, mk, sp, grid); break;
+        }
+        if (rc != QVK_OK) {
+            if (raw) cudaFreeAsync(raw, stream);
+            return rc;
+        }
+        if (direct) return QVK_OK;
     } else {
     QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&stats),
                                    sizeof(float2) * g->n_groups * n_q * static_cast<size_t>(window), stream));

@@ -7,8 +7,11 @@ NAME=${1:?name}; SRC=${2:?source}; DEFS=${3:-}
 OUT=build/ab/$NAME; mkdir -p "$OUT"
 stem=$(basename "${SRC%.cu}")
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude \
-     -Ipaper_2505_16175_b200/csrc $DEFS -c "$SRC" -o "$OUT/$stem.o"
+     -Ipaper_2505_16175_b200/csrc -I"$(python -c "import paper_2505_16175_b200.build as b; print(b.NCCL)")/include" \
+     $DEFS -c "$SRC" -o "$OUT/$stem.o"
 objs=()
 for o in build/obj/*.o; do [[ $(basename "$o") == "$stem.o" ]] && objs+=("$OUT/$stem.o") || objs+=("$o"); done
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libqvk.so" "${objs[@]}" -lcudart
+NCCL=$(python -c "import paper_2505_16175_b200.build as b; print(b.NCCL)")
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libqvk.so" "${objs[@]}" -lcudart -L"$NCCL/lib" \
+     -l:libnccl.so.2 -Xlinker=-rpath="$NCCL/lib"
 echo "$OUT/libqvk.so"
