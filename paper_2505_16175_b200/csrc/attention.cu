@@ -77,12 +77,15 @@ __device__ long long g_attn_trace[1024];
 #ifdef QVK_ATTN_UNITLOG
 // Debug per-unit log (tools/attn_unitlog.cu): the MMA thread of every CTA stamps clock64 at the top of each of its
 // first 128 valid units (and once after the last), with the unit's K/V step count.
-__device__ long long g_attn_unitlog[1024][129][2];
+__device__ long long g_attn_unitlog[1024][129][3];
 #define QVK_ULOG(i, nkv)                                                                  \
     do {                                                                                  \
         if (blockIdx.x < 1024 && (i) < 129) {                                             \
+            long long _g;                                                                 \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g));                        \
             g_attn_unitlog[blockIdx.x][(i)][0] = clock64();                               \
             g_attn_unitlog[blockIdx.x][(i)][1] = (nkv);                                   \
+            g_attn_unitlog[blockIdx.x][(i)][2] = _g;                                      \
         }                                                                                 \
     } while (0)
 #else

@@ -198,8 +198,14 @@ constexpr size_t kSnapSmem = 1024 + 2 * kSnapQChunk + kSnapStages * kSnapKTile +
 __device__ long long g_snap_trace[2][64][10];
 #define QVK_ST(item_no, tile, slot)                                                       \
     do {                                                                                  \
-        if (blockIdx.x == 0 && (item_no) < 2 && (tile) < 64)                              \
+        if (blockIdx.x == 0 && (item_no) < 2 && (tile) < 64) {                            \
             g_snap_trace[(item_no)][(tile)][(slot)] = clock64();                          \
+            if ((slot) == 0) {                                                            \
+                long long _g;                                                             \
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g));                    \
+                g_snap_trace[(item_no)][(tile)][9] = _g;                                  \
+            }                                                                             \
+        }                                                                                 \
     } while (0)
 #else
 #define QVK_ST(item_no, tile, slot) \
@@ -226,7 +232,9 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     snapkv_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const SnapParams p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-aligned window (SWIZZLE_128B atoms) by offsetting the shared array itself: the compiler keeps the shared
+    // address space (LDS / STS, not generic LD / ST as through a uintptr_t round trip).
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sQ = smem;
     uint8_t* sK = smem + 2 * kSnapQChunk;
     SnapShared* sh = reinterpret_cast<SnapShared*>(sK + kSnapStages * kSnapKTile);
@@ -341,6 +349,15 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
         const float sl2 = p.sl2;
         uint32_t acc_no = 0;
+        // acc_full of accumulator acc_no + 1 is probed (non-blocking) halfway through the math of acc_no: the MMA has
+        // usually finished by then, and the blocking try_wait at the next tile then costs a memory round trip (~300
+        // cycles per tile, all four warps of a sub-partition at once; tools/snap_trace.cu) instead of nothing.
+        bool ready = false;
+        auto wait_acc = [&]() {
+            if (!ready) ptx::mbar_wait(&sh->acc_full[acc_no & 1], (acc_no >> 1) & 1);
+            ready = false;
+        };
+        auto probe_next = [&]() { ready = ptx::mbar_test(&sh->acc_full[(acc_no + 1) & 1], ((acc_no + 1) >> 1) & 1); };
 #ifdef QVK_SNAP_TRACE
         const bool tr = (warp == 0 || warp == 13) && lane == 0;
         const int tr_o = warp == 0 ? 3 : 6;
@@ -374,7 +391,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             // ---- pass 1: running max / sum of window row c_row over key columns [64 ch, 64 ch + 64) of each tile ----
             float m = -INFINITY, l = 0.f;
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
-                ptx::mbar_wait(&sh->acc_full[acc_no & 1], (acc_no >> 1) & 1);
+                wait_acc();
                 QVK_STC(jt, 0);
                 ptx::tc_fence_after();
                 float x[64];
@@ -404,6 +421,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                     ptx::f2 sa = ptx::f2_make(0.f, 0.f), sb = sa;  // (s4[0], s4[1]), (s4[2], s4[3])
 #pragma unroll
                     for (int c = 0; c < 64; c += 2) {
+                        if (c == 32) probe_next();
                         float e0, e1;
                         ptx::f2_split(ptx::f2_fma(ptx::f2_make(x[c], x[c + 1]), sl2x2, nmn2), e0, e1);
                         if (kSnapPoly(c >> 1)) {
@@ -440,7 +458,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             ptx::named_bar_sync(1, kSnapCompute);
             // ---- pass 2: key j = jt*128 + i, window columns [col0, col0 + 8 n8) ----
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
-                ptx::mbar_wait(&sh->acc_full[acc_no & 1], (acc_no >> 1) & 1);
+                wait_acc();
                 QVK_STC(nt + jt, 0);
                 ptx::tc_fence_after();
                 const int j = jt * 128 + i;
@@ -519,14 +537,17 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 if (edge) {  // one warp-uniform branch around the whole unrolled loop keeps it one basic block
 #pragma unroll
                     for (int e4 = 0; e4 < 2 * kN8; ++e4) {
+                        if (e4 == kN8) probe_next();
                         const int4 pp = p4[e4];
                         const int pv[4] = {pp.x, pp.y, pp.z, pp.w};
                         column4(x + 4 * e4, b4[e4], pv, true, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
                     }
                 } else {
 #pragma unroll
-                    for (int e4 = 0; e4 < 2 * kN8; ++e4)
+                    for (int e4 = 0; e4 < 2 * kN8; ++e4) {
+                        if (e4 == kN8) probe_next();
                         column4(x + 4 * e4, b4[e4], nullptr, false, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
+                    }
                 }
 #endif
                 float a4[4];

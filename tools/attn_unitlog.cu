@@ -67,7 +67,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     for (int it = 0; it < 3; ++it) qvk::launch_attention(0, &grp, q, k, v, nq, nkv, d, 0.0883883f, o);
-    static long long zero[1024][129][2];
+    static long long zero[1024][129][3];
     cudaMemcpyToSymbol(qvk::g_attn_unitlog, zero, sizeof(zero));
     cudaEventRecord(e0);
     int rc = qvk::launch_attention(0, &grp, q, k, v, nq, nkv, d, 0.0883883f, o);
@@ -76,11 +76,11 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double tf = G * 4.0 * d * nq * (double)N * (N + 1) / 2 / (ms * 1e-3) / 1e12;
-    static long long lg[1024][129][2];
+    static long long lg[1024][129][3];
     cudaMemcpyFromSymbol(lg, qvk::g_attn_unitlog, sizeof(lg));
     int sms = qvk::sm_count();
     std::map<long long, std::pair<double, long long>> by;  // nkv -> (sum cycles, count)
-    double sx = 0, sy = 0, sxx = 0, sxy = 0, n = 0, tot = 0, first = 1e30, last = 0;
+    double sx = 0, sy = 0, sxx = 0, sxy = 0, n = 0, tot = 0, first = 1e30, last = 0, cyc = 0, ns = 0;
     long long steps = 0;
     for (int c = 0; c < sms; ++c) {
         int i = 0;
@@ -98,6 +98,8 @@ int main(int argc, char** argv) {
         }
         if (i > 0) {
             tot += double(lg[c][i][0] - lg[c][0][0]);
+            cyc += double(lg[c][i][0] - lg[c][0][0]);
+            ns += double(lg[c][i][2] - lg[c][0][2]);
             first = std::min(first, double(lg[c][0][0]));
             last = std::max(last, double(lg[c][i][0]));
         }
@@ -105,6 +107,7 @@ int main(int argc, char** argv) {
     const double a = (n * sxy - sx * sy) / (n * sxx - sx * sx), b = (sy - a * sx) / n;
     printf("G=%d N=%d rc=%d err=%s  %.3f ms  %.1f TFLOP/s  units logged %.0f  mean CTA loop %.0f cycles\n", G, N, rc,
            cudaGetErrorString(err), ms, tf, n, tot / sms);
+    printf("SM clock over the logged spans: %.0f MHz\n", ns > 0 ? cyc / ns * 1e3 : 0.0);
     printf("fit: cycles per unit = %.1f * nkv + %.1f   (mean K/V steps per unit %.2f)\n", a, b, sx / n);
     printf(" nkv  units  mean cycles  cycles/step\n");
     for (auto& kv : by)

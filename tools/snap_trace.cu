@@ -77,6 +77,13 @@ int main(int argc, char** argv) {
     cudaMemcpyFromSymbol(tr, qvk::g_snap_trace, sizeof(tr));
     const long long t0 = tr[0][0][0];
     const int nt = (N + 127) / 128;
+    {  // effective SM clock over CTA 0's traced span: clock64 cycles / globaltimer ns
+        long long c0 = tr[0][0][0], g0 = tr[0][0][9], c1 = 0, g1 = 0;
+        for (int it = 0; it < 2; ++it)
+            for (int t = 0; t < 64; ++t)
+                if (tr[it][t][0] && tr[it][t][9]) c1 = tr[it][t][0], g1 = tr[it][t][9];
+        if (g1 > g0) printf("SM clock over the traced span: %.0f MHz\n", double(c1 - c0) / double(g1 - g0) * 1e3);
+    }
     printf("item tile | MMA: wait  issue  done || w0: full  rel  math || w13: full  rel  math   (cycles from item 0 tile 0)\n");
     for (int it = 0; it < 2; ++it)
         for (int t = 0; t < 2 * nt && t < 64; ++t) {
