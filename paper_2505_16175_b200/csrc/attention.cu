@@ -203,7 +203,8 @@ __device__ __forceinline__ Unit decode_unit(const AttnParams& p, int u) {
 template <int D, int kPolyPairs>
 __global__ void __launch_bounds__(kThreads, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                         const AttnParams p) {
     constexpr uint32_t kTileBytes = tile_bytes<D>();
     // 228 KB of tiles + barriers leave no room for alignment slack: the dynamic window must be 1024-aligned
     // (SWIZZLE_128B atoms); checked below.
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int b = 0; b < kQBufs; ++b) {
             ptx::mbar_init(&bar->q_full[b], 1);
-            ptx::mbar_init(&bar->q_empty[b], 1);
+            ptx::mbar_init(&bar->q_empty[b], 2);  // the unit's last S MMA retired + its O stores have left the buffer
         }
         for (int s = 0; s < kStages; ++s) {
             ptx::mbar_init(&bar->kv_full[s], 1);
@@ -260,10 +261,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (decode_unit(p, u).valid) return u;
                 return p.total_units;
             };
-            auto load_q = [&](const Unit& w, int qi) {
+            // Q of unit qi goes to buffer qi & 1 once q_empty says its previous user (unit qi - 2) is done with it.
+            // block = false: only if that is already the case (the buffer is also the previous unit's O staging
+            // area, released by the epilogue — not worth stalling the K/V stream for).
+            auto load_q = [&](const Unit& w, int qi, bool block) -> bool {
                 const int qb = qi & 1;
                 uint8_t* q_dst = sQ + qb * 2 * kTileBytes;
-                ptx::mbar_wait(&bar->q_empty[qb], ((qi >> 1) & 1) ^ 1);
+                const uint32_t ph = ((qi >> 1) & 1) ^ 1;
+                if (!block && !ptx::mbar_test(&bar->q_empty[qb], ph)) return false;
+                ptx::mbar_wait(&bar->q_empty[qb], ph);
                 ptx::mbar_arrive_expect_tx(&bar->q_full[qb], w.n1 ? 2 * kTileBytes : kTileBytes);
                 const int r0 = static_cast<int>(w.tok0) + w.mt0 * kBM;
                 const int r1 = static_cast<int>(w.tok0) + w.mt1 * kBM;
@@ -274,14 +280,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tma_load_3d(q_dst + kTileBytes + c * kChunkBytes, &tm_q, &bar->q_full[qb], 64 * c, w.hq1,
                                          r1);
                 }
+                return true;
             };
             uint32_t item = 0;
             int u = next_valid(blockIdx.x);
-            if (u < p.total_units) load_q(decode_unit(p, u), 0);
+            if (u < p.total_units) load_q(decode_unit(p, u), 0, true);
             for (; u < p.total_units; ++unit_iter) {
                 const Unit w = decode_unit(p, u);
                 const int un = next_valid(u + gridDim.x);
-                const int q_at = min(2, 2 * w.nkv - 1);  // K/V item after which the next unit's Q is issued
+                const int q_at = min(2, 2 * w.nkv - 1);  // K/V item from which the next unit's Q may be issued
+                bool q_pending = un < p.total_units;
                 for (int it = 0; it < 2 * w.nkv; ++it, ++item) {
                     const uint32_t st = item % kStages;
                     ptx::mbar_wait(&bar->kv_empty[st], ((item / kStages) & 1) ^ 1);
@@ -292,7 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int c = 0; c < D / 64; ++c)
                         ptx::tma_load_3d(dst + c * kChunkBytes, map, &bar->kv_full[st], 64 * c, w.hk, row);
-                    if (it == q_at && un < p.total_units) load_q(decode_unit(p, un), unit_iter + 1);
+                    // non-blocking from q_at on, blocking at the unit's last item (the next unit needs its Q)
+                    if (q_pending && it >= q_at)
+                        q_pending = !load_q(decode_unit(p, un), unit_iter + 1, it == 2 * w.nkv - 1);
                 }
                 u = un;
             }
@@ -424,13 +434,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= kEpiWarp0) {
         ptx::setmaxnreg_dec<kRegsEpilogue>();
         // ===================== epilogue: O / l -> bf16 -> HBM =====================
+        // Full 128-row tiles are staged (bf16, SWIZZLE_128B) in the unit's own Q tile buffer — dead once the tile's
+        // last S MMA retired, which o_done implies — and written by TMA stores: one thread per row storing its own
+        // 256-byte row touched 32 lines per warp instruction and held the LSU for ~2000 cycles per tile, right at the
+        // unit boundary where the MMA thread's loads / barrier waits queue behind it (per-unit overhead 3230 -> 1960
+        // cycles with the stores removed, tools/attn_unitlog.cu).  Rows past the group's end (its last, partial
+        // tile) would overwrite the next group: that tile is stored row by row.  The buffer is handed back to the
+        // producer (q_empty, 2nd arrival) once the TMA engine has read it.
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        const bool leader = warp == kEpiWarp0 && lane == 0;
+        if (leader) ptx::prefetch_tmap(&tm_o);
         uint32_t t_units[2] = {0, 0};
         for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
             const Unit w = decode_unit(p, u);
             if (!w.valid) continue;
+            const int qb = unit_iter & 1;
             for (int t = 0; t < 2; ++t) {
                 if (t == 1 && !w.n1) continue;
                 const uint32_t ph = t_units[t] & 1;
@@ -440,8 +460,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 QVK_SWAIT_T(256, 7, &bar->o_done[t], ph);
                 ptx::tc_fence_after();
                 const uint32_t o_col = tmem + lane_off + 256 + t * 128;
-                const int qrow = (t ? w.mt1 : w.mt0) * kBM + row;
+                const int mt = t ? w.mt1 : w.mt0;
+                const int qrow = mt * kBM + row;
                 __nv_bfloat16* dst = p.o + ((w.tok0 + qrow) * p.n_q + (t ? w.hq1 : w.hq0)) * static_cast<int64_t>(D);
+                const bool staged = (mt + 1) * kBM <= w.n;  // warp-uniform (whole tile inside the group)
+                uint8_t* stage = sQ + qb * 2 * kTileBytes + t * kTileBytes;
 #pragma unroll
                 for (int c = 0; c < D / 16; ++c) {
                     uint32_t o[16];
@@ -455,16 +478,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
                         pk[e] = ptx::pack_bf16(__uint_as_float(o[2 * e]) * inv, __uint_as_float(o[2 * e + 1]) * inv);
-                    if (qrow < w.n) {
+                    if (staged) {
+                        // columns 16c..16c+15 = 16-byte units 2(c%4), 2(c%4)+1 of row `row` in d-chunk c/4, XOR-swizzled
+                        const uint32_t base = ptx::smem_u32(stage) + (c >> 2) * kChunkBytes + row * 128;
+                        const uint32_t u0 = static_cast<uint32_t>(2 * (c & 3));
+                        ptx::sts128(base + ((u0 ^ (row & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+                        ptx::sts128(base + (((u0 + 1) ^ (row & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
+                    } else if (qrow < w.n) {
                         uint4* d4 = reinterpret_cast<uint4*>(dst + c * 16);
                         d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                         d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
                     }
                 }
+                if (staged) {
+                    ptx::fence_proxy_async_smem();  // generic st.shared -> the TMA engine (async proxy)
+                    ptx::named_bar_sync(1, 128);    // the four epilogue warps' rows are all in the stage
+                    if (leader) {
+#pragma unroll
+                        for (int ch = 0; ch < D / 64; ++ch)
+                            ptx::tma_store_3d(&tm_o, stage + ch * kChunkBytes, 64 * ch, t ? w.hq1 : w.hq0,
+                                              static_cast<int>(w.tok0) + mt * kBM);
+                        ptx::bulk_commit_group();
+                    }
+                }
                 ++t_units[t];
+            }
+            if (leader) {  // the stores of this unit have read the buffer: the producer may load Q into it again
+                ptx::bulk_wait_group_read<0>();
+                ptx::mbar_arrive(&bar->q_empty[qb]);
             }
             ++unit_iter;
         }
+        if (leader) ptx::bulk_wait_group<0>();  // every O store complete before the CTA retires
     } else {
         ptx::setmaxnreg_inc<kRegsSoftmax>();
         // ===================== softmax (+ lazy O correction) =====================
@@ -618,10 +663,10 @@ bool make_map(CUtensorMap* m, const void* base, int heads, int64_t tokens, int k
 
 template <int D, int kPoly>
 int launch_attention_d(cudaStream_t stream, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                       const AttnParams& prm, unsigned grid) {
+                       const CUtensorMap& mo, const AttnParams& prm, unsigned grid) {
     QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(attention_fwd_kernel<D, kPoly>),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes<D>())));
-    attention_fwd_kernel<D, kPoly><<<grid, kThreads, smem_bytes<D>(), stream>>>(mq, mk, mv, prm);
+    attention_fwd_kernel<D, kPoly><<<grid, kThreads, smem_bytes<D>(), stream>>>(mq, mk, mv, mo, prm);
     QVK_LAUNCH_CHECK();
     return QVK_OK;
 }
@@ -644,9 +689,9 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     if (g->total_tokens > 0x7fffffff) QVK_INVALID("attention: more than 2^31 token rows");
     if (d_h == 128 && env_knob("QVK_ATTN_2CTA", 0))  // CTA-pair variant (attention2.cu), opt-in while evaluated
         return launch_attention2(stream, g, q, k, v, n_q, n_kv, scale, o);
-    CUtensorMap mq, mk, mv;
+    CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, q, n_q, g->total_tokens, d_h) || !make_map(&mk, k, n_kv, g->total_tokens, d_h) ||
-        !make_map(&mv, v, n_kv, g->total_tokens, d_h)) {
+        !make_map(&mv, v, n_kv, g->total_tokens, d_h) || !make_map(&mo, o, n_q, g->total_tokens, d_h)) {
         set_error("attention: cuTensorMapEncodeTiled failed");
         return QVK_E_CUDA;
     }
@@ -675,14 +720,14 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     }();
     if (d_h == 128) {
         switch (poly) {
-            case 0: return launch_attention_d<128, 0>(stream, mq, mk, mv, prm, grid);
-            case 2: return launch_attention_d<128, 2>(stream, mq, mk, mv, prm, grid);
-            case 6: return launch_attention_d<128, 6>(stream, mq, mk, mv, prm, grid);
-            default: return launch_attention_d<128, 4>(stream, mq, mk, mv, prm, grid);
+            case 0: return launch_attention_d<128, 0>(stream, mq, mk, mv, mo, prm, grid);
+            case 2: return launch_attention_d<128, 2>(stream, mq, mk, mv, mo, prm, grid);
+            case 6: return launch_attention_d<128, 6>(stream, mq, mk, mv, mo, prm, grid);
+            default: return launch_attention_d<128, 4>(stream, mq, mk, mv, mo, prm, grid);
         }
     }
-    return poly ? launch_attention_d<64, 4>(stream, mq, mk, mv, prm, grid)
-                : launch_attention_d<64, 0>(stream, mq, mk, mv, prm, grid);
+    return poly ? launch_attention_d<64, 4>(stream, mq, mk, mv, mo, prm, grid)
+                : launch_attention_d<64, 0>(stream, mq, mk, mv, mo, prm, grid);
 }
 
 }  // namespace qvk
