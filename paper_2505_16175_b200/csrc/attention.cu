@@ -333,16 +333,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mma_ss(tmem + t * 128, desc_plus(dq, kmajor_off(kk)), desc_plus(dk, kmajor_off(kk)), kIdS,
                                 kk > 0);
             };
-            for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+            // The next valid unit is decoded one unit ahead (two L2 loads + four integer divisions, ~1200 cycles of
+            // this single thread, tools/attn_trace.cu), and a pre-issued unit skips its Q / K(0) waits (already
+            // satisfied at the pre-issue): the unit boundary is on the tensor pipe's critical path.
+            auto next_valid = [&](int u) -> int {
+                for (; u < p.total_units; u += gridDim.x)
+                    if (decode_unit(p, u).valid) return u;
+                return p.total_units;
+            };
+            int u = next_valid(blockIdx.x);
+            Unit w = decode_unit(p, u);
+            while (u < p.total_units) {
                 QVK_TRACE(39);  // unit loop top
-                const Unit w = decode_unit(p, u);
-                if (!w.valid) continue;
                 QVK_ULOG(unit_iter, w.nkv);
                 QVK_TRACE(23);  // decoded
                 const int nt[2] = {w.n0, w.n1};
                 const int qb = unit_iter & 1;
                 const uint32_t q_addr = q_base + qb * 2 * kTileBytes;
-                QVK_SWAIT(0, &bar->q_full[qb], (unit_iter >> 1) & 1);
+                if (!s0_pre) QVK_SWAIT(0, &bar->q_full[qb], (unit_iter >> 1) & 1);
                 QVK_TRACE(31);  // Q ready
                 ptx::tc_fence_after();
                 auto issue_s = [&](int t, uint32_t k_addr) { issue_s_at(t, q_addr + t * kTileBytes, k_addr); };
@@ -366,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ++o_units[t];
                     }
                 };
-                const uint32_t k0 = wait_item(item);
+                const uint32_t k0 = s0_pre ? ring + (item % kStages) * kTileBytes : wait_item(item);
                 QVK_TRACE(15);  // K(0) ready
                 if (!s0_pre) {
                     issue_s(0, k0);
@@ -380,6 +388,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (w.nkv == 1) ptx::mma_commit(&bar->q_empty[qb]);  // every S of the unit issued
                 ptx::mma_commit(&bar->kv_empty[item % kStages]);
                 bool next_pre = false;
+                const int un = next_valid(u + gridDim.x);  // off the critical path: S0(0) / S1(0) are queued
+                const Unit wn = decode_unit(p, un);
                 for (int j = 0; j < w.nkv; ++j) {
                     const uint32_t v_item = item + 2 * j + 1;
                     const uint32_t v_addr = wait_item(v_item);
@@ -407,8 +417,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // above), so the next unit's tile-0 softmax overlaps this unit's tail.  K(0) of the next unit
                     // is the ring item after this unit's last V; the two slots released above let it load.
                     if (p.pre_issue && j + 2 == w.nkv && w.n1 == w.n0 + 1) {
-                        int un = u + gridDim.x;
-                        while (un < p.total_units && !decode_unit(p, un).valid) un += gridDim.x;
                         if (un < p.total_units) {
                             const int qbn = (unit_iter + 1) & 1;
                             QVK_SWAIT(0, &bar->q_full[qbn], ((unit_iter + 1) >> 1) & 1);
@@ -425,6 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ++unit_iter;
                 s0_pre = next_pre;
                 QVK_STALL_ADD(5, 1);
+                u = un;
+                w = wn;
             }
             QVK_ULOG(unit_iter, 0);
 #ifdef QVK_ATTN_STALLS
