@@ -148,8 +148,10 @@ __global__ void snap_pool_kernel(const float* __restrict__ raw, const int64_t* _
 }
 
 // ---------------------------------------------------------------------------------------------------------------
-// tcgen05 path (d_h = 128, gq * W <= 256 with gq = n_q / n_kv): the 224 window query rows of a KV head (gq heads x
-// W rows) are one smem operand; both passes run on the tensor pipe and the exponentials on the CUDA cores.
+// tcgen05 path (d_h = 128, gq = n_q / n_kv <= 256): the gq * W window query rows of a KV head (gq heads x W rows,
+// 224 at the default W = 32, GQA 7) are one smem operand of <= 256 rows; larger windows are cut into nb blocks of
+// wb window rows (gq * wb <= 256) that the item's CTA runs one after another, each block's per-key sums added to
+// the earlier blocks'.  Both passes run on the tensor pipe and the exponentials on the CUDA cores.
 //   pass 1  S  = Q_obs K_t^T  (M = 128 window rows per MMA, two M-tiles; N = 128 keys): row max / sum, online over
 //           key tiles — thread-local (thread = TMEM lane = window row);
 //   pass 2  S' = K_t Q_obs^T  (M = 128 keys, N = ceil32(gq W) window rows): per-key sum of the normalised
@@ -216,6 +218,7 @@ __device__ long long g_snap_trace[2][64][10];
 struct SnapParams {
     const int64_t* tok_off;
     int n_groups, n_kv, gq, window, rows, rows_pad;
+    int wb, nb;  // window rows per block (rows = gq * wb <= 256) and blocks per item (nb * wb >= window)
     float sl2;
     float* raw;   // (group, head, token) layout, when pooling follows
     double* out;  // pool == 1: the double scores written directly (same value as the pool kernel's float -> double)
@@ -274,14 +277,16 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     if (warp == kSnapTmaWarp) {
         if (ptx::elect_one()) {  // ===== TMA producer =====
             uint32_t item_no = 0, tile_no = 0;
-            for (int it = blockIdx.x; it < items; it += gridDim.x, ++item_no) {
+            for (int it = blockIdx.x; it < items; it += gridDim.x)
+              for (int b = 0; b < p.nb; ++b, ++item_no) {
                 const int g = it / p.n_kv, hk = it - g * p.n_kv;
                 const int64_t t0 = __ldg(p.tok_off + g);
                 const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - t0);
                 const int nt = (n + 127) / 128;
                 ptx::mbar_wait(&sh->q_empty, (item_no & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(&sh->q_full, 2 * p.rows * 128);
-                const int w0 = static_cast<int>(t0) + n - p.window;  // may start before the group: rows masked
+                // window rows [b wb, b wb + wb): may start before the group or run past its end (rows masked)
+                const int w0 = static_cast<int>(t0) + n - p.window + b * p.wb;
                 ptx::tma_load_3d(sQ, &tm_q, &sh->q_full, 0, hk * p.gq, w0);
                 ptx::tma_load_3d(sQ + kSnapQChunk, &tm_q, &sh->q_full, 64, hk * p.gq, w0);
                 for (int pass = 0; pass < 2; ++pass)
@@ -302,7 +307,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             const uint32_t id2 = ptx::idesc_bf16_f32(128, p.rows_pad, false, false);
             const uint32_t q_addr = ptx::smem_u32(sQ), k_base = ptx::smem_u32(sK);
             uint32_t item_no = 0, tile_no = 0, acc_no = 0;
-            for (int it = blockIdx.x; it < items; it += gridDim.x, ++item_no) {
+            for (int it = blockIdx.x; it < items; it += gridDim.x)
+              for (int b = 0; b < p.nb; ++b, ++item_no) {
                 const int g = it / p.n_kv;
                 const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - __ldg(p.tok_off + g));
                 const int nt = (n + 127) / 128;
@@ -374,20 +380,31 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         const int mt = set & 1, ch = set >> 1;  // pass 1: M-tile (window rows 128 mt ..) and key-column half
         // pass 2: window columns [col0, col0 + 8 n8) — rows_pad split evenly over the four sets in 8-column chunks
         // (224 columns: 56 each; a 64 / 64 / 64 / 32 split left one set idle for a quarter of every tile)
-#ifdef QVK_SNAP_OLDSPLIT
-        const int col0 = 64 * set;
-        const int nch = min(2, max(0, (p.rows - 64 * set + 31) / 32));
-#else
         const int col0 = set * 8 * kN8;
-#endif
+        // The next item's group bounds are loaded one item ahead: two dependent-free L2 loads at the item boundary
+        // held all 16 compute warps ~1400 cycles (tools/snap_trace.cu).
+        int64_t nx_t0 = 0, nx_t1 = 0;
+        if (blockIdx.x < items) {
+            nx_t0 = __ldg(p.tok_off + blockIdx.x / p.n_kv);
+            nx_t1 = __ldg(p.tok_off + blockIdx.x / p.n_kv + 1);
+        }
         for (int it = blockIdx.x; it < items; it += gridDim.x) {
+          const int64_t t0 = nx_t0;
+          const int n = static_cast<int>(nx_t1 - nx_t0);
+          if (it + static_cast<int>(gridDim.x) < items) {
+              const int gn = (it + gridDim.x) / p.n_kv;
+              nx_t0 = __ldg(p.tok_off + gn);
+              nx_t1 = __ldg(p.tok_off + gn + 1);
+          }
+          for (int b = 0; b < p.nb; ++b) {
             const int g = it / p.n_kv, hk = it - g * p.n_kv;
-            const int64_t t0 = __ldg(p.tok_off + g);
-            const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - t0);
+            (void)g;
             const int nt = (n + 127) / 128;
-            // window column c = r * gq + h -> query token position n - W + r (invalid when < 0)
+            // window column c = r * gq + h of block b -> window row b wb + r at token position n - W + b wb + r
+            // (invalid when before the group or past the window)
             const int c_row = mt * 128 + i;
-            const int my_pos = c_row < p.rows ? n - p.window + c_row / p.gq : -1;
+            const int wrow = b * p.wb + c_row / p.gq;
+            const int my_pos = c_row < p.rows && wrow < p.window ? n - p.window + wrow : -1;
             // ---- pass 1: running max / sum of window row c_row over key columns [64 ch, 64 ch + 64) of each tile ----
             float m = -INFINITY, l = 0.f;
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
@@ -462,21 +479,14 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 QVK_STC(nt + jt, 0);
                 ptx::tc_fence_after();
                 const int j = jt * 128 + i;
-                const bool edge = jt * 128 + 127 > n - p.window;  // some window rows precede some keys
+                const bool edge = jt * 128 + 127 > n - p.window + b * p.wb;  // some window rows precede some keys
                 // load this set's 8-column chunks and release the accumulator BEFORE the exponentials, so the next key
                 // tile's MMAs overlap them.  Columns past the window rows (up to rows_pad) have bias -inf: they add
                 // exp2(-inf) = 0.
-#ifdef QVK_SNAP_OLDSPLIT
-                float x[64];
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    QVK_TMEM_LD32F(tmem + lane_off + 256 * (acc_no & 1) + col0 + 32 * q, (x + 32 * q));
-#else
                 float x[8 * kN8];
 #pragma unroll
                 for (int c8 = 0; c8 < kN8; ++c8)
                     QVK_TMEM_LD8F(tmem + lane_off + 256 * (acc_no & 1) + col0 + 8 * c8, (x + 8 * c8));
-#endif
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&sh->acc_empty[acc_no & 1]);
@@ -511,27 +521,6 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                     a01 = ptx::f2_add(a01, ptx::f2_make(y0, y1));
                     a23 = ptx::f2_add(a23, ptx::f2_make(y2, y3));
                 };
-#ifdef QVK_SNAP_OLDSPLIT
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    if (q >= nch) continue;
-                    const float4* b4 = reinterpret_cast<const float4*>(sh->bias + col0 + 32 * q);
-                    const int4* p4 = reinterpret_cast<const int4*>(sh->pos + col0 + 32 * q);
-                    if (edge) {
-#pragma unroll
-                        for (int e4 = 0; e4 < 8; ++e4) {
-                            const int4 pp = p4[e4];
-                            const int pv[4] = {pp.x, pp.y, pp.z, pp.w};
-                            column4(x + 32 * q + 4 * e4, b4[e4], pv, true, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
-                        }
-                    } else {
-#pragma unroll
-                        for (int e4 = 0; e4 < 8; ++e4)
-                            column4(x + 32 * q + 4 * e4, b4[e4], nullptr, false, kSnapPoly(2 * e4),
-                                    kSnapPoly(2 * e4 + 1));
-                    }
-                }
-#else
                 const float4* b4 = reinterpret_cast<const float4*>(sh->bias + col0);
                 const int4* p4 = reinterpret_cast<const int4*>(sh->pos + col0);
                 if (edge) {  // one warp-uniform branch around the whole unrolled loop keeps it one basic block
@@ -549,7 +538,6 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                         column4(x + 4 * e4, b4[e4], nullptr, false, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
                     }
                 }
-#endif
                 float a4[4];
                 ptx::f2_split(a01, a4[0], a4[1]);
                 ptx::f2_split(a23, a4[2], a4[3]);
@@ -560,14 +548,18 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 if (!set && j < n) {
                     const float tot = acc + ((sh->part[jt & 1][0][i] + sh->part[jt & 1][1][i]) + sh->part[jt & 1][2][i]);
                     const int64_t e = p.n_kv * t0 + static_cast<int64_t>(hk) * n + j;
-                    if (p.out) p.out[e] = static_cast<double>(tot);
-                    else p.raw[e] = tot;
+                    // blocks after the first add to the earlier blocks' sum (same thread, program order; a
+                    // double written from a float converts back exactly)
+                    const float t = b ? tot + (p.out ? static_cast<float>(p.out[e]) : p.raw[e]) : tot;
+                    if (p.out) p.out[e] = static_cast<double>(t);
+                    else p.raw[e] = t;
                 }
             }
             ptx::named_bar_sync(1, kSnapCompute);  // bias / pos / stat reused by the next item
 #ifdef QVK_SNAP_TRACE
             ++tr_item;
 #endif
+          }
         }
     }
     ptx::tc_fence_before();
@@ -617,12 +609,17 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
     float* raw = nullptr;
     const int64_t total = g->total_tokens * n_kv;
     const int gq = n_q / n_kv;
-    const bool tc = gq * window <= 256 && window <= 256 && !env_knob("QVK_SNAPKV_SIMT", 0);
+    // tcgen05 path for every window: the gq * W window rows of a KV head are cut into nb blocks of gq * wb <= 256
+    // operand rows (wb window rows each), run one after another by the CTA that owns the (group, KV head) item.
+    const int per_block = std::max(1, 256 / gq);
+    const int nb = (window + per_block - 1) / per_block;
+    const int wb = (window + nb - 1) / nb;
+    const bool tc = gq <= 256 && !env_knob("QVK_SNAPKV_SIMT", 0);
     const bool direct = tc && pool == 1;  // the tcgen05 kernel writes the double scores itself: no pool pass
     if (!direct) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&raw), sizeof(float) * total, stream));
     if (tc) {
         CUtensorMap mq, mk;
-        if (!snap_map(&mq, q, n_q, g->total_tokens, static_cast<uint32_t>(gq), static_cast<uint32_t>(window)) ||
+        if (!snap_map(&mq, q, n_q, g->total_tokens, static_cast<uint32_t>(gq), static_cast<uint32_t>(wb)) ||
             !snap_map(&mk, k, n_kv, g->total_tokens, 1, 128)) {
             if (raw) cudaFreeAsync(raw, stream);
             set_error("snapkv: cuTensorMapEncodeTiled failed");
@@ -635,7 +632,9 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         sp.n_kv = n_kv;
         sp.gq = gq;
         sp.window = window;
-        sp.rows = gq * window;
+        sp.wb = wb;
+        sp.nb = nb;
+        sp.rows = gq * wb;
         sp.rows_pad = (sp.rows + 31) / 32 * 32;
         sp.sl2 = sl2;
         sp.raw = raw;

@@ -351,9 +351,16 @@ def test_attention_vs_double_oracle(cuda):
 
 
 # ------------------------------------------------------------------------------------------------ SnapKV
-@pytest.mark.parametrize("sizes,window,pool", [([256, 100], 32, 1), ([1024], 32, 7), ([20], 32, 1)])
-def test_snapkv_vs_oracle(cuda, sizes, window, pool):
-    n_q, n_kv = 28, 4
+@pytest.mark.parametrize("sizes,window,pool,n_q,n_kv", [
+    ([256, 100], 32, 1, 28, 4), ([1024], 32, 7, 28, 4), ([20], 32, 1, 28, 4),
+    # gq * W > 256: the window rows are cut into blocks of <= 256 operand rows run one after another
+    ([300, 1024], 64, 1, 28, 4),   # 2 blocks of 32 window rows (224 operand rows each)
+    ([700, 129], 50, 3, 28, 4),    # 2 blocks of 25 rows, pooled
+    ([40, 513], 64, 1, 28, 4),     # window longer than the first group (rows before the group masked)
+    ([600], 100, 1, 16, 2),        # gq 8: 4 blocks of 25 rows
+    ([333], 300, 1, 4, 4),         # gq 1, W 300 > 256: 2 blocks of 150 rows
+])
+def test_snapkv_vs_oracle(cuda, sizes, window, pool, n_q, n_kv):
     plan = qp.GroupPlan.from_sizes(sizes, 0.25)
     g = plan.to(cuda)
     q = synth_groups(sizes, n_q, 128, 3, False, cuda)
