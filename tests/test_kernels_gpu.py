@@ -271,7 +271,10 @@ def check_tol(got, want, what):
 
 @pytest.mark.parametrize("sizes,n_q,n_kv,d", [([128], 1, 1, 128), ([256], 2, 1, 128), ([384, 100, 1, 129], 28, 4, 128),
                                               ([4096], 28, 4, 128), ([4096] * 2 + [1000], 28, 4, 128),
-                                              ([16384], 4, 4, 128), ([256] * 4, 4, 2, 64), ([1000, 37, 4096], 28, 4, 64)])
+                                              ([16384], 4, 4, 128), ([256] * 4, 4, 2, 64), ([1000, 37, 4096], 28, 4, 64),
+                                              # 320 ragged groups: the unit order's group blocks (~32 MB of K/V
+                                              # each) give 6 blocks, the last one short
+                                              ([128, 300, 17, 256] * 80, 28, 4, 128)])
 def test_attention_vs_torch_fp32(cuda, sizes, n_q, n_kv, d):
     plan = qp.GroupPlan.from_sizes(sizes, 0.5)
     g = plan.to(cuda)
