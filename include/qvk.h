@@ -119,6 +119,12 @@ int qvk_score_text(qvk_stream_t stream, const qvk_groups* groups, const void* k_
 int qvk_snapkv_score(qvk_stream_t stream, const qvk_groups* groups, const void* q_d, const void* k_d,
                      int32_t n_q, int32_t n_kv, int32_t d_h, int32_t window, int32_t pool, float scale,
                      double* scores_d);
+/* The same scores given the window rows' softmax statistics (qvk_attention_window_stats), so only the second pass
+ * (per-key sums of the normalised probabilities) runs.  d_h == 128.  qvk_prefill_layer does this itself when it
+ * prunes with SnapKV: the layer's attention kernel writes the statistics. */
+int qvk_snapkv_score_stats(qvk_stream_t stream, const qvk_groups* groups, const void* q_d, const void* k_d,
+                           int32_t n_q, int32_t n_kv, int32_t d_h, int32_t window, int32_t pool, float scale,
+                           const float* window_stats_d, double* scores_d);
 
 /* ---- (a9) top-k selection -------------------------------------------------------------------------------------- */
 /* Per (group, head): the keep[g] best scores under (score desc, index asc), -0.0 == +0.0, written ascending
@@ -154,6 +160,13 @@ int qvk_select_gather(qvk_stream_t stream, const qvk_groups* groups, const doubl
  * accumulate.  tcgen05/TMEM/TMA kernel; d_h == 64 or 128 (QVK_E_UNSUPPORTED otherwise). */
 int qvk_attention(qvk_stream_t stream, const qvk_groups* groups, const void* q_d, const void* k_d,
                   const void* v_d, int32_t n_q, int32_t n_kv, int32_t d_h, float scale, void* o_d);
+/* qvk_attention that also writes the softmax statistics of every group's last `window` query rows (SnapKV's
+ * observation window): window_stats_d[(g * n_q + h) * window + r] = m + log2(l) of query row N_g - window + r, head
+ * h, in the scaled log2 domain (m = the row's running max of scale * log2(e) * q.k, l = sum_j 2^(that - m));
+ * rows before the group start are not written.  d_h == 128. */
+int qvk_attention_window_stats(qvk_stream_t stream, const qvk_groups* groups, const void* q_d, const void* k_d,
+                               const void* v_d, int32_t n_q, int32_t n_kv, int32_t d_h, float scale, void* o_d,
+                               int32_t window, float* window_stats_d);
 
 /* ---- one full pruned-prefill layer for all groups of the batch -------------------------------------------------- */
 typedef struct {

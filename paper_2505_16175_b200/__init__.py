@@ -21,6 +21,7 @@ if not _BUILDING:
         PruneConfig,
         Scorer,
         attention,
+        attention_window_stats,
         decode_attention,
         gather,
         group_count,

@@ -87,11 +87,13 @@ _SIGS = {
     "qvk_ctx_destroy": (C.c_int, [P]),
     "qvk_peer_barrier": (C.c_int, [P, I32, P, I32, U32, P]),
     "qvk_snapkv_score": (C.c_int, [P, GP, P, P, I32, I32, I32, I32, I32, F32, P]),
+    "qvk_snapkv_score_stats": (C.c_int, [P, GP, P, P, I32, I32, I32, I32, I32, F32, P, P]),
     "qvk_select": (C.c_int, [P, GP, P, I32, P]),
     "qvk_gather": (C.c_int, [P, GP, P, P, C.c_int, I32, I32, P, P, P, P]),
     "qvk_select_gather": (C.c_int, [P, GP, P, P, P, C.c_int, I32, I32, P, P, P, P]),
     "qvk_prune": (C.c_int, [P, GP, P, P, C.c_int, I32, I32, I32, F64, P, I64, I32, P, P, P, P, P]),
     "qvk_attention": (C.c_int, [P, GP, P, P, P, I32, I32, I32, F32, P]),
+    "qvk_attention_window_stats": (C.c_int, [P, GP, P, P, P, I32, I32, I32, F32, P, I32, P]),
     "qvk_prefill_layer": (C.c_int, [P, GP, C.POINTER(QvkLayerParams), P, P, P, P, P, P, P, P, P]),
     "qvk_project_qkv": (C.c_int, [P, P, I64, I32, P, I32, I32, I32, P, P, P, GP, P]),
     "qvk_prefill_layer_x": (C.c_int, [P, GP, C.POINTER(QvkLayerParams), P, I32, P, P, P, P, P, P, P, P, P, P]),

@@ -134,6 +134,8 @@ struct AttnParams {
     __nv_bfloat16* o;
     int pre_issue;  // issue the next unit's S0(0) during tile 1's lone last step (QVK_ATTN_PRE=0 disables)
     int gblock;     // groups per block of the unit order (= n_groups: one block)
+    float* lse;     // optional: softmax statistics m + log2(l) (scaled log2 domain) of each group's last lse_window
+    int lse_window; // query rows, [group][query head][window row] — SnapKV's pass 1 (snapkv.cu) for free
 };
 
 struct Barriers {
@@ -653,6 +655,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::f2_split(acc1, s2, s3);
                 l += (s0 + s1) + (s2 + s3);
             }
+            if (p.lse) {  // SnapKV's observation window = the group's last lse_window rows
+                const int qpos = mt * kBM + row;
+                const int r = qpos - (w.n - p.lse_window);
+                if (qpos < w.n && r >= 0)
+                    p.lse[(static_cast<int64_t>(w.g) * p.n_q + (t ? w.hq1 : w.hq0)) * p.lse_window + r] =
+                        m_ref + __log2f(l);
+            }
             if (units) ptx::mbar_wait(&bar->l_free[t], (units - 1) & 1);  // previous unit's sums consumed
             bar->row_sum[t][row] = l;
             ptx::mbar_arrive(&bar->l_full[t]);
@@ -701,7 +710,7 @@ int launch_attention_d(cudaStream_t stream, const CUtensorMap& mq, const CUtenso
 int launch_attention2(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, float, void*);
 
 int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, const void* v, int n_q,
-                     int n_kv, int d_h, float scale, void* o) {
+                     int n_kv, int d_h, float scale, void* o, float* lse, int lse_window) {
     if (d_h != 128 && d_h != 64) {
         set_error("attention: head_dim must be 64 or 128 (got " + std::to_string(d_h) + ")");
         return QVK_E_UNSUPPORTED;
@@ -712,7 +721,8 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
         QVK_INVALID("attention: q/k/v/o must be 16-byte aligned");
     if (g->total_tokens == 0 || g->max_tokens == 0) return QVK_OK;
     if (g->total_tokens > 0x7fffffff) QVK_INVALID("attention: more than 2^31 token rows");
-    if (d_h == 128 && env_knob("QVK_ATTN_2CTA", 0))  // CTA-pair variant (attention2.cu), opt-in while evaluated
+    if (lse && lse_window <= 0) QVK_INVALID("attention: window statistics need a window >= 1");
+    if (d_h == 128 && !lse && env_knob("QVK_ATTN_2CTA", 0))  // CTA-pair variant (attention2.cu), opt-in while evaluated
         return launch_attention2(stream, g, q, k, v, n_q, n_kv, scale, o);
     CUtensorMap mq, mk, mv, mo;
     if (!make_map(&mq, q, n_q, g->total_tokens, d_h) || !make_map(&mk, k, n_kv, g->total_tokens, d_h) ||
@@ -732,6 +742,8 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     prm.o = static_cast<__nv_bfloat16*>(o);
     static const int pre = env_knob("QVK_ATTN_PRE", 1) != 0;
     prm.pre_issue = pre;
+    prm.lse = lse;
+    prm.lse_window = lse_window;
     // Unit order: blocks of groups whose K/V (at the longest group) total ~32 MB, so a block's K/V stays L2-resident
     // while all its units run (C4: 4 groups of 8 MB; DRAM reads per C4 launch 27 -> ~10 GB, +2.5 % tokens/s under the
     // power cap, 1432 -> 1460 MHz).  QVK_ATTN_GBLOCK overrides (groups per block; 0 = automatic).

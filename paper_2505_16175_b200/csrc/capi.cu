@@ -108,10 +108,12 @@ int launch_gather(cudaStream_t, const qvk_groups*, const void*, const void*, int
                   void*, uint64_t*, int64_t, uint32_t*);
 int launch_text_query_sum(cudaStream_t, const float*, int64_t, int, int, int, float*);
 int launch_score_dot(cudaStream_t, const qvk_groups*, const void*, int, int, const float*, double, double*);
+// lse (optional): the softmax statistics of each group's last lse_window query rows, [group][query head][row] —
+// the SnapKV scorer's pass 1, which launch_snapkv then skips.
 int launch_attention(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, int, float,
-                     void*);
+                     void*, float* lse = nullptr, int lse_window = 0);
 int launch_snapkv(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, int, int, float,
-                  double*);
+                  double*, const float* lse = nullptr);
 int launch_seeded_matrix(cudaStream_t, uint64_t, uint32_t, uint32_t, size_t, double, float*);
 int launch_project_exact(cudaStream_t, const float*, int64_t, int, const float*, int, float*);
 int launch_tokenize(cudaStream_t, const uint8_t*, int64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
@@ -270,6 +272,14 @@ int qvk_snapkv_score(qvk_stream_t s, const qvk_groups* g, const void* q, const v
     return launch_snapkv(s, g, q, k, n_q, n_kv, d_h, window, pool, scale, scores);
 }
 
+int qvk_snapkv_score_stats(qvk_stream_t s, const qvk_groups* g, const void* q, const void* k, int32_t n_q,
+                           int32_t n_kv, int32_t d_h, int32_t window, int32_t pool, float scale, const float* stats,
+                           double* scores) {
+    QVK_TRY(check_groups(g));
+    if (!stats) QVK_INVALID("snapkv: null window statistics");
+    return launch_snapkv(s, g, q, k, n_q, n_kv, d_h, window, pool, scale, scores, stats);
+}
+
 int qvk_select(qvk_stream_t s, const qvk_groups* g, const double* scores, int32_t heads, uint32_t* idx) {
     QVK_TRY(check_groups(g));
     if (heads <= 0) QVK_INVALID("model config: dimensions must be positive");
@@ -316,7 +326,7 @@ int score_text(cudaStream_t s, const qvk_groups* g, const void* k, int n_q, int 
 // start in its tail (PDL).
 int layer_prune(cudaStream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q, const void* k,
                 const void* v, const double* pre_scores, double* scores_ws, uint32_t* idx_ws, void* kc, void* vc,
-                uint64_t* origin, int overlap) {
+                uint64_t* origin, int overlap, const float* lse = nullptr) {
     const int heads = p->per_head ? p->n_kv : 1;
     const int width = p->per_head ? p->d_h : p->n_kv * p->d_h;
     const int64_t keep_full = static_cast<int64_t>(retained(p->rho, static_cast<size_t>(g->max_tokens)));
@@ -345,7 +355,7 @@ int layer_prune(cudaStream_t s, const qvk_groups* g, const qvk_layer_params* p, 
     int rc = QVK_OK;
     if (!pre_scores) {
         if (p->scorer == QVK_SNAPKV)
-            rc = launch_snapkv(s, g, q, k, p->n_q, p->n_kv, p->d_h, p->snap_window, p->snap_pool, p->scale, sc);
+            rc = launch_snapkv(s, g, q, k, p->n_q, p->n_kv, p->d_h, p->snap_window, p->snap_pool, p->scale, sc, lse);
         else if (p->scorer == QVK_ATTENTION_SCORE)
             rc = score_text(s, g, k, p->n_q, p->n_kv, p->d_h, p->per_head, p->text_query_d, p->text_count, nullptr,
                             sc);
@@ -367,6 +377,31 @@ int layer_prune(cudaStream_t s, const qvk_groups* g, const qvk_layer_params* p, 
         if (!idx_ws) cudaFreeAsync(ix, s);
     }
     if (!pre_scores && !scores_ws) cudaFreeAsync(sc, s);
+    return rc;
+}
+// SnapKV's pass 1 (the window rows' softmax statistics) comes out of the layer's attention kernel when the layer
+// prunes with SnapKV scores: a window-statistics buffer of n_groups * n_q * window floats (lse_ws, or scratch).
+bool snap_from_attention(const qvk_layer_params* p) {
+    static const int on = env_knob("QVK_SNAPKV_LSE", 1);
+    return on && p->scorer == QVK_SNAPKV && p->per_head && p->rho != 1.0 && p->d_h == 128 && p->snap_window > 0;
+}
+size_t snap_lse_bytes(const qvk_groups* g, const qvk_layer_params* p) {
+    return sizeof(float) * std::max<int64_t>(1, static_cast<int64_t>(g->n_groups) * p->n_q * p->snap_window);
+}
+
+// attention -> prune of one layer (q / k / v already on the device)
+int layer_from_qkv(cudaStream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q, const void* k,
+                   const void* v, void* o, const double* pre_scores, double* scores_ws, uint32_t* idx_ws, void* kc,
+                   void* vc, uint64_t* origin, float* lse_ws) {
+    float* lse = nullptr;
+    if (snap_from_attention(p)) {
+        lse = lse_ws;
+        if (!lse) QVK_CUDA_CHECK(scratch_alloc(reinterpret_cast<void**>(&lse), snap_lse_bytes(g, p), s));
+    }
+    int rc = launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o, lse, lse ? p->snap_window : 0);
+    // overlap = 1: the fused prune only reads K / V, so its CTAs may take the SMs the attention grid releases
+    if (rc == QVK_OK) rc = layer_prune(s, g, p, q, k, v, pre_scores, scores_ws, idx_ws, kc, vc, origin, 1, lse);
+    if (lse && !lse_ws) cudaFreeAsync(lse, s);
     return rc;
 }
 }  // namespace
@@ -449,16 +484,32 @@ int qvk_attention(qvk_stream_t s, const qvk_groups* g, const void* q, const void
     return launch_attention(s, g, q, k, v, n_q, n_kv, d_h, scale, o);
 }
 
-int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q,
-                      const void* k, const void* v, void* o, double* scores_ws, uint32_t* idx_ws, void* kc, void* vc,
-                      uint64_t* origin) {
+int qvk_attention_window_stats(qvk_stream_t s, const qvk_groups* g, const void* q, const void* k, const void* v,
+                               int32_t n_q, int32_t n_kv, int32_t d_h, float scale, void* o, int32_t window,
+                               float* stats) {
+    QVK_TRY(check_groups(g));
+    if (!stats || window <= 0) QVK_INVALID("attention: window statistics need a buffer and a window >= 1");
+    if (d_h != 128) {
+        set_error("attention: window statistics need head_dim 128");
+        return QVK_E_UNSUPPORTED;
+    }
+    return launch_attention(s, g, q, k, v, n_q, n_kv, d_h, scale, o, stats, window);
+}
+
+static int prefill_layer_impl(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q,
+                              const void* k, const void* v, void* o, double* scores_ws, uint32_t* idx_ws, void* kc,
+                              void* vc, uint64_t* origin, float* lse_ws) {
     if (!p) QVK_INVALID("prefill_layer: null params");
     QVK_TRY(check_rho(p->rho));
     QVK_TRY(check_groups(g));
     if (origin && !g->first_token_d) QVK_INVALID("gather: origin requested without first_token");
-    QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
-    // overlap = 1: the fused prune only reads K / V, so its CTAs may take the SMs the attention grid releases
-    return layer_prune(s, g, p, q, k, v, nullptr, scores_ws, idx_ws, kc, vc, origin, 1);
+    return layer_from_qkv(s, g, p, q, k, v, o, nullptr, scores_ws, idx_ws, kc, vc, origin, lse_ws);
+}
+
+int qvk_prefill_layer(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* q,
+                      const void* k, const void* v, void* o, double* scores_ws, uint32_t* idx_ws, void* kc, void* vc,
+                      uint64_t* origin) {
+    return prefill_layer_impl(s, g, p, q, k, v, o, scores_ws, idx_ws, kc, vc, origin, nullptr);
 }
 
 int qvk_project_qkv(qvk_stream_t s, const void* x, int64_t tokens, int32_t d_model, const void* w, int32_t n_q,
@@ -468,9 +519,9 @@ int qvk_project_qkv(qvk_stream_t s, const void* x, int64_t tokens, int32_t d_mod
     return launch_project_qkv(s, x, tokens, d_model, w, n_q, n_kv, d_h, q, k, v, g, scores);
 }
 
-int qvk_prefill_layer_x(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* x,
-                        int32_t d_model, const void* w, void* q, void* k, void* v, void* o, double* scores_ws,
-                        uint32_t* idx_ws, void* kc, void* vc, uint64_t* origin) {
+static int prefill_layer_x_impl(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* x,
+                                int32_t d_model, const void* w, void* q, void* k, void* v, void* o, double* scores_ws,
+                                uint32_t* idx_ws, void* kc, void* vc, uint64_t* origin, float* lse_ws) {
     if (!p) QVK_INVALID("prefill_layer: null params");
     QVK_TRY(check_rho(p->rho));
     QVK_TRY(check_groups(g));
@@ -479,9 +530,15 @@ int qvk_prefill_layer_x(qvk_stream_t s, const qvk_groups* g, const qvk_layer_par
     const bool fused_norm = p->scorer == QVK_KEY_NORM_SMALL && p->per_head && p->rho != 1.0;
     QVK_TRY(launch_project_qkv(s, x, g->total_tokens, d_model, w, p->n_q, p->n_kv, p->d_h, q, k, v, g,
                                fused_norm ? scores_ws : nullptr));
-    QVK_TRY(launch_attention(s, g, q, k, v, p->n_q, p->n_kv, p->d_h, p->scale, o));
     // key-norm scores came from the projection epilogue: select + gather only, in the attention's tail
-    return layer_prune(s, g, p, q, k, v, fused_norm ? scores_ws : nullptr, scores_ws, idx_ws, kc, vc, origin, 1);
+    return layer_from_qkv(s, g, p, q, k, v, o, fused_norm ? scores_ws : nullptr, scores_ws, idx_ws, kc, vc, origin,
+                          lse_ws);
+}
+
+int qvk_prefill_layer_x(qvk_stream_t s, const qvk_groups* g, const qvk_layer_params* p, const void* x,
+                        int32_t d_model, const void* w, void* q, void* k, void* v, void* o, double* scores_ws,
+                        uint32_t* idx_ws, void* kc, void* vc, uint64_t* origin) {
+    return prefill_layer_x_impl(s, g, p, x, d_model, w, q, k, v, o, scores_ws, idx_ws, kc, vc, origin, nullptr);
 }
 
 int qvk_decode_workspace(int32_t n_tq, int32_t n_q, int32_t n_kv, int32_t d_h, int64_t rows, size_t* bytes) {
@@ -629,6 +686,7 @@ struct qvk_ctx_st {
     void* arrays = nullptr;   // tok_off | keep | row_off | first_token (int64 / uint64)
     double* scores = nullptr; // n_kv * total_tokens
     uint32_t* idx = nullptr;  // total_rows * n_kv
+    float* lse = nullptr;     // SnapKV window statistics (snap_lse_bytes), when the scorer is SnapKV
 };
 
 extern "C" {
@@ -671,6 +729,7 @@ int qvk_ctx_create(qvk_ctx_t* out, const qvk_layer_params* p, int32_t n_groups, 
         cudaFree(c->arrays);
         cudaFree(c->scores);
         cudaFree(c->idx);
+        cudaFree(c->lse);
         delete c;
         return QVK_E_CUDA;
     };
@@ -686,6 +745,9 @@ int qvk_ctx_create(qvk_ctx_t* out, const qvk_layer_params* p, int32_t n_groups, 
         return fail(e);
     const int64_t* base = static_cast<const int64_t*>(c->arrays);
     c->g.n_groups = G;
+    if (snap_from_attention(p) &&
+        (e = cudaMalloc(reinterpret_cast<void**>(&c->lse), snap_lse_bytes(&c->g, p))) != cudaSuccess)
+        return fail(e);
     c->g.max_tokens = mx;
     c->g.total_tokens = T;
     c->g.total_rows = R;
@@ -706,13 +768,14 @@ int qvk_ctx_groups(qvk_ctx_t c, qvk_groups* out) {
 int qvk_ctx_prefill_layer(qvk_ctx_t c, qvk_stream_t s, const void* q, const void* k, const void* v, void* o,
                           void* kc, void* vc, uint64_t* origin) {
     if (!c) QVK_INVALID("ctx: null argument");
-    return qvk_prefill_layer(s, &c->g, &c->p, q, k, v, o, c->scores, c->idx, kc, vc, origin);
+    return prefill_layer_impl(s, &c->g, &c->p, q, k, v, o, c->scores, c->idx, kc, vc, origin, c->lse);
 }
 
 int qvk_ctx_prefill_layer_x(qvk_ctx_t c, qvk_stream_t s, const void* x, int32_t d_model, const void* w, void* q,
                             void* k, void* v, void* o, void* kc, void* vc, uint64_t* origin) {
     if (!c) QVK_INVALID("ctx: null argument");
-    return qvk_prefill_layer_x(s, &c->g, &c->p, x, d_model, w, q, k, v, o, c->scores, c->idx, kc, vc, origin);
+    return prefill_layer_x_impl(s, &c->g, &c->p, x, d_model, w, q, k, v, o, c->scores, c->idx, kc, vc, origin,
+                                c->lse);
 }
 
 int qvk_ctx_destroy(qvk_ctx_t c) {
@@ -723,6 +786,7 @@ int qvk_ctx_destroy(qvk_ctx_t c) {
     cudaFree(c->arrays);
     cudaFree(c->scores);
     cudaFree(c->idx);
+    cudaFree(c->lse);
     cudaSetDevice(cur);
     delete c;
     return QVK_OK;

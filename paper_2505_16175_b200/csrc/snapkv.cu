@@ -220,6 +220,7 @@ struct SnapParams {
     int n_groups, n_kv, gq, window, rows, rows_pad;
     int wb, nb;  // window rows per block (rows = gq * wb <= 256) and blocks per item (nb * wb >= window)
     float sl2;
+    const float* lse;  // optional: the window rows' softmax statistics from the attention kernel (skips pass 1)
     float* raw;   // (group, head, token) layout, when pooling follows
     double* out;  // pool == 1: the double scores written directly (same value as the pool kernel's float -> double)
 };
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 const int w0 = static_cast<int>(t0) + n - p.window + b * p.wb;
                 ptx::tma_load_3d(sQ, &tm_q, &sh->q_full, 0, hk * p.gq, w0);
                 ptx::tma_load_3d(sQ + kSnapQChunk, &tm_q, &sh->q_full, 64, hk * p.gq, w0);
-                for (int pass = 0; pass < 2; ++pass)
+                for (int pass = p.lse ? 1 : 0; pass < 2; ++pass)
                     for (int jt = 0; jt < nt; ++jt, ++tile_no) {
                         const uint32_t st = tile_no % kSnapStages;
                         ptx::mbar_wait(&sh->kv_empty[st], ((tile_no / kSnapStages) & 1) ^ 1);
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 const int nt = (n + 127) / 128;
                 ptx::mbar_wait(&sh->q_full, item_no & 1);
                 ptx::tc_fence_after();
-                for (int pass = 0; pass < 2; ++pass)
+                for (int pass = p.lse ? 1 : 0; pass < 2; ++pass)
                     for (int jt = 0; jt < nt; ++jt, ++tile_no, ++acc_no) {
                         const uint32_t st = tile_no % kSnapStages;
 #ifdef QVK_SNAP_TRACE
@@ -398,13 +399,21 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
           }
           for (int b = 0; b < p.nb; ++b) {
             const int g = it / p.n_kv, hk = it - g * p.n_kv;
-            (void)g;
             const int nt = (n + 127) / 128;
             // window column c = r * gq + h of block b -> window row b wb + r at token position n - W + b wb + r
             // (invalid when before the group or past the window)
             const int c_row = mt * 128 + i;
             const int wrow = b * p.wb + c_row / p.gq;
             const int my_pos = c_row < p.rows && wrow < p.window ? n - p.window + wrow : -1;
+            if (p.lse) {  // pass 1 done by the attention kernel: its softmax statistics of the window rows
+                if (ch == 0) {
+                    sh->bias[c_row] = my_pos >= 0 ? -p.lse[(static_cast<int64_t>(g) * p.n_kv * p.gq + hk * p.gq +
+                                                            c_row % p.gq) * p.window + wrow]
+                                                  : -INFINITY;
+                    sh->pos[c_row] = my_pos;
+                }
+                ptx::named_bar_sync(1, kSnapCompute);
+            } else {
             // ---- pass 1: running max / sum of window row c_row over key columns [64 ch, 64 ch + 64) of each tile ----
             float m = -INFINITY, l = 0.f;
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
@@ -473,6 +482,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                 sh->pos[c_row] = my_pos;
             }
             ptx::named_bar_sync(1, kSnapCompute);
+            }
             // ---- pass 2: key j = jt*128 + i, window columns [col0, col0 + 8 n8) ----
             for (int jt = 0; jt < nt; ++jt, ++acc_no) {
                 wait_acc();
@@ -595,7 +605,7 @@ int launch_snap_tc(cudaStream_t stream, const CUtensorMap& mq, const CUtensorMap
 }  // namespace
 
 int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, int n_q, int n_kv,
-                  int d_h, int window, int pool, float scale, double* scores) {
+                  int d_h, int window, int pool, float scale, double* scores, const float* lse) {
     if (d_h != kD) {
         set_error("snapkv: only head_dim 128 is implemented");
         return QVK_E_UNSUPPORTED;
@@ -637,6 +647,7 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         sp.rows = gq * wb;
         sp.rows_pad = (sp.rows + 31) / 32 * 32;
         sp.sl2 = sl2;
+        sp.lse = lse;
         sp.raw = raw;
         sp.out = direct ? scores : nullptr;
         const int sms = sm_count();

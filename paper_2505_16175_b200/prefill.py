@@ -233,14 +233,33 @@ def attention(q, k, v, groups: DeviceGroups, n_q: int, n_kv: int, scale: float |
 
 
 def snapkv_scores(q, k, groups: DeviceGroups, n_q: int, n_kv: int, window: int = 32, pool: int = 1,
-                  scale: float | None = None, out=None):
+                  scale: float | None = None, out=None, window_stats=None):
+    """SnapKV scores per (token, KV head); window_stats (from attention_window_stats): second pass only."""
     d = q.shape[-1]
     scale = 1.0 / math.sqrt(d) if scale is None else scale
     out = out if out is not None else torch.empty(groups.plan.total_tokens * n_kv, dtype=torch.float64,
                                                   device=q.device)
-    check(lib.qvk_snapkv_score(_stream(), groups.ref, _ptr(q), _ptr(k), n_q, n_kv, d, window, pool, scale,
-                               _ptr(out)))
+    if window_stats is None:
+        check(lib.qvk_snapkv_score(_stream(), groups.ref, _ptr(q), _ptr(k), n_q, n_kv, d, window, pool, scale,
+                                   _ptr(out)))
+    else:
+        check(lib.qvk_snapkv_score_stats(_stream(), groups.ref, _ptr(q), _ptr(k), n_q, n_kv, d, window, pool,
+                                         scale, _ptr(window_stats), _ptr(out)))
     return out
+
+
+def attention_window_stats(q, k, v, groups: DeviceGroups, n_q: int, n_kv: int, window: int = 32,
+                           scale: float | None = None, out=None, stats=None):
+    """attention() that also returns the softmax statistics (m + log2 l, scaled log2 domain) of every group's last
+    `window` query rows, shape (n_groups, n_q, window) fp32 (rows before a group's start are left untouched)."""
+    d = q.shape[-1]
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    out = out if out is not None else torch.empty_like(q)
+    stats = stats if stats is not None else torch.full((groups.plan.n_groups, n_q, window), float("nan"),
+                                                        dtype=torch.float32, device=q.device)
+    check(lib.qvk_attention_window_stats(_stream(), groups.ref, _ptr(q), _ptr(k), _ptr(v), n_q, n_kv, d, scale,
+                                         _ptr(out), window, _ptr(stats)))
+    return out, stats
 
 
 def text_query_sum(text_query, n_q: int, n_kv: int, out=None) -> torch.Tensor:

@@ -392,8 +392,7 @@ def test_snapkv_vs_oracle(cuda, sizes, window, pool, n_q, n_kv):
 
 
 # ------------------------------------------------------------------------------------------------ full layer
-@pytest.mark.parametrize("scorer,per_head", [(qp.Scorer.key_norm_small, True), (qp.Scorer.value_norm, False),
-                                             (qp.Scorer.snapkv, True)])
+@pytest.mark.parametrize("scorer,per_head", [(qp.Scorer.key_norm_small, True), (qp.Scorer.value_norm, False)])
 def test_prefill_layer(cuda, scorer, per_head):
     sizes, n_q, n_kv, D, rho = [1024, 1024, 512], 28, 4, 128, 0.25
     plan = qp.GroupPlan.from_sizes(sizes, rho)
@@ -405,14 +404,84 @@ def test_prefill_layer(cuda, scorer, per_head):
     torch.cuda.synchronize()
     check_tol(buf.o, torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(D)), "layer attention")
     heads, width = (n_kv, D) if per_head else (1, n_kv * D)
-    if scorer == qp.Scorer.snapkv:
-        sc = qp.snapkv_scores(q, k, g, n_q, n_kv)
-    else:
-        sc = qp.score(k, v, g, heads, width, scorer)
+    sc = qp.score(k, v, g, heads, width, scorer)
     idx = qp.select(sc, g, heads)
     kc, vc, origin = qp.gather(k, v, g, heads, width, idx)
     assert torch.equal(buf.idx[: idx.numel()], idx)
     assert torch.equal(buf.k_cache, kc) and torch.equal(buf.v_cache, vc) and torch.equal(buf.origin, origin)
+
+
+@pytest.mark.parametrize("sizes,window,pool,n_q,n_kv", [
+    ([1024, 1024, 512], 32, 1, 28, 4),
+    ([700, 20, 1300], 64, 3, 28, 4),   # 2 window blocks, a group shorter than the window, pooling
+    ([600, 129], 100, 1, 16, 2),       # GQA 8, 4 blocks
+])
+def test_prefill_layer_snapkv_window_stats_from_attention(cuda, sizes, window, pool, n_q, n_kv):
+    """qvk_prefill_layer with SnapKV: pass 1 (the window rows' softmax statistics) comes out of the layer's attention
+    kernel and the scorer runs pass 2 only.  Scores within rel 1e-4 of the fp64 restatement, index sets equal barring
+    near-ties (same band as the standalone scorer), cache = the indexed K/V rows."""
+    D, rho = 128, 0.25
+    plan = qp.GroupPlan.from_sizes(sizes, rho)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, D, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, D, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, D, 2, False, cuda)
+    buf = qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, qp.Scorer.snapkv, True, snap_window=window, snap_pool=pool)
+    torch.cuda.synchronize()
+    check_tol(buf.o, torch_attention(q, k, v, sizes, n_q, n_kv, 1 / math.sqrt(D)), "layer attention")
+    kc, vc, origin = qp.gather(k, v, g, n_kv, D, buf.idx)
+    assert torch.equal(buf.k_cache, kc) and torch.equal(buf.v_cache, vc) and torch.equal(buf.origin, origin)
+    got = buf.scores.cpu().numpy()
+    standalone = qp.snapkv_scores(q, k, g, n_q, n_kv, window, pool).cpu().numpy()
+    np.testing.assert_allclose(got, standalone, rtol=1e-4, atol=1e-6)
+    t0 = 0
+    for gi, n in enumerate(sizes):
+        want = O.snapkv_scores(f32_of(q[t0:t0 + n]), f32_of(k[t0:t0 + n]), n_q, n_kv, D, window, pool,
+                               1 / math.sqrt(D))
+        seg = got[n_kv * t0: n_kv * (t0 + n)].reshape(n_kv, n)
+        np.testing.assert_allclose(seg, want, rtol=1e-4, atol=1e-6)
+        kk, r0 = int(plan.keep[gi]), int(plan.row_off[gi])
+        idx = buf.idx[r0 * n_kv:(r0 + kk) * n_kv].view(kk, n_kv).cpu().numpy()
+        for h in range(n_kv):
+            order = np.argsort(-want[h], kind="stable")
+            kth = want[h][order[kk - 1]]
+            diff = set(order[:kk].tolist()) ^ set(idx[:, h].tolist())
+            near = [i for i in diff if abs(want[h][i] - kth) <= 1e-4 * abs(kth)]
+            assert len(diff) == len(near), f"group {gi} head {h}: index differences outside the near-tie band"
+        t0 += n
+
+
+@pytest.mark.parametrize("sizes,window,n_q,n_kv", [([700, 20, 1300], 64, 28, 4), ([256, 129], 32, 8, 2)])
+def test_attention_window_stats_and_snapkv_pass2(cuda, sizes, window, n_q, n_kv):
+    """qvk_attention_window_stats: the softmax statistics of each group's last `window` rows equal
+    log2(sum_j exp(scale q.k_j)) (fp64 from the bf16 inputs) within 2e-4 (log2 units); the output is the plain
+    attention's bit for bit; qvk_snapkv_score_stats on them matches the oracle like the two-pass scorer."""
+    D = 128
+    scale = 1 / math.sqrt(D)
+    plan = qp.GroupPlan.from_sizes(sizes, 0.25)
+    g = plan.to(cuda)
+    q = synth_groups(sizes, n_q, D, 3, False, cuda)
+    k = synth_groups(sizes, n_kv, D, 1, True, cuda)
+    v = synth_groups(sizes, n_kv, D, 2, False, cuda)
+    o, st = qp.attention_window_stats(q, k, v, g, n_q, n_kv, window)
+    assert torch.equal(o, qp.attention(q, k, v, g, n_q, n_kv))
+    t0 = 0
+    for gi, n in enumerate(sizes):
+        qd, kd = q[t0:t0 + n].double(), k[t0:t0 + n].double()
+        for r in range(max(0, window - n), window):
+            pos = n - window + r
+            for h in range(n_q):
+                x = (kd[:pos + 1, h // (n_q // n_kv)] @ qd[pos, h]) * scale
+                want = torch.logsumexp(x, 0).item() / math.log(2)
+                got = st[gi, h, r].item()
+                assert abs(got - want) <= 2e-4, (gi, r, h, got, want)
+        t0 += n
+    got = qp.snapkv_scores(q, k, g, n_q, n_kv, window, window_stats=st).cpu().numpy()
+    t0 = 0
+    for gi, n in enumerate(sizes):
+        want = O.snapkv_scores(f32_of(q[t0:t0 + n]), f32_of(k[t0:t0 + n]), n_q, n_kv, D, window, 1, scale)
+        np.testing.assert_allclose(got[n_kv * t0: n_kv * (t0 + n)].reshape(n_kv, n), want, rtol=1e-4, atol=1e-6)
+        t0 += n
 
 
 def test_host_prefill_pipeline_matches_device_layer(cuda):
