@@ -113,7 +113,7 @@ int launch_score_dot(cudaStream_t, const qvk_groups*, const void*, int, int, con
 int launch_attention(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, int, float,
                      void*, float* lse = nullptr, int lse_window = 0);
 int launch_snapkv(cudaStream_t, const qvk_groups*, const void*, const void*, int, int, int, int, int, float,
-                  double*, const float* lse = nullptr);
+                  double*, const float* lse = nullptr, int after_attention = 0);
 int launch_seeded_matrix(cudaStream_t, uint64_t, uint32_t, uint32_t, size_t, double, float*);
 int launch_project_exact(cudaStream_t, const float*, int64_t, int, const float*, int, float*);
 int launch_tokenize(cudaStream_t, const uint8_t*, int64_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t,
@@ -355,7 +355,8 @@ int layer_prune(cudaStream_t s, const qvk_groups* g, const qvk_layer_params* p, 
     int rc = QVK_OK;
     if (!pre_scores) {
         if (p->scorer == QVK_SNAPKV)
-            rc = launch_snapkv(s, g, q, k, p->n_q, p->n_kv, p->d_h, p->snap_window, p->snap_pool, p->scale, sc, lse);
+            rc = launch_snapkv(s, g, q, k, p->n_q, p->n_kv, p->d_h, p->snap_window, p->snap_pool, p->scale, sc, lse,
+                               lse != nullptr);  // right behind the attention that writes lse: PDL
         else if (p->scorer == QVK_ATTENTION_SCORE)
             rc = score_text(s, g, k, p->n_q, p->n_kv, p->d_h, p->per_head, p->text_query_d, p->text_count, nullptr,
                             sc);

@@ -221,6 +221,7 @@ struct SnapParams {
     int wb, nb;  // window rows per block (rows = gq * wb <= 256) and blocks per item (nb * wb >= window)
     float sl2;
     const float* lse;  // optional: the window rows' softmax statistics from the attention kernel (skips pass 1)
+    int after_attention;  // launched (PDL) while the attention that writes lse may still run: compute warps wait
     float* raw;   // (group, head, token) layout, when pooling follows
     double* out;  // pool == 1: the double scores written directly (same value as the pool kernel's float -> double)
 };
@@ -351,6 +352,10 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         }
     } else {
         // ===== compute: warps 0-15, set = warp / 4 (four warps, one per TMEM lane quarter) =====
+        // Programmatic dependent launch behind the attention kernel: the TMA / MMA warps start on Q and K (inputs the
+        // attention only reads) in its tail; the window statistics it writes are read only after this wait, which
+        // also makes this grid's completion imply the attention's.
+        if (p.after_attention) asm volatile("griddepcontrol.wait;" ::: "memory");
         const int set = warp >> 2, quarter = warp & 3;
         const int i = quarter * 32 + lane;  // TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
@@ -597,15 +602,24 @@ int launch_snap_tc(cudaStream_t stream, const CUtensorMap& mq, const CUtensorMap
                    unsigned grid) {
     QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(snapkv_tc_kernel<kN8>),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSnapSmem)));
-    snapkv_tc_kernel<kN8><<<grid, kSnapThreads, kSnapSmem, stream>>>(mq, mk, sp);
-    QVK_LAUNCH_CHECK();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kSnapThreads);
+    cfg.dynamicSmemBytes = kSnapSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = sp.after_attention ? 1 : 0;
+    QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, snapkv_tc_kernel<kN8>, mq, mk, sp));
     return QVK_OK;
 }
 
 }  // namespace
 
 int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, int n_q, int n_kv,
-                  int d_h, int window, int pool, float scale, double* scores, const float* lse) {
+                  int d_h, int window, int pool, float scale, double* scores, const float* lse, int after_attention) {
     if (d_h != kD) {
         set_error("snapkv: only head_dim 128 is implemented");
         return QVK_E_UNSUPPORTED;
@@ -648,6 +662,7 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         sp.rows_pad = (sp.rows + 31) / 32 * 32;
         sp.sl2 = sl2;
         sp.lse = lse;
+        sp.after_attention = lse && after_attention && pool == 1;
         sp.raw = raw;
         sp.out = direct ? scores : nullptr;
         const int sms = sm_count();

@@ -69,6 +69,7 @@ def run(name, c, steps, warmup, dev):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     snap = c["scorer"] == "snapkv"
+    win_stats = torch.empty(plan.n_groups, n_q, 32, dtype=torch.float32, device=dev) if snap else None
     scorer = qp.Scorer.snapkv if snap else qp.Scorer.key_norm_small
     times = {"attention": [], "score": [], "prune": []}
 
@@ -83,13 +84,16 @@ def run(name, c, steps, warmup, dev):
         q, k, v = sets[l % len(sets)]
         e = [ev() for _ in range(4)]
         e[0].record(stream)
-        qp.attention(q, k, v, g, n_q, n_kv, out=o)
+        if snap and rho != 1.0:  # the production path: the attention also writes SnapKV's window statistics
+            qp.attention_window_stats(q, k, v, g, n_q, n_kv, 32, out=o, stats=win_stats)
+        else:
+            qp.attention(q, k, v, g, n_q, n_kv, out=o)
         e[1].record(stream)
         if rho == 1.0:  # identity path: no scoring (prefill.cpp:263-270)
             e[2].record(stream)
             qp.gather(k, v, g, n_kv, d, None, kc[l], vc[l], org[l])
         elif snap:
-            qp.snapkv_scores(q, k, g, n_q, n_kv, 32, 1, out=scores)
+            qp.snapkv_scores(q, k, g, n_q, n_kv, 32, 1, out=scores, window_stats=win_stats)
             e[2].record(stream)
             qp.select_gather(scores, k, v, g, n_kv, d, idx, kc[l], vc[l], org[l])
         else:
@@ -152,8 +156,14 @@ def run(name, c, steps, warmup, dev):
         "peaks": {"tflops": tf_burst, "tflops_sustained": tf_sus, "hbm_gbs": hbm, "source": src},
     }
     if snap:
+        # pass 2 only (pass 1 = the attention kernel's window statistics): one exponential per (window row of
+        # each query head, key); its MUFU floor at 16 ex2 / clk / SM and the 1965 MHz boost clock
+        exps = sum(int(n) * n_q * min(32, int(n)) for n in sizes)
+        floor_ms = exps / (16 * 148 * 1.965e9) * 1e3
         out["snapkv_score"] = {"ms": avg["score"], "bytes": b_score, "gbs": gbs(b_score, avg["score"]),
-                               "frac": (gbs(b_score, avg["score"]) or 0) / hbm}
+                               "frac": (gbs(b_score, avg["score"]) or 0) / hbm,
+                               "passes": "pass 2 only (window statistics from the attention kernel)",
+                               "mufu_floor_ms": floor_ms, "frac_of_mufu_floor": floor_ms / avg["score"]}
         out["select_gather"] = {"ms": avg["prune"], "bytes": b_prune, "gbs": gbs(b_prune, avg["prune"]),
                                 "frac": (gbs(b_prune, avg["prune"]) or 0) / hbm}
     return out
