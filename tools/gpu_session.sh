@@ -29,6 +29,9 @@ ncu)
 snapncu)
   timeout 300 python tools/snapkv_bench.py > "$OUT/snapkv_bench.jsonl" 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:snapkv_tc -s 1 -c 1 -f -o "$OUT/snap" \
-     python tools/snapkv_bench.py > "$OUT/ncu_snap.log" 2>&1 ;;
+     python tools/snapkv_bench.py > "$OUT/ncu_snap.log" 2>&1
+  # launch 22 of the C3 shape = the first pass-2-only launch (window statistics from the attention kernel)
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:snapkv_tc -s 21 -c 1 -f -o "$OUT/snap2" \
+     python tools/snapkv_bench.py > "$OUT/ncu_snap2.log" 2>&1 ;;
 esac; done
 ls -la "$OUT"
