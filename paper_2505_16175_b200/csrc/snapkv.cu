@@ -222,6 +222,8 @@ struct SnapParams {
     float sl2;
     const float* lse;  // optional: the window rows' softmax statistics from the attention kernel (skips pass 1)
     int after_attention;  // launched (PDL) while the attention that writes lse may still run: compute warps wait
+    int tiles_flat;       // > 0 (pass 2 only, one window block): CTAs own equal ranges of the (item, key tile) space
+                          // of tiles_flat tiles per item instead of whole items (pass-2 tiles are independent)
     float* raw;   // (group, head, token) layout, when pooling follows
     double* out;  // pool == 1: the double scores written directly (same value as the pool kernel's float -> double)
 };
@@ -230,6 +232,43 @@ __device__ __forceinline__ uint64_t snap_desc(uint32_t chunk_addr, uint32_t chun
     // k-step kk (16 of the 128 head-dim columns) of a K-major SW128 operand stored as two d-chunks.
     return ptx::umma_desc_sw128(chunk_addr + (kk >> 2) * chunk_stride + (kk & 3) * 32, 16, 1024);
 }
+
+// The work segments of a CTA: whole (group, KV head) items round-robin, or — pass 2 alone, where every key tile is
+// independent given the window statistics — a contiguous range of the items x tiles_flat key-tile space (C3: 2048
+// tiles over 148 CTAs = 13-14 each instead of 1.73 waves of 8-tile items).  Every role walks the same segments.
+struct SnapSegs {
+    int64_t f1;
+    int it, tm;
+    int64_t f0;
+    __device__ explicit SnapSegs(const SnapParams& p, int items) : tm(p.tiles_flat) {
+        if (tm > 0) {
+            const int64_t total = static_cast<int64_t>(items) * tm;
+            f0 = total * blockIdx.x / gridDim.x;
+            f1 = total * (blockIdx.x + 1) / gridDim.x;
+            it = static_cast<int>(f0 / tm);
+        } else {
+            f0 = f1 = 0;
+            it = blockIdx.x;
+        }
+    }
+    // next segment: item, key tiles [jt0, jt1) (jt1 clipped to the group's tiles by the caller)
+    __device__ bool next(int items, int& item, int& jt0, int& jt1) {
+        if (tm > 0) {
+            const int64_t base = static_cast<int64_t>(it) * tm;
+            if (base >= f1 || it >= items) return false;
+            item = it++;
+            jt0 = static_cast<int>(f0 > base ? f0 - base : 0);
+            jt1 = static_cast<int>(f1 - base < tm ? f1 - base : tm);
+            return true;
+        }
+        if (it >= items) return false;
+        item = it;
+        it += gridDim.x;
+        jt0 = 0;
+        jt1 = 0x7fffffff;
+        return true;
+    }
+};
 
 // kN8: 8-column chunks of the pass-2 window columns per compute set (rows_pad = 32 kN8).
 template <int kN8>
@@ -279,20 +318,25 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     if (warp == kSnapTmaWarp) {
         if (ptx::elect_one()) {  // ===== TMA producer =====
             uint32_t item_no = 0, tile_no = 0;
-            for (int it = blockIdx.x; it < items; it += gridDim.x)
-              for (int b = 0; b < p.nb; ++b, ++item_no) {
+            SnapSegs segs(p, items);
+            int it, jt0, jt1;
+            while (segs.next(items, it, jt0, jt1))
+              for (int b = 0; b < p.nb; ++b) {
                 const int g = it / p.n_kv, hk = it - g * p.n_kv;
                 const int64_t t0 = __ldg(p.tok_off + g);
                 const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - t0);
                 const int nt = (n + 127) / 128;
-                ptx::mbar_wait(&sh->q_empty, (item_no & 1) ^ 1);
+                const int jte = min(jt1, nt);
+                if (jt0 >= jte) continue;  // empty segment (every role skips it)
+                ++item_no;
+                ptx::mbar_wait(&sh->q_empty, ((item_no - 1) & 1) ^ 1);
                 ptx::mbar_arrive_expect_tx(&sh->q_full, 2 * p.rows * 128);
                 // window rows [b wb, b wb + wb): may start before the group or run past its end (rows masked)
                 const int w0 = static_cast<int>(t0) + n - p.window + b * p.wb;
                 ptx::tma_load_3d(sQ, &tm_q, &sh->q_full, 0, hk * p.gq, w0);
                 ptx::tma_load_3d(sQ + kSnapQChunk, &tm_q, &sh->q_full, 64, hk * p.gq, w0);
                 for (int pass = p.lse ? 1 : 0; pass < 2; ++pass)
-                    for (int jt = 0; jt < nt; ++jt, ++tile_no) {
+                    for (int jt = pass ? jt0 : 0; jt < (pass ? jte : nt); ++jt, ++tile_no) {
                         const uint32_t st = tile_no % kSnapStages;
                         ptx::mbar_wait(&sh->kv_empty[st], ((tile_no / kSnapStages) & 1) ^ 1);
                         uint8_t* dst = sK + st * kSnapKTile;
@@ -309,24 +353,29 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             const uint32_t id2 = ptx::idesc_bf16_f32(128, p.rows_pad, false, false);
             const uint32_t q_addr = ptx::smem_u32(sQ), k_base = ptx::smem_u32(sK);
             uint32_t item_no = 0, tile_no = 0, acc_no = 0;
-            for (int it = blockIdx.x; it < items; it += gridDim.x)
-              for (int b = 0; b < p.nb; ++b, ++item_no) {
+            SnapSegs segs(p, items);
+            int it, jt0, jt1;
+            while (segs.next(items, it, jt0, jt1))
+              for (int b = 0; b < p.nb; ++b) {
                 const int g = it / p.n_kv;
                 const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - __ldg(p.tok_off + g));
                 const int nt = (n + 127) / 128;
+                const int jte = min(jt1, nt);
+                if (jt0 >= jte) continue;
                 ptx::mbar_wait(&sh->q_full, item_no & 1);
+                ++item_no;
                 ptx::tc_fence_after();
                 for (int pass = p.lse ? 1 : 0; pass < 2; ++pass)
-                    for (int jt = 0; jt < nt; ++jt, ++tile_no, ++acc_no) {
+                    for (int jt = pass ? jt0 : 0; jt < (pass ? jte : nt); ++jt, ++tile_no, ++acc_no) {
                         const uint32_t st = tile_no % kSnapStages;
 #ifdef QVK_SNAP_TRACE
                         const int tr_tile = pass * nt + jt;
 #endif
                         ptx::mbar_wait(&sh->kv_full[st], (tile_no / kSnapStages) & 1);
-                        QVK_ST(item_no, tr_tile, 0);
+                        QVK_ST(item_no - 1, tr_tile, 0);
                         const uint32_t ab = acc_no & 1, acol = tmem + 256 * ab;  // accumulator buffer
                         ptx::mbar_wait(&sh->acc_empty[ab], ((acc_no >> 1) & 1) ^ 1);
-                        QVK_ST(item_no, tr_tile, 1);
+                        QVK_ST(item_no - 1, tr_tile, 1);
                         ptx::tc_fence_after();
                         const uint32_t ka = k_base + st * kSnapKTile;
                         if (pass == 0) {
@@ -345,8 +394,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
                         }
                         ptx::mma_commit(&sh->kv_empty[st]);
                         ptx::mma_commit(&sh->acc_full[ab]);
-                        if (pass == 1 && jt == nt - 1) ptx::mma_commit(&sh->q_empty);
-                        QVK_ST(item_no, tr_tile, 2);
+                        if (pass == 1 && jt == jte - 1) ptx::mma_commit(&sh->q_empty);
+                        QVK_ST(item_no - 1, tr_tile, 2);
                     }
             }
         }
@@ -387,24 +436,16 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         // pass 2: window columns [col0, col0 + 8 n8) — rows_pad split evenly over the four sets in 8-column chunks
         // (224 columns: 56 each; a 64 / 64 / 64 / 32 split left one set idle for a quarter of every tile)
         const int col0 = set * 8 * kN8;
-        // The next item's group bounds are loaded one item ahead: two dependent-free L2 loads at the item boundary
-        // held all 16 compute warps ~1400 cycles (tools/snap_trace.cu).
-        int64_t nx_t0 = 0, nx_t1 = 0;
-        if (blockIdx.x < items) {
-            nx_t0 = __ldg(p.tok_off + blockIdx.x / p.n_kv);
-            nx_t1 = __ldg(p.tok_off + blockIdx.x / p.n_kv + 1);
-        }
-        for (int it = blockIdx.x; it < items; it += gridDim.x) {
-          const int64_t t0 = nx_t0;
-          const int n = static_cast<int>(nx_t1 - nx_t0);
-          if (it + static_cast<int>(gridDim.x) < items) {
-              const int gn = (it + gridDim.x) / p.n_kv;
-              nx_t0 = __ldg(p.tok_off + gn);
-              nx_t1 = __ldg(p.tok_off + gn + 1);
-          }
+        SnapSegs segs(p, items);
+        int it, jt0, jt1;
+        while (segs.next(items, it, jt0, jt1)) {
+          const int g = it / p.n_kv, hk = it - g * p.n_kv;
+          const int64_t t0 = __ldg(p.tok_off + g);
+          const int n = static_cast<int>(__ldg(p.tok_off + g + 1) - t0);
+          const int nt = (n + 127) / 128;
+          const int jte = min(jt1, nt);
+          if (jt0 >= jte) continue;
           for (int b = 0; b < p.nb; ++b) {
-            const int g = it / p.n_kv, hk = it - g * p.n_kv;
-            const int nt = (n + 127) / 128;
             // window column c = r * gq + h of block b -> window row b wb + r at token position n - W + b wb + r
             // (invalid when before the group or past the window)
             const int c_row = mt * 128 + i;
@@ -489,7 +530,7 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             ptx::named_bar_sync(1, kSnapCompute);
             }
             // ---- pass 2: key j = jt*128 + i, window columns [col0, col0 + 8 n8) ----
-            for (int jt = 0; jt < nt; ++jt, ++acc_no) {
+            for (int jt = jt0; jt < jte; ++jt, ++acc_no) {
                 wait_acc();
                 QVK_STC(nt + jt, 0);
                 ptx::tc_fence_after();
@@ -666,7 +707,11 @@ int launch_snapkv(cudaStream_t stream, const qvk_groups* g, const void* q, const
         sp.raw = raw;
         sp.out = direct ? scores : nullptr;
         const int sms = sm_count();
-        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(static_cast<int64_t>(g->n_groups) * n_kv, sms));
+        // pass 2 alone with one window block: split the (item, key tile) space evenly over the CTAs
+        static const int flat_on = env_knob("QVK_SNAPKV_FLAT", 1);
+        sp.tiles_flat = (lse && nb == 1 && flat_on) ? static_cast<int>((g->max_tokens + 127) / 128) : 0;
+        const int64_t units = static_cast<int64_t>(g->n_groups) * n_kv * (sp.tiles_flat > 0 ? sp.tiles_flat : 1);
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
         int rc = QVK_OK;
         switch (sp.rows_pad / 32) {
             case 1: rc = launch_snap_tc<1>(stream, mq, mk, sp, grid); break;

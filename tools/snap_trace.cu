@@ -59,13 +59,13 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int it = 0; it < 3; ++it) qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc);
+    for (int it = 0; it < 3; ++it) qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc, nullptr, 0);
     static long long zero[2][64][10];
     cudaMemcpyToSymbol(qvk::g_snap_trace, zero, sizeof(zero));
     float best = 1e9;
     for (int it = 0; it < 5; ++it) {
         cudaEventRecord(e0);
-        qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc);
+        qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc, nullptr, 0);
         cudaEventRecord(e1);
         cudaDeviceSynchronize();
         float ms;
