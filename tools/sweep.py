@@ -9,6 +9,7 @@ bench.py keeps the driver contract on the headline config (C2); this tool covers
   C3   7B SnapKV: 1024 frames x 64 tok (64 groups x 1024), SnapKV w=32 rho 0.25, 28 layers
   C3b  same with 256 tok/frame (64 groups x 4096)
   C4   1 h @ 1 FPS: 3600 frames x 256 tok (225 groups x 4096), key-norm rho 0.5, 28 layers (1 GPU holds all groups)
+  C4L1 one C4 layer (225 groups x 4096) at rho {0.125, 0.25, 0.5}: the prune at the metric's scale
   C5   256 frames x 256 tok, group {4,8,16,32,64} frames x rho {0.125,0.25,0.5,1.0}, 1 layer
 Per layer: one qvk_prefill_layer call (attention, then the prune: fused key-norm score+select+gather, or SnapKV
 score + fused select+gather) into that layer's cache; a second, serialised pass times every kernel with CUDA events.  Layers use two alternating synthetic Q/K/V sets (each larger than L2, the
@@ -38,6 +39,10 @@ CONFIGS = {
     "C3b": dict(frames=1024, tpf=256, fpg=16, n_q=28, n_kv=4, d=128, layers=28, scorer="snapkv", rho=0.25),
     "C4": dict(frames=3600, tpf=256, fpg=16, n_q=28, n_kv=4, d=128, layers=28, scorer="key_norm_small", rho=0.5),
 }
+# the prune at the metric's scale (225 groups of 4096 tokens, ~12 waves of clusters) for every retention ratio
+for rho in (0.125, 0.25, 0.5):
+    CONFIGS[f"C4L1-r{rho}"] = dict(frames=3600, tpf=256, fpg=16, n_q=28, n_kv=4, d=128, layers=1,
+                                   scorer="key_norm_small", rho=rho)
 for fpg in (4, 8, 16, 32, 64):
     for rho in (0.125, 0.25, 0.5, 1.0):
         CONFIGS[f"C5-g{fpg}-r{rho}"] = dict(frames=256, tpf=256, fpg=fpg, n_q=28, n_kv=4, d=128, layers=1,
@@ -171,7 +176,7 @@ def run(name, c, steps, warmup, dev):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="C1,C2,C3,C3b,C4,C5")
+    ap.add_argument("--configs", default="C1,C2,C3,C3b,C4,C4L1,C5")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
     args = ap.parse_args()
@@ -179,7 +184,7 @@ def main():
     torch.cuda.set_device(dev)
     want = []
     for c in args.configs.split(","):
-        want += [k for k in CONFIGS if k == c or (c == "C5" and k.startswith("C5-"))]
+        want += [k for k in CONFIGS if k == c or (c in ("C5", "C4L1") and k.startswith(c + "-"))]
     for name in want:
         res = run(name, CONFIGS[name], args.steps, args.warmup, dev)
         print(json.dumps(res), flush=True)
