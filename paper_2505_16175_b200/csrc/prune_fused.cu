@@ -162,12 +162,6 @@ __device__ __noinline__ double seq_sumsq_global(const uint4* row, int chunks) {
     return acc;
 }
 
-// |x| of a normal bf16 (15-bit magnitude a = E<<7 | m, E >= 1) as a double, built with integer ops (no F2F):
-// exponent E - 127 + 1023 = E + 896, mantissa m in the top 7 bits.  a == 0 -> 0.0.  Subnormals (E == 0, a != 0)
-// come out wrong and inf / nan (E == 255) finite: rows holding either take the sequential fallback.
-__device__ __forceinline__ double bf16_mag_to_double(uint32_t a) {
-    return __hiloint2double(a ? static_cast<int>(a * 8192u + 0x38000000u) : 0, 0);
-}
 
 // W = row width in bf16 elements (64..512); CL = CTAs per segment (cluster size); kScore: compute norm scores
 // (negate = key_norm_small) from x, else read the double scores (SnapKV).
@@ -231,7 +225,7 @@ __global__ void __launch_bounds__(kThreads) prune_fused_kernel(
                     const uint32_t a = w[q] & 0x7fff7fffu;
                     mx2 = __vmaxu2(mx2, a);
                     mn2 = __vminu2(mn2, __vsub2(a, 0x00010001u));
-                    const double dl = bf16_mag_to_double(a & 0xffffu), dh = bf16_mag_to_double(a >> 16);
+                    const double dl = ptx::bf16_lo_scaled(w[q]), dh = ptx::bf16_hi_scaled(w[q]);
                     acc[0] = __fma_rn(dl, dl, acc[0]);  // squares of bf16 values are exact in double
                     acc[1] = __fma_rn(dh, dh, acc[1]);
                 }
@@ -249,10 +243,13 @@ __global__ void __launch_bounds__(kThreads) prune_fused_kernel(
             // (0 < |x| < 0x80) and inf / nan (|x| >= 0x7f80) are not representable above: sequential fallback.
             bool exact = mx < 0x7f80u;
             if (mn != 0xffffu) {  // some nonzero element: mn + 1 = smallest nonzero magnitude
-                exact = exact && mn + 1 >= 0x80u;
+                exact = exact && mn + 1 >= (37u << 7);  // >= 2^-90: the zero elements' stand-ins are absorbed
                 const int qmin = 2 * (static_cast<int>((mn + 1) >> 7) - 134);
-                const int es = static_cast<int>((__double_as_longlong(sum) >> 52) & 0x7ff) - 1023;
+                const int es = static_cast<int>((__double_as_longlong(sum) >> 52) & 0x7ff) - 1023 - 256;
                 exact = exact && es <= qmin + 52;
+                sum *= 0x1p-256;  // unscale (exact: the sum is >= 2^-180)
+            } else {
+                sum = 0.0;  // all zero
             }
             const int r = p0 + slot;
             if (sl == 0 && r < nr) {

@@ -332,5 +332,19 @@ __device__ __forceinline__ void ex2_poly2(float& a, float& b) {
     b = __uint_as_float(__float_as_uint(ph) + (__float_as_uint(th) << 23));
 }
 
+// The two bf16 of a 32-bit word as doubles SCALED by 2^128, with two integer ops each (shift, and-or; no F2F, no
+// select): magnitude bits (E << 7 | m) into exponent / mantissa bits 20..27 / 13..19 of the high word and exponent
+// bit 10 set, i.e. double exponent E + 1024 = (E - 127) + 128 + 1023.  A zero element becomes 2.0 (2^-127 unscaled)
+// and contributes 4 to the scaled sum of squares; such contributions vanish exactly in the rounding of any partial
+// sum that holds a nonzero square once every nonzero |x| >= 2^-90 (its scaled square >= 2^76 has ulp >= 2^24, and
+// at most 512 zeros add <= 2048 < 2^23) — the exactness test below requires that, and all-zero rows are detected
+// from the maximum.  Subnormals (E == 0, m != 0) and inf / nan (E == 255) come out wrong: sequential fallback.
+__device__ __forceinline__ double bf16_lo_scaled(uint32_t w) {
+    return __hiloint2double(static_cast<int>(((w << 13) & 0x0fffe000u) | 0x40000000u), 0);
+}
+__device__ __forceinline__ double bf16_hi_scaled(uint32_t w) {
+    return __hiloint2double(static_cast<int>(((w >> 3) & 0x0fffe000u) | 0x40000000u), 0);
+}
+
 }  // namespace ptx
 }  // namespace qvk
