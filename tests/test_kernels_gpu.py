@@ -618,6 +618,51 @@ def test_prune_fused_extreme_values(cuda):
     assert torch.equal(kc, kc2) and torch.equal(origin, origin2)
 
 
+def test_prune_fused_scores_zero_and_tiny_rows_bitexact(cuda):
+    """The fused scoring's scaled conversion: zero elements enter as stand-ins that must vanish exactly, which needs
+    every nonzero |x| >= 2^-90 (else the sequential fallback).  Rows mixing zeros with normal values, with values just
+    above / below 2^-90, a lone tiny nonzero among zeros, all-zero rows and huge values: the fused kernel's double
+    scores equal the separate key-norm kernel's bit for bit (both = the reference's sequential sums)."""
+    heads, width, n = 4, 128, 1536
+    gen = torch.Generator().manual_seed(11)
+    x = torch.randn(n, heads, width, generator=gen)
+    kind = torch.arange(n) % 8
+    zero = torch.rand(n, heads, width, generator=gen) < 0.3
+    x[(kind == 0)[:, None, None] & zero] = 0.0                                   # normal values, 30 % zeros
+    x[kind == 1] = x[kind == 1] * 2.0 ** -89                                     # tiny, >= 2^-90 mostly
+    x[(kind == 1)[:, None, None] & zero] = 0.0
+    x[kind == 2] = x[kind == 2] * 2.0 ** -91                                     # below 2^-90: fallback
+    x[(kind == 2)[:, None, None] & zero] = 0.0
+    x[kind == 3] = 0.0                                                           # all zero
+    x[kind == 4] = 0.0
+    x[kind == 4, :, 5] = 2.0 ** -90                                              # lone tiny at the bound
+    x[kind == 5] = x[kind == 5] * 2.0 ** 60                                      # huge
+    x[(kind == 5)[:, None, None] & zero] = 0.0
+    x[kind == 6] = 0.0
+    x[kind == 6, :, ::17] = 1.0                                                  # sparse ones
+    x[kind == 7] = x[kind == 7] * 2.0 ** -60                                     # small, zeros mixed
+    x[(kind == 7)[:, None, None] & zero] = 0.0
+    k = x.to(torch.bfloat16).to(cuda)
+    v = synth_groups([n], heads, width, 2, False, cuda)
+    plan = qp.GroupPlan.from_sizes([512, 1024], 0.5)
+    g = plan.to(cuda)
+    R = plan.total_rows
+    sc = torch.empty(n * heads, dtype=torch.float64, device=cuda)
+    idx = torch.empty(R * heads, dtype=torch.int32, device=cuda)
+    kc = torch.empty(R * heads * width, dtype=torch.bfloat16, device=cuda)
+    vc, org = torch.empty_like(kc), torch.empty(R * heads, dtype=torch.int64, device=cuda)
+    s = torch.cuda.current_stream().cuda_stream
+    for scorer in (qp.Scorer.key_norm_small, qp.Scorer.value_norm):
+        x_in = (k, v) if scorer == qp.Scorer.key_norm_small else (v, k)
+        qp._lib.check(qp.lib.qvk_prune(s, g.ref, x_in[0].data_ptr(), x_in[1].data_ptr(), qp._lib.QVK_BF16, heads,
+                                       width, int(scorer), 0.5, None, 0, heads, sc.data_ptr(), idx.data_ptr(),
+                                       kc.data_ptr(), vc.data_ptr(), org.data_ptr()))
+        want = qp.score(x_in[0], x_in[1], g, heads, width, scorer)
+        torch.cuda.synchronize()
+        assert qp.last_prune_route() == 0, "the fused kernel must have run"
+        assert torch.equal(sc.view(torch.int64), want.view(torch.int64)), scorer
+
+
 @pytest.mark.parametrize("sizes,window", [([1024, 1024, 300], 32), ([4096, 77], 16)])
 def test_select_gather_snapkv_matches_separate(cuda, sizes, window):
     """qvk_select_gather (one cluster launch from precomputed SnapKV scores) == qvk_select + qvk_gather."""
