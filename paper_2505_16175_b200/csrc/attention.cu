@@ -709,8 +709,9 @@ int launch_attention_d(cudaStream_t stream, const CUtensorMap& mq, const CUtenso
 
 int launch_attention2(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, float, void*);
 
+// (defaults for the developer tools that include this file directly; capi.cu declares its own)
 int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, const void* k, const void* v, int n_q,
-                     int n_kv, int d_h, float scale, void* o, float* lse, int lse_window) {
+                     int n_kv, int d_h, float scale, void* o, float* lse = nullptr, int lse_window = 0) {
     if (d_h != 128 && d_h != 64) {
         set_error("attention: head_dim must be 64 or 128 (got " + std::to_string(d_h) + ")");
         return QVK_E_UNSUPPORTED;

@@ -29,6 +29,9 @@ int env_knob(const char* name, int def) {
     return e ? atoi(e) : def;
 }
 cudaError_t func_attr(const void* f, cudaFuncAttribute a, int v) { return cudaFuncSetAttribute(f, a, v); }
+int launch_attention2(cudaStream_t, const qvk_groups*, const void*, const void*, const void*, int, int, float, void*) {
+    return QVK_E_UNSUPPORTED;
+}
 }
 
 __global__ void fill(__nv_bfloat16* p, size_t n, uint32_t seed) {
