@@ -66,5 +66,13 @@ wf = torch.randn(96, 96, device=dev)
 of = torch.empty(70, 96, device=dev)
 check(qp.lib.qvk_project_exact(torch.cuda.current_stream().cuda_stream, xf.data_ptr(), 70, 96, wf.data_ptr(), 96,
                                of.data_ptr()))
+# round 2, late: SnapKV windows of several operand blocks (two-pass and pass 2 alone), the attention's window
+# statistics, the pass-2 flat (item, key tile) split, the layer path with SnapKV pass 1 from the attention (PDL)
+qp.snapkv_scores(q, k, g, n_q, n_kv, 100, 3)
+_, st = qp.attention_window_stats(q, k, v, g, n_q, n_kv, 100)
+qp.snapkv_scores(q, k, g, n_q, n_kv, 100, 1, window_stats=st)
+_, st32 = qp.attention_window_stats(q, k, v, g, n_q, n_kv, 32)
+qp.snapkv_scores(q, k, g, n_q, n_kv, 32, 1, window_stats=st32)
+qp.prefill_layer(q, k, v, g, n_q, n_kv, rho, qp.Scorer.snapkv, True, snap_window=100, snap_pool=3)
 torch.cuda.synchronize()
 print("sanitize run ok")
