@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         ptx::mbar_init(&sh->q_empty, 1);
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(&sh->acc_full[b], 1);
-            ptx::mbar_init(&sh->acc_empty[b], kSnapCompute);
+            // pass 2 alone: a team of two compute sets (256 threads) per accumulator buffer
+            ptx::mbar_init(&sh->acc_empty[b], p.lse ? kSnapCompute / 2 : kSnapCompute);
         }
         for (int st = 0; st < kSnapStages; ++st) {
             ptx::mbar_init(&sh->kv_full[st], 1);
@@ -529,6 +530,89 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
             }
             ptx::named_bar_sync(1, kSnapCompute);
             }
+            // ---- pass 2 alone (window statistics given): two teams of two compute sets take alternate key tiles —
+            // team t the tiles of accumulator buffer t — so one team's TMEM loads and partial-sum exchange overlap
+            // the other team's exponentials (with all four sets on every tile, the sub-partition's four warps ran
+            // each tile's load / exponentials / exchange in lockstep: ~2200 cycles per tile for ~1344 of MUFU work).
+            // A set covers two slices of 8 kN8 window columns, loaded one after the other into the same registers.
+            if (p.lse) {
+                const int team = set >> 1, sub = set & 1;
+                const ptx::f2 sl2x2 = ptx::f2_make(sl2, sl2);
+                for (int jt = jt0; jt < jte; ++jt, ++acc_no) {
+                    if (static_cast<int>(acc_no & 1) != team) continue;
+                    ptx::mbar_wait(&sh->acc_full[team], (acc_no >> 1) & 1);
+                    ptx::tc_fence_after();
+                    const int j = jt * 128 + i;
+                    const bool edge = jt * 128 + 127 > n - p.window + b * p.wb;
+                    ptx::f2 a01 = ptx::f2_make(0.f, 0.f), a23 = a01;
+                    float x[8 * kN8];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const int c0 = (2 * sub + r) * 8 * kN8;
+#pragma unroll
+                        for (int c8 = 0; c8 < kN8; ++c8)
+                            QVK_TMEM_LD8F(tmem + lane_off + 256 * team + c0 + 8 * c8, (x + 8 * c8));
+                        ptx::tmem_ld_wait();
+                        if (r == 1) {  // both slices read: the MMA may refill this buffer
+                            ptx::tc_fence_before();
+                            ptx::mbar_arrive(&sh->acc_empty[team]);
+                        }
+                        const float4* b4 = reinterpret_cast<const float4*>(sh->bias + c0);
+                        const int4* p4 = reinterpret_cast<const int4*>(sh->pos + c0);
+                        auto col4 = [&](const float* xq, const float4 bb, const int4* pp, bool poly01, bool poly23) {
+                            float y0, y1, y2, y3;
+                            ptx::f2_split(ptx::f2_fma(ptx::f2_make(xq[0], xq[1]), sl2x2, ptx::f2_make(bb.x, bb.y)),
+                                          y0, y1);
+                            ptx::f2_split(ptx::f2_fma(ptx::f2_make(xq[2], xq[3]), sl2x2, ptx::f2_make(bb.z, bb.w)),
+                                          y2, y3);
+                            if (pp) {
+                                const int4 pv = *pp;
+                                if (j > pv.x) y0 = -INFINITY;
+                                if (j > pv.y) y1 = -INFINITY;
+                                if (j > pv.z) y2 = -INFINITY;
+                                if (j > pv.w) y3 = -INFINITY;
+                            }
+                            if (poly01) {
+                                ptx::ex2_poly2(y0, y1);
+                            } else {
+                                y0 = ptx::ex2(y0);
+                                y1 = ptx::ex2(y1);
+                            }
+                            if (poly23) {
+                                ptx::ex2_poly2(y2, y3);
+                            } else {
+                                y2 = ptx::ex2(y2);
+                                y3 = ptx::ex2(y3);
+                            }
+                            a01 = ptx::f2_add(a01, ptx::f2_make(y0, y1));
+                            a23 = ptx::f2_add(a23, ptx::f2_make(y2, y3));
+                        };
+                        if (edge) {
+#pragma unroll
+                            for (int e4 = 0; e4 < 2 * kN8; ++e4)
+                                col4(x + 4 * e4, b4[e4], p4 + e4, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
+                        } else {
+#pragma unroll
+                            for (int e4 = 0; e4 < 2 * kN8; ++e4)
+                                col4(x + 4 * e4, b4[e4], nullptr, kSnapPoly(2 * e4), kSnapPoly(2 * e4 + 1));
+                        }
+                    }
+                    float a4[4];
+                    ptx::f2_split(a01, a4[0], a4[1]);
+                    ptx::f2_split(a23, a4[2], a4[3]);
+                    const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+                    const uint32_t tp = (acc_no >> 1) & 1;  // the team's tile parity: part[] double-buffered
+                    if (sub) sh->part[tp][team][i] = acc;
+                    ptx::named_bar_sync(2 + 4 * team + quarter, 64);  // the two sets of this team and lane quarter
+                    if (!sub && j < n) {
+                        const float tot = acc + sh->part[tp][team][i];
+                        const int64_t e = p.n_kv * t0 + static_cast<int64_t>(hk) * n + j;
+                        const float t = b ? tot + (p.out ? static_cast<float>(p.out[e]) : p.raw[e]) : tot;
+                        if (p.out) p.out[e] = static_cast<double>(t);
+                        else p.raw[e] = t;
+                    }
+                }
+            } else
             // ---- pass 2: key j = jt*128 + i, window columns [col0, col0 + 8 n8) ----
             for (int jt = jt0; jt < jte; ++jt, ++acc_no) {
                 wait_acc();

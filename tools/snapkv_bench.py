@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """SnapKV scorer microbenchmark (GPU): qvk_snapkv_score on the C3 shape (64 groups x 1024 tokens, 28 / 4 heads,
-window 32) and C3b (64 x 4096), CUDA-event timed per launch after an L2 flush; one JSON line per shape."""
+window 32) and C3b (64 x 4096), CUDA-event timed per launch after an L2 flush; one JSON line per shape.
+QVK_BENCH_DRAIN=1: a ~100 us sleep kernel between the flush and the timed launch, so the flush's dirty L2 lines are
+written back (and the launch is queued) before the first event — the kernel alone instead of kernel + write-back."""
 import json
+import os
 import statistics
 import sys
 from pathlib import Path
@@ -13,6 +16,7 @@ import paper_2505_16175_b200 as qp  # noqa: E402
 
 dev = torch.device("cuda:0")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+drain = os.environ.get("QVK_BENCH_DRAIN") == "1"
 for G, N in ((64, 1024), (64, 4096)):
     plan = qp.GroupPlan.from_sizes([N] * G, 0.25)
     g = plan.to(dev)
@@ -23,6 +27,8 @@ for G, N in ((64, 1024), (64, 4096)):
     ts = []
     for _ in range(20):
         flush.zero_()
+        if drain:
+            torch.cuda._sleep(200_000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         qp.snapkv_scores(q, k, g, 28, 4, 32, out=sc)
@@ -35,6 +41,8 @@ for G, N in ((64, 1024), (64, 4096)):
     ts2 = []
     for _ in range(20):
         flush.zero_()
+        if drain:
+            torch.cuda._sleep(200_000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         qp.snapkv_scores(q, k, g, 28, 4, 32, out=sc, window_stats=st)
