@@ -198,6 +198,7 @@ constexpr size_t kSnapSmem = 1024 + 2 * kSnapQChunk + kSnapStages * kSnapKTile +
 //   [3..5] warp 0 (set 0, quarter 0) lane 0: acc_full seen, accumulator released, tile's math done
 //   [6..8] the same for warp 13 (set 3, quarter 1)
 __device__ long long g_snap_trace[2][64][10];
+__device__ unsigned long long g_snap_span[3];  // globaltimer: earliest CTA start, latest CTA end, CTA 0's first tile
 #define QVK_ST(item_no, tile, slot)                                                       \
     do {                                                                                  \
         if (blockIdx.x == 0 && (item_no) < 2 && (tile) < 64) {                            \
@@ -284,6 +285,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
     SnapShared* sh = reinterpret_cast<SnapShared*>(sK + kSnapStages * kSnapKTile);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int items = p.n_groups * p.n_kv;
+#ifdef QVK_SNAP_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long g0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+        atomicMin(&g_snap_span[0], g0);
+    }
+#endif
 
     if (threadIdx.x == 0) {
         ptx::mbar_init(&sh->q_full, 1);
@@ -708,6 +716,13 @@ __global__ void __launch_bounds__(kSnapThreads, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512>(tmem);
     }
+#ifdef QVK_SNAP_TRACE
+    if (threadIdx.x == 0) {
+        unsigned long long g1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+        atomicMax(&g_snap_span[1], g1);
+    }
+#endif
 }
 
 bool snap_map(CUtensorMap* m, const void* base, int heads, int64_t tokens, uint32_t box_heads, uint32_t box_rows) {

@@ -59,20 +59,35 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int it = 0; it < 3; ++it) qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc, nullptr, 0);
+    // argv[3] == "p2": pass 2 alone on (arbitrary, finite) window statistics, as the layer path runs it
+    const bool p2 = argc > 3 && std::string(argv[3]) == "p2";
+    float* lse = nullptr;
+    if (p2) {
+        cudaMalloc(&lse, sizeof(float) * G * nq * 32);
+        cudaMemset(lse, 0, sizeof(float) * G * nq * 32);
+    }
+    for (int it = 0; it < 3; ++it) qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc, lse, 0);
     static long long zero[2][64][10];
     cudaMemcpyToSymbol(qvk::g_snap_trace, zero, sizeof(zero));
     float best = 1e9;
     for (int it = 0; it < 5; ++it) {
+        unsigned long long span0[3] = {~0ull, 0ull, 0ull};
+        cudaMemcpyToSymbol(qvk::g_snap_span, span0, sizeof(span0));
         cudaEventRecord(e0);
-        qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc, nullptr, 0);
+        qvk::launch_snapkv(0, &grp, q, k, nq, nkv, d, 32, 1, 0.0883883f, sc, lse, 0);
         cudaEventRecord(e1);
         cudaDeviceSynchronize();
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         best = std::min(best, ms);
     }
-    printf("G=%d N=%d err=%s  best of 5: %.1f us\n", G, N, cudaGetErrorString(cudaGetLastError()), best * 1e3);
+    printf("G=%d N=%d %s err=%s  best of 5: %.1f us\n", G, N, p2 ? "pass 2 alone" : "two passes",
+           cudaGetErrorString(cudaGetLastError()), best * 1e3);
+    {
+        unsigned long long span[3];
+        cudaMemcpyFromSymbol(span, qvk::g_snap_span, sizeof(span));
+        printf("last launch: CTAs from first start to last end %.1f us\n", (span[1] - span[0]) * 1e-3);
+    }
     static long long tr[2][64][10];
     cudaMemcpyFromSymbol(tr, qvk::g_snap_trace, sizeof(tr));
     const long long t0 = tr[0][0][0];
