@@ -758,17 +758,17 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     const int sms = sm_count();
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
     // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 2 | 4 | 6;
-    // DESIGN.md §3.1).
+    // DESIGN.md §3.1): 2 and 4 are equal at boost clocks, 2 is ~0.5 % ahead inside the power-capped C4 step.
     static const int poly = [] {
-        const int v = env_knob("QVK_ATTN_POLY", 4);
-        return (v == 0 || v == 2 || v == 6) ? v : 4;
+        const int v = env_knob("QVK_ATTN_POLY", 2);
+        return (v == 0 || v == 4 || v == 6) ? v : 2;
     }();
     if (d_h == 128) {
         switch (poly) {
             case 0: return launch_attention_d<128, 0>(stream, mq, mk, mv, mo, prm, grid);
-            case 2: return launch_attention_d<128, 2>(stream, mq, mk, mv, mo, prm, grid);
+            case 4: return launch_attention_d<128, 4>(stream, mq, mk, mv, mo, prm, grid);
             case 6: return launch_attention_d<128, 6>(stream, mq, mk, mv, mo, prm, grid);
-            default: return launch_attention_d<128, 4>(stream, mq, mk, mv, mo, prm, grid);
+            default: return launch_attention_d<128, 2>(stream, mq, mk, mv, mo, prm, grid);
         }
     }
     return poly ? launch_attention_d<64, 4>(stream, mq, mk, mv, mo, prm, grid)
