@@ -117,6 +117,91 @@ __device__ __forceinline__ void store_tile(const ProjParams& p, uint32_t acc, in
     }
 }
 
+// The same epilogue with coalesced output: each 64-column chunk of the CTA's 128 x 256 accumulator is staged as bf16
+// in shared memory (128-byte swizzle, one row per thread) and written by ONE TMA store (16 KB) into the Q, K or V
+// tensor it belongs to (64-column chunks never straddle them) — instead of 16-byte per-thread stores, 32 rows per warp
+// instruction, which cost two L2 write operations per sector and twice the instructions (ncu vs cuBLAS on the C4
+// layer shape).  Two staging buffers: a buffer is rewritten only after its previous store has read it.  Rows past the
+// last token are clipped by the TMA.  Named barrier 1 = the 128 epilogue threads.
+__device__ __forceinline__ void store_tile_staged(const ProjParams& p, uint32_t acc, int64_t m0, int row, int nt,
+                                                  uint32_t acc_empty, bool remote, uint8_t* stage, uint32_t& n_chunk,
+                                                  const CUtensorMap* tm_q, const CUtensorMap* tm_k,
+                                                  const CUtensorMap* tm_v, bool leader) {
+    const int64_t m = m0 + row;
+    const bool live = m < p.m;
+    double ss = 0.0;
+#pragma unroll 1
+    for (int c2 = 0; c2 < kBN / 64; ++c2, ++n_chunk) {
+        const uint32_t buf = n_chunk & 1;
+        if (n_chunk >= 2) {  // this buffer's previous store must have read it
+            if (leader) ptx::bulk_wait_group_read<1>();
+            ptx::named_bar_sync(1, 128);
+        }
+        uint8_t* sb = stage + buf * (128 * 128);
+        const uint32_t rbase = ptx::smem_u32(sb) + row * 128;
+        const int col64 = nt * kBN + 64 * c2;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            const int c = 2 * c2 + h;
+            float x[32];
+            QVK_TMEM_LD32F(acc + 32 * c, x);
+            ptx::tmem_ld_wait();
+            if (c == kBN / 32 - 1) {  // accumulator fully read: the MMA warp may reuse it
+                ptx::tc_fence_before();
+                if (remote)
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc_empty) : "memory");
+                else
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acc_empty) : "memory");
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[e] = ptx::pack_bf16(x[2 * e], x[2 * e + 1]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t u = static_cast<uint32_t>(4 * h + q);  // 16-byte unit of the 128-byte staged row
+                ptx::sts128(rbase + ((u ^ (row & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
+            const int col = col64 + 32 * h;
+            if (p.scores && live && col >= p.q_cols && col < p.q_cols + p.kv_cols) {
+                const int kcol = col - p.q_cols;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const double lo = static_cast<double>(__uint_as_float(pk[e] << 16));
+                    const double hi = static_cast<double>(__uint_as_float(pk[e] & 0xffff0000u));
+                    ss = __fma_rn(lo, lo, ss);
+                    ss = __fma_rn(hi, hi, ss);
+                }
+                if ((kcol + 32) % p.d_h == 0) {
+                    const int hh = kcol / p.d_h;
+                    const int g = find_group_fast(p.tok_off, p.n_groups, m, p.max_tokens);
+                    const int64_t t0 = __ldg(p.tok_off + g);
+                    const int64_t n = __ldg(p.tok_off + g + 1) - t0;
+                    p.scores[p.n_kv * t0 + hh * n + (m - t0)] = -__dsqrt_rn(ss);
+                    ss = 0.0;
+                }
+            }
+        }
+        ptx::fence_proxy_async_smem();  // generic st.shared -> the TMA engine
+        ptx::named_bar_sync(1, 128);
+        if (leader) {
+            const CUtensorMap* tm;
+            int cc;
+            if (col64 < p.q_cols) {
+                tm = tm_q;
+                cc = col64;
+            } else if (col64 < p.q_cols + p.kv_cols) {
+                tm = tm_k;
+                cc = col64 - p.q_cols;
+            } else {
+                tm = tm_v;
+                cc = col64 - p.q_cols - p.kv_cols;
+            }
+            ptx::tma_store_2d(tm, sb, cc, static_cast<int>(m0));
+            ptx::bulk_commit_group();
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     project_qkv_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                        const ProjParams p) {
@@ -225,7 +310,9 @@ struct ProjBarriers2 {
     uint64_t acc_full[2], acc_empty[2];
     uint32_t tmem_base;
 };
-constexpr size_t kSmem2 = 1024 + kStages2 * kStage2 + sizeof(ProjBarriers2);
+constexpr uint32_t kStageOut = 2 * 128 * 128;  // two 128-row x 128-byte bf16 staging buffers of the epilogue
+constexpr size_t kSmem2 = 1024 + kStages2 * kStage2 + kStageOut + sizeof(ProjBarriers2);
+static_assert(kSmem2 <= 232448, "project: 2-SM kernel shared memory above 227 KB");
 
 __device__ __forceinline__ uint32_t cta_rank_in_cluster() {
     uint32_t r;
@@ -243,10 +330,13 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 __global__ void __launch_bounds__(kThreads, 1)
     project_qkv_2sm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                           const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v,
                            const ProjParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    ProjBarriers2* bar = reinterpret_cast<ProjBarriers2*>(smem + kStages2 * kStage2);
+    uint8_t* stage_out = smem + kStages2 * kStage2;  // 1024-aligned (SWIZZLE_128B staging of the epilogue)
+    ProjBarriers2* bar = reinterpret_cast<ProjBarriers2*>(stage_out + kStageOut);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cta_rank_in_cluster();
     const bool leader = rank == 0;
@@ -347,16 +437,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-        uint32_t n_acc = 0;
+        uint32_t n_acc = 0, n_chunk = 0;
+        const bool out_leader = warp == 2 && lane == 0;  // issues the epilogue's TMA stores
+        if (out_leader) {
+            ptx::prefetch_tmap(&tm_q);
+            ptx::prefetch_tmap(&tm_k);
+            ptx::prefetch_tmap(&tm_v);
+        }
         for (int tile = pair; tile < tiles; tile += pairs, ++n_acc) {
             const int mt = tile / n_tiles, nt = tile - mt * n_tiles;
             const uint32_t b = n_acc & 1;
             ptx::mbar_wait(&bar->acc_full[b], (n_acc >> 1) & 1);
             ptx::tc_fence_after();
-            const int64_t m = static_cast<int64_t>(mt) * 2 * kBM + static_cast<int64_t>(rank) * kBM + row;
-            store_tile(p, tmem + lane_off + b * kBN, m, nt, map_to_cta(ptx::smem_u32(&bar->acc_empty[b]), 0),
-                       true);
+            const int64_t m0 = static_cast<int64_t>(mt) * 2 * kBM + static_cast<int64_t>(rank) * kBM;
+            store_tile_staged(p, tmem + lane_off + b * kBN, m0, row, nt,
+                              map_to_cta(ptx::smem_u32(&bar->acc_empty[b]), 0), true, stage_out, n_chunk, &tm_q,
+                              &tm_k, &tm_v, out_leader);
         }
+        if (out_leader) ptx::bulk_wait_group<0>();  // every output store complete before the CTA retires
     }
     ptx::tc_fence_before();
     cluster_sync_all();  // both CTAs done with TMEM (and with the leader's barriers)
@@ -375,6 +473,18 @@ bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int cols, int b
     cuuint32_t estr[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_map_out(CUtensorMap* m, const void* base, int64_t rows, int cols) {
+    const auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
+    if (!enc) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(kBM)};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -441,7 +551,13 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, project_qkv_2sm_kernel, mx, mw2, p));
+        CUtensorMap mq, mk, mv;  // outputs: boxes of 64 columns x 128 rows (one staged chunk)
+        if (!make_map_out(&mq, q, tokens, p.q_cols) || !make_map_out(&mk, k, tokens, p.kv_cols) ||
+            !make_map_out(&mv, v, tokens, p.kv_cols)) {
+            set_error("project: cuTensorMapEncodeTiled failed");
+            return QVK_E_CUDA;
+        }
+        QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, project_qkv_2sm_kernel, mx, mw2, mq, mk, mv, p));
         return QVK_OK;
     }
     const int64_t tiles = ((tokens + kBM - 1) / kBM) * (n / kBN);
