@@ -11,6 +11,8 @@ key-norm per KV head at rho 0.5 (the exact launch bench.py times 28 times per st
 C3b: 64 groups x 4096 tokens with the SnapKV scorer at rho 0.25 — scores of 3 sampled groups within rel 1e-4 of the
 fp64 restatement, index sets equal except for documented near-ties (an index may differ only when its oracle score
 lies within the tie band of the oracle's k-th score; the count is asserted small and printed).
+C3: 64 groups x 1024 tokens with SnapKV through the layer path (window statistics from the attention), W = 32 and a
+two-block W = 64 with pooling — same checks.
 """
 import math
 
@@ -131,4 +133,34 @@ def test_c3b_launch_shape_snapkv(cuda):
             total_diff += diff
             total_rows += kk
     print(f"C3b SnapKV: {total_diff} near-tie index differences over {total_rows} retained rows")
+    assert total_diff <= 0.01 * total_rows
+
+
+@pytest.mark.parametrize("window,pool", [(32, 1), (64, 3)])
+def test_c3_launch_shape_snapkv_layer(cuda, window, pool):
+    """C3's launch shape (64 groups x 1024 tokens, SnapKV, rho 0.25) through qvk_prefill_layer: pass 1 from the
+    attention kernel's window statistics, pass 2 (flat tile split, two teams) launched with PDL behind it, then the
+    fused select + gather.  W = 32 is the default one-block window; W = 64 at GQA 7 is two operand blocks with
+    pooling.  Every group structurally, 3 sampled groups against the fp64 restatement (rel 1e-4, near-tie band)."""
+    plan, sizes, q, k, v = _c4_like(1024, 64, 16, 0.25, cuda)
+    assert plan.n_groups == 64 and sizes[0] == 1024
+    g = plan.to(cuda)
+    buf = qp.prefill_layer(q, k, v, g, N_Q, N_KV, 0.25, qp.Scorer.snapkv, True, snap_window=window, snap_pool=pool)
+    torch.cuda.synchronize()
+    _device_structure(plan, k, v, buf, N_KV, D)
+    scale = 1 / math.sqrt(D)
+    total_diff = total_rows = 0
+    for gi in (0, 31, 63):
+        t0, n, r0, kk = int(plan.tok_off[gi]), sizes[gi], int(plan.row_off[gi]), int(plan.keep[gi])
+        qf, kf = (x[t0:t0 + n].float().cpu().numpy() for x in (q, k))
+        want = O.snapkv_scores(qf, kf, N_Q, N_KV, D, window, pool, scale)
+        got = buf.scores[N_KV * t0: N_KV * (t0 + n)].cpu().numpy().reshape(N_KV, n)
+        np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-7)
+        idx = buf.idx[r0 * N_KV:(r0 + kk) * N_KV].view(kk, N_KV).cpu().numpy()
+        for h in range(N_KV):
+            diff, allowed = _near_tie_mismatches(idx[:, h], want[h], kk, 1e-4)
+            assert diff == allowed, f"group {gi} head {h}: {diff - allowed} index differences outside the tie band"
+            total_diff += diff
+            total_rows += kk
+    print(f"C3 SnapKV W={window} pool={pool}: {total_diff} near-tie index differences over {total_rows} rows")
     assert total_diff <= 0.01 * total_rows
