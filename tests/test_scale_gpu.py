@@ -13,6 +13,9 @@ fp64 restatement, index sets equal except for documented near-ties (an index may
 lies within the tie band of the oracle's k-th score; the count is asserted small and printed).
 C3: 64 groups x 1024 tokens with SnapKV through the layer path (window statistics from the attention), W = 32 and a
 two-block W = 64 with pooling — same checks.
+C5: the sweep's extremes through the layer path — 64-frame groups (16384 tokens) at rho 0.125, 4-frame groups at rho 1
+(the identity), value norm per token at rho 0.25 — attention rows, scores / index sets / caches bit-exact.
+C2: attention_score (GQA text query) at C2's shape, scores bit-exact against the reference's own dot product.
 """
 import math
 
@@ -44,22 +47,23 @@ def _device_structure(plan, k, v, buf, heads, width):
     idx = buf.idx[: G * kk * heads].view(G, kk, heads).long()
     assert bool((idx[:, 1:] > idx[:, :-1]).all()), "indices not ascending"
     assert bool((idx >= 0).all()) and bool((idx < n).all())
-    sc = buf.scores[: G * heads * n].view(G, heads, n)
-    # top-k under (score desc, index asc): every retained score >= every dropped one, ties broken by index
-    kept = torch.zeros(G, heads, n, dtype=torch.bool, device=dev)
-    kept.scatter_(2, idx.permute(0, 2, 1), True)
-    s = sc.clone()
-    s[s == 0] = 0.0  # -0.0 == +0.0
-    min_kept = torch.where(kept, s, torch.full_like(s, float("inf"))).amin(2)
-    max_drop = torch.where(~kept, s, torch.full_like(s, float("-inf"))).amax(2)
-    assert bool((min_kept >= max_drop).all()), "a dropped score beats a retained one"
-    tie = min_kept == max_drop
-    if bool(tie.any()):  # at an exact tie the lower index must be the retained one
-        pos = torch.arange(n, device=dev).expand(G, heads, n)
-        at = s == min_kept.unsqueeze(2)
-        last_kept = torch.where(kept & at, pos, torch.full_like(pos, -1)).amax(2)
-        first_drop = torch.where(~kept & at, pos, torch.full_like(pos, n)).amin(2)
-        assert bool(((last_kept < first_drop) | ~tie).all()), "tie broken against the index order"
+    if kk < n:  # (kk == n: rho 1, the identity — every index retained, nothing scored)
+        sc = buf.scores[: G * heads * n].view(G, heads, n)
+        # top-k under (score desc, index asc): every retained score >= every dropped one, ties broken by index
+        kept = torch.zeros(G, heads, n, dtype=torch.bool, device=dev)
+        kept.scatter_(2, idx.permute(0, 2, 1), True)
+        s = sc.clone()
+        s[s == 0] = 0.0  # -0.0 == +0.0
+        min_kept = torch.where(kept, s, torch.full_like(s, float("inf"))).amin(2)
+        max_drop = torch.where(~kept, s, torch.full_like(s, float("-inf"))).amax(2)
+        assert bool((min_kept >= max_drop).all()), "a dropped score beats a retained one"
+        tie = min_kept == max_drop
+        if bool(tie.any()):  # at an exact tie the lower index must be the retained one
+            pos = torch.arange(n, device=dev).expand(G, heads, n)
+            at = s == min_kept.unsqueeze(2)
+            last_kept = torch.where(kept & at, pos, torch.full_like(pos, -1)).amax(2)
+            first_drop = torch.where(~kept & at, pos, torch.full_like(pos, n)).amin(2)
+            assert bool(((last_kept < first_drop) | ~tie).all()), "tie broken against the index order"
     t0 = torch.from_numpy(plan.tok_off[:-1]).to(dev).view(G, 1, 1)
     src = (t0 + idx) * heads + torch.arange(heads, device=dev).view(1, 1, heads)  # source (token, head) unit
     kr = k.view(-1, width)[src.view(-1)]
@@ -164,3 +168,73 @@ def test_c3_launch_shape_snapkv_layer(cuda, window, pool):
             total_rows += kk
     print(f"C3 SnapKV W={window} pool={pool}: {total_diff} near-tie index differences over {total_rows} rows")
     assert total_diff <= 0.01 * total_rows
+
+
+@pytest.mark.parametrize("fpg,rho,scorer,per_head", [
+    (64, 0.125, qp.Scorer.key_norm_small, True),   # C5's largest group (16384 tokens) at its smallest rho
+    (4, 1.0, qp.Scorer.key_norm_small, True),      # C5's smallest group, no pruning (every row retained)
+    (16, 0.25, qp.Scorer.value_norm, False),       # value norm over the flattened n_kv*d row (per-token select)
+])
+def test_c5_sweep_launch_shapes(cuda, fpg, rho, scorer, per_head):
+    """C5 (retention-ratio / group-size sweep) launch shapes through qvk_prefill_layer at 1024 frames x 256 tokens:
+    every group structurally (per-head modes), 3 sampled groups' attention rows against the fp64 restatement and
+    their scores / index sets / cache rows bit-exact against the oracle."""
+    plan, sizes, q, k, v = _c4_like(1024, 256, fpg, rho, cuda)
+    assert plan.n_groups == 1024 // fpg
+    g = plan.to(cuda)
+    buf = qp.prefill_layer(q, k, v, g, N_Q, N_KV, rho, scorer, per_head)
+    torch.cuda.synchronize()
+    heads, width = (N_KV, D) if per_head else (1, N_KV * D)
+    if per_head:
+        _device_structure(plan, k, v, buf, heads, width)
+    scale = 1 / math.sqrt(D)
+    G = plan.n_groups
+    for gi in (0, G // 2, G - 1):
+        t0, n, r0, kk = int(plan.tok_off[gi]), sizes[gi], int(plan.row_off[gi]), int(plan.keep[gi])
+        qf, kf, vf = (x[t0:t0 + n].float().cpu().numpy() for x in (q, k, v))
+        got = buf.o[t0:t0 + n].float().cpu().numpy()
+        for begin, step in ((5, max(97, n // 16)), (n - 1, n)):
+            want, _ = O.attention_rows(qf, kf, vf, N_Q, N_KV, D, scale, begin, step)
+            sel = np.arange(begin, n, step)
+            err = np.abs(got[sel] - want[sel])
+            assert (err <= 1e-2 + 1e-2 * np.abs(want[sel])).all(), f"group {gi}: attention error {err.max():.3e}"
+        src = kf if scorer == qp.Scorer.key_norm_small else vf
+        sc = O.score_norm(src, heads, width, scorer == qp.Scorer.key_norm_small)
+        if rho < 1.0:  # rho == 1 is the identity without scoring (prefill.cpp:263-270): no scores to compare
+            got_sc = buf.scores[heads * t0: heads * (t0 + n)].cpu().numpy().reshape(heads, n)
+            assert np.array_equal(got_sc.view(np.uint64), sc.view(np.uint64)), f"group {gi}: scores"
+        want_idx = O.select_heads(sc, n, heads, kk)
+        idx = buf.idx[r0 * heads:(r0 + kk) * heads].view(kk, heads).cpu().numpy()
+        assert np.array_equal(idx, want_idx), f"group {gi}: retained index sets"
+        kc = buf.k_cache.view(-1, heads, width)[r0:r0 + kk].float().cpu().numpy()
+        vc = buf.v_cache.view(-1, heads, width)[r0:r0 + kk].float().cpu().numpy()
+        assert np.array_equal(kc, O.gather_heads(kf, heads, width, want_idx)), f"group {gi}: K cache"
+        assert np.array_equal(vc, O.gather_heads(vf, heads, width, want_idx)), f"group {gi}: V cache"
+        org = buf.origin.view(-1, heads)[r0:r0 + kk].cpu().numpy()
+        assert np.array_equal(org, want_idx.astype(np.int64) + t0), f"group {gi}: origin"
+        if rho == 1.0:
+            assert kk == n and np.array_equal(want_idx[:, 0], np.arange(n))
+
+
+def test_c2_launch_shape_attention_score(cuda):
+    """C2's shape (256 frames x 256 tokens, 16-frame groups) with the attention_score scorer (GQA text query, 64 text
+    tokens) at rho 0.5: 3 sampled groups' scores bit-exact against the reference's own sequential dot product on the
+    pre-summed query, index sets / cache rows / origins against the oracle; every group structurally."""
+    plan, sizes, q, k, v = _c4_like(256, 256, 16, 0.5, cuda)
+    gen = torch.Generator().manual_seed(11)
+    T = 64
+    tq = (torch.randn(T, N_Q, D, generator=gen) * 0.5).to(cuda)
+    g = plan.to(cuda)
+    buf = qp.prefill_layer(q, k, v, g, N_Q, N_KV, 0.5, qp.Scorer.attention_score, True, text_query=tq)
+    torch.cuda.synchronize()
+    _device_structure(plan, k, v, buf, N_KV, D)
+    qbar = O.text_query_sum(tq.cpu().numpy(), N_Q, N_KV, D)
+    for gi in (0, 7, plan.n_groups - 1):
+        t0, n, r0, kk = int(plan.tok_off[gi]), sizes[gi], int(plan.row_off[gi]), int(plan.keep[gi])
+        kf = k[t0:t0 + n].float().cpu().numpy()
+        sc = O.score_text_ref(kf, n, N_Q, N_KV, D, True, qbar, T)
+        got_sc = buf.scores[N_KV * t0: N_KV * (t0 + n)].cpu().numpy().reshape(N_KV, n)
+        assert np.array_equal(got_sc.view(np.uint64), sc.view(np.uint64)), f"group {gi}: scores"
+        want_idx = O.select_heads(sc, n, N_KV, kk)
+        idx = buf.idx[r0 * N_KV:(r0 + kk) * N_KV].view(kk, N_KV).cpu().numpy()
+        assert np.array_equal(idx, want_idx), f"group {gi}: retained index sets"
