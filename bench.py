@@ -454,6 +454,8 @@ def main():
         ag_report = {"allgather_ms_alone": ag_ms, "compute_ms_alone": comp_ms, "step_ms": step_ms,
                      "exposed_ms": exposed, "hidden_frac": (1.0 - exposed / ag_ms) if ag_ms > 0 else None,
                      "bytes_received_per_rank_per_step": recv,
+                     "nccl_ctas_and_reserved_sms": (int(os.environ.get("QVK_COMM_CTAS", "8"))
+                                                    if comm is not None and world > 1 else 0),
                      "collective": "qvk_allgather_layer (NCCL, C ABI)" if comm is not None else
                                    "torch.distributed broadcasts (gloo, shared-GPU test mode)",
                      "note": "exposed = step - compute-only step (max over ranks); layer l's all-gather runs on a "

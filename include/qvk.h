@@ -264,7 +264,10 @@ int qvk_prefill_layer_dests(qvk_stream_t stream, const qvk_groups* groups, const
  * the first cache row of each rank's segment (row_off[rank_begin[r]]).  k/v caches hold heads * width bf16 per
  * row, origin heads uint64 per row (may be NULL).  Stream-ordered on `stream`.
  *   qvk_comm_unique_id   rank 0 creates the 128-byte ncclUniqueId; the caller ships it to the other ranks
- *   qvk_comm_init        one rank per process on the current device (ncclCommInitRank)
+ *   qvk_comm_init        one rank per process on the current device (ncclCommInitRankConfig); for world > 1 NCCL
+ *                        is capped at QVK_COMM_CTAS CTAs (default 8, world 1: 0; 0 = NCCL's choice) and as many SMs are
+ *                        reserved (qvk_reserve_sms) until qvk_comm_destroy, so the persistent kernels never wait
+ *                        for SMs held by an all-gather overlapping them
  *   qvk_comm_init_all    one process driving n_dev GPUs (ncclCommInitAll): comms_out[i] drives devices[i]; wrap
  *                        the per-device calls in qvk_comm_group_start / qvk_comm_group_end
  *   qvk_comm_wrap        adopt a caller's ncclComm_t (not destroyed by qvk_comm_destroy)
@@ -281,6 +284,10 @@ int qvk_comm_group_start(void);
 int qvk_comm_group_end(void);
 int qvk_allgather_layer(qvk_stream_t stream, qvk_comm_t comm, const int64_t* rank_row_begin, int32_t heads,
                         int32_t width, void* k_cache_d, void* v_cache_d, uint64_t* origin_d);
+/* SMs the persistent kernels (attention, projection: one CTA per SM walking a static work list) leave free for
+ * kernels running beside them on other streams — a collective, a decoder.  Their grids become SM count - n (>= 2).
+ * Results do not depend on it.  0 <= n < SM count; returns the previous value in *previous (may be NULL). */
+int qvk_reserve_sms(int32_t n, int32_t* previous);
 
 /* ---- diagnostics ------------------------------------------------------------------------------------------------ */
 /* Route the last qvk_prune / qvk_prefill_layer* call of this thread took for its prune step: 0 = fused cluster

@@ -26,6 +26,7 @@ if not _BUILDING:
         gather,
         group_count,
         last_prune_route,
+        reserve_sms,
         prefill_layer,
         prefill_layer_dests,
         prefill_layer_x,

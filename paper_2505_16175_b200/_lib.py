@@ -80,6 +80,7 @@ _SIGS = {
     "qvk_comm_group_end": (C.c_int, []),
     "qvk_allgather_layer": (C.c_int, [P, P, P, I32, I32, P, P, P]),
     "qvk_last_prune_route": (C.c_int, []),
+    "qvk_reserve_sms": (C.c_int, [C.c_int32, C.POINTER(C.c_int32)]),
     "qvk_ctx_create": (C.c_int, [C.POINTER(P), C.POINTER(QvkLayerParams), I32, P, P]),
     "qvk_ctx_groups": (C.c_int, [P, GP]),
     "qvk_ctx_prefill_layer": (C.c_int, [P, P, P, P, P, P, P, P, P]),

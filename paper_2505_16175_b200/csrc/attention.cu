@@ -755,7 +755,7 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     const int64_t units = static_cast<int64_t>((prm.tiles_max + 1) / 2) * g->n_groups * n_q;
     if (units > 0x7fffffff) QVK_INVALID("attention: too many work units");
     prm.total_units = static_cast<int>(units);
-    const int sms = sm_count();
+    const int sms = grid_sms();
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
     // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 2 | 4 | 6;
     // DESIGN.md §3.1): 2 and 4 are equal at boost clocks, 2 is ~0.5 % ahead inside the power-capped C4 step.

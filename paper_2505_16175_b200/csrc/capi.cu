@@ -3,6 +3,7 @@
 // attention.cu, snapkv.cu, exact.cu).  No computation of the path happens on the host.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
@@ -83,6 +84,31 @@ int sm_count() {
     }();
     return n;
 }
+
+// SMs the persistent kernels (attention, projection) leave free for work running beside them — the N > 1
+// all-gather's NCCL CTAs (qvk_comm_init caps NCCL at QVK_COMM_CTAS CTAs and reserves as many SMs).  A persistent
+// grid of one CTA per SM walks a static unit list, so a CTA that has to wait for an SM held by a collective delays
+// the whole launch by the collective's duration; with the reservation it never waits.
+std::atomic<int> g_reserved_sms{0};
+
+int grid_sms() {
+    const int n = sm_count() - g_reserved_sms.load(std::memory_order_relaxed);
+    return n < 2 ? 2 : n;
+}
+
+}  // namespace qvk
+
+extern "C" int qvk_reserve_sms(int32_t n, int32_t* previous) {
+    if (n < 0 || n >= qvk::sm_count()) {
+        qvk::set_error("reserve_sms: n must be in [0, SM count)");
+        return QVK_E_INVALID;
+    }
+    const int old = qvk::g_reserved_sms.exchange(n);
+    if (previous) *previous = old;
+    return QVK_OK;
+}
+
+namespace qvk {
 
 int env_knob(const char* name, int def) {
     const char* e = std::getenv(name);

@@ -6,6 +6,7 @@
 // torch bundles (nvidia/nccl, 2.28) so a torch process loads one NCCL runtime.
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -16,6 +17,7 @@ struct qvk_comm_st {
     ncclComm_t comm = nullptr;
     bool owned = true;
     int rank = 0, world = 1;
+    int reserved = 0;  // SMs this communicator reserved (qvk_reserve_sms), released by qvk_comm_destroy
 };
 
 namespace qvk {
@@ -114,13 +116,22 @@ int qvk_comm_init(qvk_comm_t* out, int32_t world, int32_t rank, const void* uniq
     ncclUniqueId id;
     std::memcpy(&id, unique_id, sizeof(id));
     auto* c = new qvk_comm_st;
-    const ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    // world 1 has nothing to overlap: no cap unless QVK_COMM_CTAS is set explicitly (the test hook)
+    const int ctas = std::max(0, qvk::env_knob("QVK_COMM_CTAS", world > 1 ? 8 : 0));
+    if (ctas > 0) cfg.maxCTAs = ctas;
+    const ncclResult_t r = ncclCommInitRankConfig(&c->comm, world, id, rank, &cfg);
     if (r != ncclSuccess) {
         delete c;
-        return nccl_fail(r, "ncclCommInitRank");
+        return nccl_fail(r, "ncclCommInitRankConfig");
     }
     c->rank = rank;
     c->world = world;
+    if (ctas > 0 && ctas < qvk::sm_count() - 2) {  // the all-gather's CTAs get SMs of their own
+        int32_t prev = 0;
+        qvk_reserve_sms(ctas, &prev);
+        c->reserved = ctas;
+    }
     *out = c;
     return QVK_OK;
 }
@@ -175,6 +186,7 @@ int qvk_comm_destroy(qvk_comm_t c) {
         r = ncclCommFinalize(c->comm);
         if (r == ncclSuccess) r = ncclCommDestroy(c->comm);
     }
+    if (c->reserved) qvk_reserve_sms(0, nullptr);
     delete c;
     if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
     return QVK_OK;

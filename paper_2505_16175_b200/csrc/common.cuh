@@ -27,6 +27,7 @@ cudaError_t func_attr(const void* func, cudaFuncAttribute attr, int value);
 // Process-wide lookups, initialised once in a thread-safe way (capi.cu): the SM count of the current device at first
 // use, an integer tuning knob from the environment (default when unset), and the driver's cuTensorMapEncodeTiled.
 int sm_count();
+int grid_sms();  // sm_count() minus the SMs reserved for concurrent work (qvk_reserve_sms)
 int env_knob(const char* name, int def);
 void* tensor_map_encoder();  // PFN_cuTensorMapEncodeTiled_v12000, or nullptr
 

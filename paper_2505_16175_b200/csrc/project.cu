@@ -526,7 +526,7 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
     p.max_tokens = g ? g->max_tokens : 0;
     QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(project_qkv_kernel),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem)));
-    const int sms = sm_count();
+    const int sms = grid_sms();
     static const int two_sm = env_knob("QVK_PROJ_2SM", 1) != 0;  // tuning knob QVK_PROJ_2SM = 0 | 1
     if (two_sm) {
         CUtensorMap mw2;  // W boxes of 128 rows: each CTA of the pair stages half of the 256-column tile

@@ -285,6 +285,14 @@ def score_text(k, groups: DeviceGroups, text_query, n_q: int, n_kv: int, per_hea
     return out
 
 
+def reserve_sms(n: int) -> int:
+    """Leave n SMs free of the persistent kernels' grids (qvk_reserve_sms) for work on other streams; returns the
+    previous reservation.  Results do not depend on it."""
+    prev = C.c_int32(0)
+    check(lib.qvk_reserve_sms(int(n), C.byref(prev)))
+    return prev.value
+
+
 def last_prune_route() -> int:
     """Route of this thread's last prune step: 0 fused, 1 separate kernels, 2 rho = 1 identity, 3 select + gather on
     precomputed scores (qvk_last_prune_route)."""

@@ -46,6 +46,39 @@ def test_nccl_world_one_allgather(cuda):
     check(lib.qvk_comm_destroy(comm))
 
 
+def test_nccl_cta_cap_reserves_sms(cuda):
+    """QVK_COMM_CTAS: qvk_comm_init caps NCCL's CTAs (ncclConfig_t.maxCTAs) and reserves as many SMs from the
+    persistent kernels' grids until qvk_comm_destroy (a world-1 communicator with the cap set explicitly — at
+    world > 1 it is on by default)."""
+    import subprocess
+    import sys
+    code = r"""
+import ctypes as C, sys, torch
+sys.path.insert(0, %r)
+import paper_2505_16175_b200 as qp
+from paper_2505_16175_b200._lib import check, lib
+torch.zeros(1, device='cuda')
+uid = (C.c_char * 128)(); check(lib.qvk_comm_unique_id(uid))
+comm = C.c_void_p(0); check(lib.qvk_comm_init(C.byref(comm), 1, 0, uid))
+assert qp.reserve_sms(6) == 6            # the communicator's reservation was active
+qp.reserve_sms(6)
+rows, heads, width = 512, 2, 128
+kc = torch.randn(rows * heads * width, device='cuda').to(torch.bfloat16); ref = kc.clone()
+seg = (C.c_int64 * 2)(0, rows)
+check(lib.qvk_allgather_layer(torch.cuda.current_stream().cuda_stream, comm, seg, heads, width, kc.data_ptr(),
+                              kc.data_ptr(), None))
+torch.cuda.synchronize(); check(lib.qvk_comm_check(comm))
+assert torch.equal(kc, ref)
+check(lib.qvk_comm_destroy(comm))
+assert qp.reserve_sms(0) == 0            # released by qvk_comm_destroy
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QVK_COMM_CTAS="6")
+    r = subprocess.run([sys.executable, "-c", code % root], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
 def _free_port() -> int:
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

@@ -992,3 +992,32 @@ def test_streaming_prefill_overlaps_a_slow_producer(cuda):
     assert torch.equal(out_k, buf.k_cache.cpu()) and torch.equal(out_v, buf.v_cache.cpu())
     assert torch.equal(out_o, buf.origin.cpu())
     assert wall < len(order) * delay + 0.5, wall  # prefill hidden under the producer (plus a first-launch margin)
+
+
+def test_reserve_sms_leaves_results_unchanged(cuda):
+    """qvk_reserve_sms shrinks the persistent grids (attention, projection) for work running beside them (the N > 1
+    all-gather's NCCL CTAs); each work unit is computed the same way whatever CTA runs it, so outputs are
+    bit-identical with and without a reservation."""
+    sizes, n_q, n_kv, d = [1024, 700, 4096], 28, 4, 128
+    plan = qp.GroupPlan.from_sizes(sizes, 0.5)
+    g = plan.to(cuda)
+    q = torch.cat([qp.synth_bf16(9, 3, 0, i, n, n_q, d, False, cuda) for i, n in enumerate(sizes)])
+    k = torch.cat([qp.synth_bf16(9, 1, 0, i, n, n_kv, d, True, cuda) for i, n in enumerate(sizes)])
+    v = torch.cat([qp.synth_bf16(9, 2, 0, i, n, n_kv, d, False, cuda) for i, n in enumerate(sizes)])
+    x, w = _proj_inputs(sum(sizes), 1024, n_q, n_kv, d, cuda)
+    outs = []
+    for n in (0, 20, 0):
+        qp.reserve_sms(n)
+        try:
+            o = qp.attention(q, k, v, g, n_q, n_kv, 1 / math.sqrt(d))
+            pq, pk, pv = qp.project_qkv(x, w, n_q, n_kv, d)
+            torch.cuda.synchronize()
+        finally:
+            qp.reserve_sms(0)
+        outs.append((o, pq, pk, pv))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    with pytest.raises(qp.QvError):
+        qp.reserve_sms(-1)
+    with pytest.raises(qp.QvError):
+        qp.reserve_sms(100000)
