@@ -202,6 +202,98 @@ __device__ __forceinline__ void store_tile_staged(const ProjParams& p, uint32_t 
     }
 }
 
+// One staged 64-column chunk of the fast drain below: bf16 words pk[0..31] of output columns col64 .. col64 + 63 of
+// row m -> staging buffer (SW128) -> one TMA store; key-norm of the K columns in the reference's order.
+__device__ __forceinline__ void emit_chunk(const ProjParams& p, const uint32_t* pk, int64_t m0, int row, int col64,
+                                           uint8_t* stage, uint32_t& n_chunk, double& ss,
+                                           const CUtensorMap* tm_q, const CUtensorMap* tm_k,
+                                           const CUtensorMap* tm_v, bool leader) {
+    const int64_t m = m0 + row;
+    const uint32_t buf = n_chunk & 1;
+    if (n_chunk >= 2) {  // this buffer's previous store must have read it
+        if (leader) ptx::bulk_wait_group_read<1>();
+        ptx::named_bar_sync(1, 128);
+    }
+    uint8_t* sb = stage + buf * (128 * 128);
+    const uint32_t rbase = ptx::smem_u32(sb) + row * 128;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        ptx::sts128(rbase + ((static_cast<uint32_t>(u) ^ (row & 7)) << 4), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2],
+                    pk[4 * u + 3]);
+    if (p.scores && m < p.m && col64 >= p.q_cols && col64 < p.q_cols + p.kv_cols) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int kcol = col64 - p.q_cols + 32 * h;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const double lo = static_cast<double>(__uint_as_float(pk[16 * h + e] << 16));
+                const double hi = static_cast<double>(__uint_as_float(pk[16 * h + e] & 0xffff0000u));
+                ss = __fma_rn(lo, lo, ss);
+                ss = __fma_rn(hi, hi, ss);
+            }
+            if ((kcol + 32) % p.d_h == 0) {
+                const int hh = kcol / p.d_h;
+                const int g = find_group_fast(p.tok_off, p.n_groups, m, p.max_tokens);
+                const int64_t t0 = __ldg(p.tok_off + g);
+                const int64_t n = __ldg(p.tok_off + g + 1) - t0;
+                p.scores[p.n_kv * t0 + hh * n + (m - t0)] = -__dsqrt_rn(ss);
+                ss = 0.0;
+            }
+        }
+    }
+    ptx::fence_proxy_async_smem();
+    ptx::named_bar_sync(1, 128);
+    if (leader) {
+        const CUtensorMap* tm;
+        int cc;
+        if (col64 < p.q_cols) {
+            tm = tm_q;
+            cc = col64;
+        } else if (col64 < p.q_cols + p.kv_cols) {
+            tm = tm_k;
+            cc = col64 - p.q_cols;
+        } else {
+            tm = tm_v;
+            cc = col64 - p.q_cols - p.kv_cols;
+        }
+        ptx::tma_store_2d(tm, sb, cc, static_cast<int>(m0));
+        ptx::bulk_commit_group();
+    }
+    ++n_chunk;
+}
+
+// Fast drain of one 128 x 256 accumulator for the single-buffered wide kernel: the TMEM is read in two batches of
+// 128 columns (4 loads, ONE wait each) and released right after the second batch lands — before any conversion or
+// store — so the next tile's MMAs wait two TMEM load latencies instead of eight plus the whole store path.
+__device__ __forceinline__ void store_tile_fast(const ProjParams& p, uint32_t acc, int64_t m0, int row, int col0,
+                                                uint32_t acc_empty, uint8_t* stage, uint32_t& n_chunk,
+                                                const CUtensorMap* tm_q, const CUtensorMap* tm_k,
+                                                const CUtensorMap* tm_v, bool leader) {
+    float x[128];
+    uint32_t pa[64];
+    QVK_TMEM_LD32F(acc + 0, (x + 0));
+    QVK_TMEM_LD32F(acc + 32, (x + 32));
+    QVK_TMEM_LD32F(acc + 64, (x + 64));
+    QVK_TMEM_LD32F(acc + 96, (x + 96));
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < 64; ++e) pa[e] = ptx::pack_bf16(x[2 * e], x[2 * e + 1]);
+    QVK_TMEM_LD32F(acc + 128, (x + 0));
+    QVK_TMEM_LD32F(acc + 160, (x + 32));
+    QVK_TMEM_LD32F(acc + 192, (x + 64));
+    QVK_TMEM_LD32F(acc + 224, (x + 96));
+    ptx::tmem_ld_wait();
+    ptx::tc_fence_before();
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acc_empty) : "memory");
+    double ss = 0.0;
+    emit_chunk(p, pa, m0, row, col0, stage, n_chunk, ss, tm_q, tm_k, tm_v, leader);
+    emit_chunk(p, pa + 32, m0, row, col0 + 64, stage, n_chunk, ss, tm_q, tm_k, tm_v, leader);
+#pragma unroll
+    for (int e = 0; e < 64; ++e) pa[e] = ptx::pack_bf16(x[2 * e], x[2 * e + 1]);
+    emit_chunk(p, pa, m0, row, col0 + 128, stage, n_chunk, ss, tm_q, tm_k, tm_v, leader);
+    emit_chunk(p, pa + 32, m0, row, col0 + 192, stage, n_chunk, ss, tm_q, tm_k, tm_v, leader);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     project_qkv_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
                        const ProjParams p) {
@@ -464,6 +556,184 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------------------------------------
+// Wide 2-SM variant: a CTA pair computes a 256 x 512 output tile as two M = 256, N = 256 MMAs per k-step ("sub-tiles"
+// 0 and 1), so every k-block's X rows are staged once for 512 output columns instead of 256 — L2 -> SMEM operand
+// traffic per FLOP drops by a quarter (X 16 KB + W 2 x 16 KB per CTA per k-block for 2 x 256 x 256 x 64 MACs).
+// Each CTA's whole TMEM (512 columns) is the accumulator: sub-tile j in columns [256 j, 256 j + 256), single-buffered,
+// one acc_full / acc_empty barrier per sub-tile.  To overlap the drain anyway, the MMA issuer runs sub-tile 1 kSkew
+// k-blocks BEHIND sub-tile 0 (a stage is released by sub-tile 1's commit): sub-tile 0 of a tile completes early and
+// is drained (store_tile_fast: released after two TMEM load batches) while the tensor pipe finishes sub-tile 1.
+constexpr int kStagesW = 4;
+constexpr uint32_t kStageW = kABytes + 2 * kBHalf;  // 48 KB: X 128 rows + W 2 x 128 rows
+struct ProjBarriersW {
+    uint64_t full[kStagesW], empty[kStagesW];
+    uint64_t acc_full[2], acc_empty[2];  // per sub-tile
+    uint32_t tmem_base;
+};
+constexpr size_t kSmemW = 1024 + kStagesW * kStageW + kStageOut + sizeof(ProjBarriersW);
+static_assert(kSmemW <= 232448, "project: wide 2-SM kernel shared memory above 227 KB");
+
+__device__ __forceinline__ void mma2_kblock(uint32_t d, uint32_t a_addr, uint32_t b_addr, uint32_t id, bool first) {
+#pragma unroll
+    for (int kk = 0; kk < kBK / 16; ++kk) {
+        const uint64_t da = kdesc(a_addr, kk), db = kdesc(b_addr, kk);
+        const uint32_t acc = (!first || kk != 0) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(da), "l"(db), "r"(id), "r"(acc));
+    }
+}
+__device__ __forceinline__ void commit2_multicast(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            ptx::smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
+template <int kSkew>
+__global__ void __launch_bounds__(kThreads, 1)
+    project_qkv_2sm_wide_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+                                const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                                const __grid_constant__ CUtensorMap tm_v, const ProjParams p) {
+    static_assert(kStagesW >= kSkew + 2, "wide projection: the ring must hold the skew plus one stage in flight");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stage_out = smem + kStagesW * kStageW;
+    ProjBarriersW* bar = reinterpret_cast<ProjBarriersW*>(stage_out + kStageOut);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cta_rank_in_cluster();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, pairs = gridDim.x >> 1;
+    constexpr int kBNW = 2 * kBN;
+    const int m_tiles = static_cast<int>((p.m + 2 * kBM - 1) / (2 * kBM));
+    const int n_tiles = p.n / kBNW;
+    const int tiles = m_tiles * n_tiles;
+    const int kb_count = p.k / kBK;
+    const int my_tiles = pair < tiles ? (tiles - pair + pairs - 1) / pairs : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesW; ++s) {
+            ptx::mbar_init(&bar->full[s], 1);
+            ptx::mbar_init(&bar->empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&bar->acc_full[b], 1);
+            ptx::mbar_init(&bar->acc_empty[b], 2 * 128);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         ptx::smem_u32(&bar->tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    ptx::tc_fence_before();
+    cluster_sync_all();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = bar->tmem_base;
+
+    if (warp == kTmaWarp) {
+        if (ptx::elect_one()) {
+            ptx::prefetch_tmap(&tm_x);
+            ptx::prefetch_tmap(&tm_w);
+            uint32_t it = 0;
+            for (int tile = pair; tile < tiles; tile += pairs) {
+                const int mt = tile / n_tiles, nt = tile - mt * n_tiles;
+                for (int kb = 0; kb < kb_count; ++kb, ++it) {
+                    const uint32_t s = it % kStagesW;
+                    ptx::mbar_wait(&bar->empty[s], ((it / kStagesW) & 1) ^ 1);
+                    const uint32_t st = ptx::smem_u32(smem + s * kStageW);
+                    if (leader) ptx::mbar_arrive_expect_tx(&bar->full[s], 2 * kStageW);
+                    const uint32_t fb = map_to_cta(ptx::smem_u32(&bar->full[s]), 0);  // the leader's full[s]
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+                        "[%0], [%1, {%3, %4}], [%2];" ::"r"(st),
+                        "l"(reinterpret_cast<uint64_t>(&tm_x)), "r"(fb), "r"(kb * kBK),
+                        "r"(mt * 2 * kBM + static_cast<int>(rank) * kBM)
+                        : "memory");
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+                            "[%0], [%1, {%3, %4}], [%2];" ::"r"(st + kABytes + j * kBHalf),
+                            "l"(reinterpret_cast<uint64_t>(&tm_w)), "r"(fb), "r"(kb * kBK),
+                            "r"(nt * kBNW + j * kBN + static_cast<int>(rank) * (kBN / 2))
+                            : "memory");
+                }
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (leader && ptx::elect_one()) {
+            constexpr uint32_t kId = ptx::idesc_bf16_f32(2 * kBM, kBN, false, false);
+            const uint32_t base = ptx::smem_u32(smem);
+            const int total = my_tiles * kb_count;
+            // step i: sub-tile 1 of k-block i - kSkew (releases its stage), then sub-tile 0 of k-block i
+            for (int i = 0; i < total + kSkew; ++i) {
+                const int j = i - kSkew;
+                if (j >= 0) {
+                    const int tj = j / kb_count, kbj = j - tj * kb_count;
+                    const uint32_t s = static_cast<uint32_t>(j) % kStagesW;
+                    if (kbj == 0) {
+                        ptx::mbar_wait(&bar->acc_empty[1], (tj & 1) ^ 1);
+                        ptx::tc_fence_after();
+                    }
+                    const uint32_t a_addr = base + s * kStageW;
+                    mma2_kblock(tmem + kBN, a_addr, a_addr + kABytes + kBHalf, kId, kbj == 0);
+                    commit2_multicast(&bar->empty[s]);
+                    if (kbj == kb_count - 1) commit2_multicast(&bar->acc_full[1]);
+                }
+                if (i < total) {
+                    const int ti = i / kb_count, kb = i - ti * kb_count;
+                    const uint32_t s = static_cast<uint32_t>(i) % kStagesW;
+                    if (kb == 0) {
+                        ptx::mbar_wait(&bar->acc_empty[0], (ti & 1) ^ 1);
+                        ptx::tc_fence_after();
+                    }
+                    ptx::mbar_wait(&bar->full[s], (static_cast<uint32_t>(i) / kStagesW) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = base + s * kStageW;
+                    mma2_kblock(tmem, a_addr, a_addr + kABytes, kId, kb == 0);
+                    if (kb == kb_count - 1) commit2_multicast(&bar->acc_full[0]);
+                }
+            }
+        }
+    } else {
+        const int quarter = warp & 3;
+        const int row = quarter * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+        uint32_t n_acc = 0, n_chunk = 0;
+        const bool out_leader = warp == 2 && lane == 0;
+        if (out_leader) {
+            ptx::prefetch_tmap(&tm_q);
+            ptx::prefetch_tmap(&tm_k);
+            ptx::prefetch_tmap(&tm_v);
+        }
+        for (int tile = pair; tile < tiles; tile += pairs, ++n_acc) {
+            const int mt = tile / n_tiles, nt = tile - mt * n_tiles;
+            const int64_t m0 = static_cast<int64_t>(mt) * 2 * kBM + static_cast<int64_t>(rank) * kBM;
+#pragma unroll 1
+            for (int sub = 0; sub < 2; ++sub) {
+                ptx::mbar_wait(&bar->acc_full[sub], n_acc & 1);
+                ptx::tc_fence_after();
+                store_tile_fast(p, tmem + lane_off + sub * kBN, m0, row, nt * kBNW + sub * kBN,
+                                map_to_cta(ptx::smem_u32(&bar->acc_empty[sub]), 0), stage_out, n_chunk, &tm_q,
+                                &tm_k, &tm_v, out_leader);
+            }
+        }
+        if (out_leader) ptx::bulk_wait_group<0>();
+    }
+    ptx::tc_fence_before();
+    cluster_sync_all();
+    if (warp == kMmaWarp) {
+        ptx::tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
 bool make_map_2d(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows) {
     const auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(tensor_map_encoder());
     if (!enc) return false;
@@ -534,15 +804,21 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
             set_error("project: cuTensorMapEncodeTiled failed");
             return QVK_E_CUDA;
         }
-        QVK_CUDA_CHECK(func_attr(reinterpret_cast<const void*>(project_qkv_2sm_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem2)));
-        const int64_t tiles2 = ((tokens + 2 * kBM - 1) / (2 * kBM)) * (n / kBN);
+        // QVK_PROJ_WIDE = 0 (256 x 256 pair tiles) | 1 | 2 (256 x 512 pair tiles, sub-tile skew 1 or 2 k-blocks)
+        static const int wide_knob = env_knob("QVK_PROJ_WIDE", 0);
+        const bool wide = wide_knob != 0 && n % (2 * kBN) == 0;
+        const void* kfn = !wide ? reinterpret_cast<const void*>(project_qkv_2sm_kernel)
+                          : wide_knob == 2 ? reinterpret_cast<const void*>(project_qkv_2sm_wide_kernel<2>)
+                                           : reinterpret_cast<const void*>(project_qkv_2sm_wide_kernel<1>);
+        const size_t smem_bytes = wide ? kSmemW : kSmem2;
+        QVK_CUDA_CHECK(func_attr(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_bytes)));
+        const int64_t tiles2 = ((tokens + 2 * kBM - 1) / (2 * kBM)) * (n / (wide ? 2 * kBN : kBN));
         if (tiles2 > 0x7fffffff) QVK_INVALID("project: too many tiles");
         const unsigned pairs = static_cast<unsigned>(std::min<int64_t>(tiles2, sms / 2));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * pairs);
         cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = kSmem2;
+        cfg.dynamicSmemBytes = smem_bytes;
         cfg.stream = stream;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -557,7 +833,12 @@ int launch_project_qkv(cudaStream_t stream, const void* x, int64_t tokens, int d
             set_error("project: cuTensorMapEncodeTiled failed");
             return QVK_E_CUDA;
         }
-        QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, project_qkv_2sm_kernel, mx, mw2, mq, mk, mv, p));
+        if (wide && wide_knob == 2)
+            QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, project_qkv_2sm_wide_kernel<2>, mx, mw2, mq, mk, mv, p));
+        else if (wide)
+            QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, project_qkv_2sm_wide_kernel<1>, mx, mw2, mq, mk, mv, p));
+        else
+            QVK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, project_qkv_2sm_kernel, mx, mw2, mq, mk, mv, p));
         return QVK_OK;
     }
     const int64_t tiles = ((tokens + kBM - 1) / kBM) * (n / kBN);

@@ -872,8 +872,10 @@ def test_host_prefill_chained_calls(cuda):
 
 
 def test_project_qkv_one_sm_variant(cuda, tmp_path):
-    """The 1-SM GEMM variant (QVK_PROJ_2SM=0, read once per process: run in a subprocess) agrees with the default
-    2-SM kernel within the bf16 tolerance and its fused key-norm equals qvk_score on its own K bit for bit."""
+    """The 1-SM GEMM variant (QVK_PROJ_2SM=0) and the opt-in 256 x 512 pair-tile variant (QVK_PROJ_WIDE=1; knobs are
+    read once per process: one subprocess each) agree with the default 2-SM kernel — the wide one bit for bit (same
+    per-element accumulation order), the 1-SM one within the bf16 tolerance — and their fused key-norm equals
+    qvk_score on their own K bit for bit."""
     import subprocess
     import sys
     code = r"""
@@ -890,15 +892,16 @@ assert sc.cpu().numpy().tobytes() == qp.score(k, v, g, 2, 128, qp.Scorer.key_nor
 torch.save({'q': q.cpu(), 'k': k.cpu(), 'v': v.cpu()}, %r)
 """
     outs = []
-    for flag in ("0", "1"):
-        path = tmp_path / f"p{flag}.pt"
-        env = dict(__import__("os").environ, QVK_PROJ_2SM=flag)
+    for i, knobs in enumerate(({"QVK_PROJ_2SM": "0"}, {"QVK_PROJ_2SM": "1"}, {"QVK_PROJ_WIDE": "1"})):
+        path = tmp_path / f"p{i}.pt"
+        env = dict(__import__("os").environ, **knobs)
         r = subprocess.run([sys.executable, "-c", code % (str(GOLD.parent.parent), str(path))], env=env,
                            capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(torch.load(path))
     for name in ("q", "k", "v"):
         check_tol(outs[0][name], outs[1][name], f"1-SM vs 2-SM {name}")
+        assert torch.equal(outs[1][name], outs[2][name]), f"wide vs 2-SM {name}"
 
 
 @pytest.mark.parametrize("scorer,per_head", [(qp.Scorer.snapkv, True), (qp.Scorer.value_norm, True),
