@@ -21,15 +21,19 @@ __global__ void seeded_matrix_kernel(uint64_t state0, size_t count, double scale
 // out(rows, d_out) = x(rows, d_in) * w(d_in, d_out): every output accumulates i = 0..d_in-1 in order, in double
 // (prefill.cpp:38-54 `acc[o] += xi * wrow[o]`).  The product of two floats is exact in double (24 + 24 bits), so
 // fma(xi, w, acc) rounds exactly like acc + xi * w: bit-identical to the reference while running one DFMA per MAC.
-// CTA tile 64 rows x 64 outputs, 256 threads with 4 x 4 outputs each (register tile), reduction chunks of 16
-// staged in shared memory as doubles (converted once per element, not per use).
-constexpr int kPM = 64, kPN = 64, kPK = 16;
+// CTA tile 64 rows x 64 outputs, 256 threads with 4 x 4 outputs each (register tile), reduction chunks of 32
+// staged in shared memory as doubles (converted once per element, not per use).  Shared-memory layout chosen for
+// the banks (the first version was bound by bank conflicts: ncu L1 94 %, FP64 pipe 23 %): the x tile's rows are
+// padded to 66 doubles, so the transposing stores hit distinct bank pairs; a thread's
+// four outputs are columns {2 tx, 2 tx + 1, 32 + 2 tx, 33 + 2 tx}, so each 16-byte w load of a warp covers 256
+// contiguous bytes (two wavefronts, no conflict).
+constexpr int kPM = 64, kPN = 64, kPK = 32, kPXS = kPM + 2;
 __global__ void __launch_bounds__(256) project_exact_kernel(const float* __restrict__ x, int64_t rows, int d_in,
                                                             const float* __restrict__ w, int d_out,
                                                             float* __restrict__ out) {
-    __shared__ __align__(16) double xs[kPK][kPM];  // xs[i][r]
-    __shared__ __align__(16) double ws[kPK][kPN];  // ws[i][o]
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // outputs 4 tx.., rows 4 ty..
+    __shared__ __align__(16) double xs[kPK][kPXS];  // xs[i][r]
+    __shared__ __align__(16) double ws[kPK][kPN];   // ws[i][o]
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // outputs {2tx, 2tx+1, 32+2tx, 33+2tx}, rows 4ty..
     const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kPM;
     const int o0 = blockIdx.x * kPN;
     double acc[4][4];
@@ -39,8 +43,11 @@ __global__ void __launch_bounds__(256) project_exact_kernel(const float* __restr
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
     for (int i0 = 0; i0 < d_in; i0 += kPK) {
         __syncthreads();
-        for (int e = threadIdx.x; e < kPM * kPK; e += 256) {  // x tile: consecutive threads walk i (coalesced rows)
-            const int rr = e / kPK, ii = e % kPK;
+        // x tile: a warp covers 2 rows x 16 consecutive i (64-byte row segments); with the 66-double rows its 32
+        // transposing stores land on distinct bank pairs two by two (the minimum two wavefronts)
+        for (int e = threadIdx.x; e < kPM * kPK; e += 256) {
+            const int e2 = e % (kPM * 16);
+            const int rr = e2 / 16, ii = (e / (kPM * 16)) * 16 + (e2 % 16);
             const int64_t gr = r0 + rr;
             xs[ii][rr] = (gr < rows && i0 + ii < d_in) ? static_cast<double>(__ldg(x + gr * d_in + i0 + ii)) : 0.0;
         }
@@ -52,11 +59,12 @@ __global__ void __launch_bounds__(256) project_exact_kernel(const float* __restr
         }
         __syncthreads();
         const int kw = min(kPK, d_in - i0);
+#pragma unroll 4
         for (int ii = 0; ii < kw; ++ii) {
             const double2 xa = *reinterpret_cast<const double2*>(&xs[ii][ty * 4]);
             const double2 xb = *reinterpret_cast<const double2*>(&xs[ii][ty * 4 + 2]);
-            const double2 wa = *reinterpret_cast<const double2*>(&ws[ii][tx * 4]);
-            const double2 wb = *reinterpret_cast<const double2*>(&ws[ii][tx * 4 + 2]);
+            const double2 wa = *reinterpret_cast<const double2*>(&ws[ii][2 * tx]);
+            const double2 wb = *reinterpret_cast<const double2*>(&ws[ii][32 + 2 * tx]);
             const double xv[4] = {xa.x, xa.y, xb.x, xb.y}, wv[4] = {wa.x, wa.y, wb.x, wb.y};
 #pragma unroll
             for (int a = 0; a < 4; ++a)
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(256) project_exact_kernel(const float* __restr
         if (r >= rows) continue;
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-            const int o = o0 + tx * 4 + b;
+            const int o = o0 + (b < 2 ? 2 * tx + b : 32 + 2 * tx + (b - 2));
             if (o < d_out) out[r * d_out + o] = __double2float_rn(acc[a][b]);
         }
     }

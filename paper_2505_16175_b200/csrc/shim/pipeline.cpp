@@ -133,6 +133,19 @@ qv::KvCache run_pipeline(const qv::VideoFile& file, const qv::SampleSpec& spec, 
     for (size_t w = 0; w < workers; ++w) pool.emplace_back(worker);
 
     qv::KvCache cache = qv::make_cache(model.config());
+    if (cfg.prune.rho > 0.0 && cfg.prune.rho <= 1.0) {  // the cache's final size is static (prefill.cpp:304-308 appends retained_count rows per group): reserve it
+        // once, so appending group by group never reallocates and copies the rows already there
+        size_t rows = 0;
+        for (size_t g = 0; g < G; ++g) {
+            const size_t f0 = g * fpg, f1 = std::min<size_t>(f0 + fpg, slots);
+            rows += qv::retained_count(cfg.prune.rho, (f1 - f0) * model.config().tokens_per_frame);
+        }
+        for (qv::LayerCache& l : cache.layers) {
+            l.k.reserve(rows * model.config().d_model);
+            l.v.reserve(rows * model.config().d_model);
+            l.origin.reserve(rows);
+        }
+    }
     std::vector<GroupTiming> times(G);
     double t_prefill = 0, t_last = 0;
     try {

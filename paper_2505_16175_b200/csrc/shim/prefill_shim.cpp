@@ -9,13 +9,17 @@
 //   tokenize               exact integer patch sums, fp64 embed           (prefill.cpp:123-168)
 //   project                fp64 accumulation in the reference's order     (prefill.cpp:38-54, 185-190)
 //   score / top-k / gather exact fp64 scores, exact radix select, copies  (prefill.cpp:192-282)
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <thread>
 
 #include "qv/prefill.hpp"
 #include "qvk.h"
@@ -89,6 +93,41 @@ public:
 private:
     void* p_ = nullptr;
 };
+
+// QV_SHIM_TRACE=1: host-side phase times of tokenize / prefill on stderr (developer diagnostics).
+struct Phase {
+    const char* name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    static bool on() {
+        static const bool v = std::getenv("QV_SHIM_TRACE") != nullptr;
+        return v;
+    }
+    void lap(const char* what) {
+        if (!on()) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[qv shim] %s %s %.2f ms\n", name, what,
+                     std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
+
+// Size every vector of `vs` to its count on several host threads: value-initialising a fresh allocation costs a
+// page fault and a zero fill per 4 KB page, serial inside one resize but independent between vectors.
+template <class T>
+void resize_parallel(std::vector<std::vector<T>*>& vs, const std::vector<size_t>& counts) {
+    const size_t n = vs.size();
+    const size_t threads = std::min<size_t>(n, 16);
+    if (threads <= 1) {
+        for (size_t i = 0; i < n; ++i) vs[i]->resize(counts[i]);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < threads; ++t)
+        th.emplace_back([&, t] {
+            for (size_t i = t; i < n; i += threads) vs[i]->resize(counts[i]);
+        });
+    for (auto& x : th) x.join();
+}
 
 template <class T>
 void download(std::vector<T>& out, const Dev& d, size_t count) {
@@ -236,6 +275,7 @@ void prefill_device(const StandInModel& model, const float* x_d, const Groups& g
     auto dm = device_model(cfg);
     const size_t d = cfg.d_model;
     const size_t T = static_cast<size_t>(gr.g.total_tokens), R = static_cast<size_t>(gr.g.total_rows);
+    Phase ph{"prefill"};
     Dev k(T * d * sizeof(float)), v(T * d * sizeof(float));
     Dev kc(std::max<size_t>(1, R * d) * sizeof(float)), vc(std::max<size_t>(1, R * d) * sizeof(float));
     Dev org(std::max<size_t>(1, R) * sizeof(uint64_t));
@@ -252,13 +292,19 @@ void prefill_device(const StandInModel& model, const float* x_d, const Groups& g
                         ix.get<uint32_t>(), kc.get(), vc.get(), org.get<uint64_t>()));
         LayerCache& layer = cache.layers[l];
         const size_t base = layer.origin.size();
-        layer.k.resize(layer.k.size() + R * d);
-        layer.v.resize(layer.v.size() + R * d);
-        layer.origin.resize(base + R);
+        ph.lap("launch");
+        {  // grown on two host threads while the layer's kernels run
+            std::thread tk([&] { layer.k.resize(layer.k.size() + R * d); });
+            layer.v.resize(layer.v.size() + R * d);
+            layer.origin.resize(base + R);
+            tk.join();
+        }
+        ph.lap("alloc");
         // synchronous, stream-ordered after this layer's prune and before the next layer's (which reuses kc / vc)
         check(qvk_memcpy_d2h_pageable(layer.k.data() + base * d, kc.get(), R * d * sizeof(float), nullptr));
         check(qvk_memcpy_d2h_pageable(layer.v.data() + base * d, vc.get(), R * d * sizeof(float), nullptr));
         check(qvk_memcpy_d2h_pageable(layer.origin.data() + base, org.get(), R * sizeof(uint64_t), nullptr));
+        ph.lap("d2h");
     }
     for (size_t i = 0; i < token_counts.size(); ++i) {  // prefill.cpp:309-313 (last layer's retained count)
         cache.retained_per_group.push_back(static_cast<size_t>(gr.keep[i]));
@@ -272,6 +318,7 @@ void prefill_batch(const StandInModel& model, std::span<const TokenGroup> groups
     check_prune(model, groups, prune);
     const size_t d = model.config().d_model;
     Groups gr(groups, prune.rho);
+    Phase ph{"prefill"};
     Dev x(static_cast<size_t>(gr.g.total_tokens) * d * sizeof(float));
     std::vector<size_t> counts;
     for (size_t i = 0; i < groups.size(); ++i) {
@@ -279,6 +326,7 @@ void prefill_batch(const StandInModel& model, std::span<const TokenGroup> groups
                                       groups[i].token_count * d * sizeof(float), nullptr));
         counts.push_back(groups[i].token_count);
     }
+    ph.lap("h2d");
     prefill_device(model, x.get<float>(), gr, prune, cache, counts);
 }
 
@@ -367,28 +415,34 @@ std::vector<TokenGroup> StandInModel::tokenize(const FrameBuffer& frames, uint32
         throw Error("tokenize: frame size not divisible into the patch grid");
     // One H2D of every slot and one launch for all tokens; groups are slices (prefill.cpp:170-183 order).
     const size_t d = config_.d_model, tpf = config_.tokens_per_frame, slots = frames.slots();
+    Phase ph{"tokenize"};
     Dev pixels(frames.bytes().data(), frames.bytes().size());
     Dev embed(embed_.data(), embed_.size() * sizeof(float));
     Dev tokens(slots * tpf * d * sizeof(float));
+    ph.lap("h2d");
     check(qvk_tokenize(nullptr, pixels.get<uint8_t>(), static_cast<int64_t>(slots), frames.width(), frames.height(),
                        config_.tokens_per_frame, embed.get<float>(), static_cast<int32_t>(d), tokens.get<float>()));
-    std::vector<float> all;
-    download(all, tokens, slots * tpf * d);
     uint64_t count = 0;
     check(qvk_group_count(slots, frames_per_group, &count));
-    std::vector<TokenGroup> groups;
-    groups.reserve(count);
+    std::vector<TokenGroup> groups(count);
+    std::vector<std::vector<float>*> vecs;
+    std::vector<size_t> sizes;
     for (uint64_t g = 0; g < count; ++g) {
-        TokenGroup group;
+        TokenGroup& group = groups[g];
         group.group_id = size_t(g);
         group.frame_begin = size_t(g) * frames_per_group;
         group.frame_end = std::min<size_t>(group.frame_begin + frames_per_group, slots);
         group.first_token = uint64_t(group.frame_begin) * tpf;
         group.token_count = (group.frame_end - group.frame_begin) * tpf;
-        const float* src = all.data() + group.frame_begin * tpf * d;
-        group.tokens.assign(src, src + group.token_count * d);
-        groups.push_back(std::move(group));
+        vecs.push_back(&group.tokens);
+        sizes.push_back(group.token_count * d);
     }
+    resize_parallel(vecs, sizes);  // overlaps the tokenizer kernel
+    ph.lap("alloc");
+    for (uint64_t g = 0; g < count; ++g)  // each group's slice of the device tokens straight into its vector
+        check(qvk_memcpy_d2h_pageable(groups[g].tokens.data(), tokens.get<float>() + groups[g].frame_begin * tpf * d,
+                                      sizes[g] * sizeof(float), nullptr));
+    ph.lap("d2h");
     return groups;
 }
 

@@ -89,9 +89,11 @@ def test_overlap_pipeline_bitexact(cuda, args):
 def test_overlap_pipeline_c2_video_latency_model(cuda):
     """A C2-sized video (256 frames of 448 x 448, 256 tokens per frame, groups of 16 frames, the 7B shape, 1 layer)
     through the overlap pipeline: the paper's t_total = max(t_dec + t_g_prefill, t_prefill + t_g_dec) + Delta
-     predicts the measured time within 10 %, and the overlap beats decode-then-prefill."""
+     predicts the measured time within 10 %, and the overlap beats decode-then-prefill.  Two decode
+    cores, so decoding is a sizeable share of the sequential time (with 8 it is ~10 % of it and the saving sits
+    within the timing noise)."""
     rc, out, err = run("overlap", 1, 1, 256, 448, 448, 3584, 28, 128, 1, 256, 64, 16, "key_norm_small", 0.5,
-                       8, 64, 24, 1, 0)
+                       2, 64, 24, 1, 0)
     res = json.loads(out.strip().splitlines()[-1])
     print(res)
     assert rc == 0, (res, err)
