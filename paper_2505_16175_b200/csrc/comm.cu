@@ -120,14 +120,20 @@ int qvk_comm_init(qvk_comm_t* out, int32_t world, int32_t rank, const void* uniq
     // world 1 has nothing to overlap: no cap unless QVK_COMM_CTAS is set explicitly (the test hook)
     const int ctas = std::max(0, qvk::env_knob("QVK_COMM_CTAS", world > 1 ? 8 : 0));
     if (ctas > 0) cfg.maxCTAs = ctas;
-    const ncclResult_t r = ncclCommInitRankConfig(&c->comm, world, id, rank, &cfg);
+    ncclResult_t r = ncclCommInitRankConfig(&c->comm, world, id, rank, &cfg);
+    bool capped = ctas > 0;
+    if (r == ncclInvalidArgument && capped) {  // an NCCL that rejects the cap (same on every rank): uncapped init
+        c->comm = nullptr;
+        r = ncclCommInitRank(&c->comm, world, id, rank);
+        capped = false;
+    }
     if (r != ncclSuccess) {
         delete c;
         return nccl_fail(r, "ncclCommInitRankConfig");
     }
     c->rank = rank;
     c->world = world;
-    if (ctas > 0 && ctas < qvk::sm_count() - 2) {  // the all-gather's CTAs get SMs of their own
+    if (capped && ctas < qvk::sm_count() - 2) {  // the all-gather's CTAs get SMs of their own
         int32_t prev = 0;
         qvk_reserve_sms(ctas, &prev);
         c->reserved = ctas;

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <list>
 #include <map>
 #include <memory>
@@ -122,11 +123,18 @@ void resize_parallel(std::vector<std::vector<T>*>& vs, const std::vector<size_t>
         return;
     }
     std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(threads);
     for (size_t t = 0; t < threads; ++t)
         th.emplace_back([&, t] {
-            for (size_t i = t; i < n; i += threads) vs[i]->resize(counts[i]);
+            try {
+                for (size_t i = t; i < n; i += threads) vs[i]->resize(counts[i]);
+            } catch (...) {
+                err[t] = std::current_exception();  // bad_alloc etc. reach the caller, as with a serial resize
+            }
         });
     for (auto& x : th) x.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
 }
 
 template <class T>
@@ -294,10 +302,23 @@ void prefill_device(const StandInModel& model, const float* x_d, const Groups& g
         const size_t base = layer.origin.size();
         ph.lap("launch");
         {  // grown on two host threads while the layer's kernels run
-            std::thread tk([&] { layer.k.resize(layer.k.size() + R * d); });
-            layer.v.resize(layer.v.size() + R * d);
-            layer.origin.resize(base + R);
+            std::exception_ptr ek;
+            std::thread tk([&] {
+                try {
+                    layer.k.resize(layer.k.size() + R * d);
+                } catch (...) {
+                    ek = std::current_exception();
+                }
+            });
+            try {
+                layer.v.resize(layer.v.size() + R * d);
+                layer.origin.resize(base + R);
+            } catch (...) {
+                tk.join();
+                throw;
+            }
             tk.join();
+            if (ek) std::rethrow_exception(ek);
         }
         ph.lap("alloc");
         // synchronous, stream-ordered after this layer's prune and before the next layer's (which reuses kc / vc)
