@@ -178,3 +178,17 @@ def test_c_abi_rejects_bad_arguments_without_a_gpu():
     assert lib.qvk_decode_workspace(1, 27, 4, 128, 100, C.byref(n)) == -1  # n_q not a multiple of n_kv
     assert lib.qvk_decode_workspace(1, 28, 4, 128, 100, C.byref(n)) == 0 and n.value > 0
     assert lib.qvk_ipc_get_handle(None, None, None) == -1
+
+
+def test_reserve_sms_bounds_and_previous_value():
+    """qvk_reserve_sms (host-only bookkeeping: the persistent grids read it at launch) returns the previous
+    reservation and rejects n < 0 and n >= the SM count with QVK_E_INVALID and a message."""
+    prev = qp.reserve_sms(8)
+    try:
+        assert qp.reserve_sms(3) == 8
+        for bad in (-1, 100000):
+            with pytest.raises(qp.QvError, match="reserve_sms"):
+                qp.reserve_sms(bad)
+        assert qp.reserve_sms(0) == 3
+    finally:
+        qp.reserve_sms(prev)
