@@ -92,14 +92,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     }
 }
 #else
+#ifndef QVK_MBAR_SUSPEND_NS
+#define QVK_MBAR_SUSPEND_NS 1000000u  // try_wait suspend-time hint: a waiting warp sleeps until the phase completes
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     asm volatile(
         "{\n\t.reg .pred P;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
         "@!P bra WAIT_%=;\n\t}" ::"r"(addr),
-        "r"(parity)
+        "r"(parity), "r"(QVK_MBAR_SUSPEND_NS)
         : "memory");
 }
 #endif
