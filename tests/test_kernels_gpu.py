@@ -16,6 +16,7 @@ import torch
 
 import paper_2505_16175_b200 as qp
 from oracle import oracle as O
+from tiecheck import error_bounded_ties
 
 pytestmark = pytest.mark.gpu
 GOLD = __import__("pathlib").Path(__file__).resolve().parent / "golden"
@@ -386,8 +387,10 @@ def test_snapkv_vs_oracle(cuda, sizes, window, pool, n_q, n_kv):
             diff = got_set ^ want_set
             near = [i for i in diff if abs(want[h][i] - kth) <= 1e-4 * abs(kth)]
             assert len(diff) == len(near), f"group {gi} head {h}: index differences outside the near-tie band"
-            if diff:
-                print(f"snapkv group {gi} head {h}: {len(diff)} near-tie index differences")
+            # and the tighter, error-derived band: differences only within 2 x this head's measured score error
+            nd, eps, band = error_bounded_ties(sorted(got_set), seg[h], want[h], kk)
+            print(f"snapkv group {gi} head {h}: {nd} near-tie index differences, eps {eps:.3g} "
+                  f"(rel {eps / max(abs(kth), 1e-300):.3g} of the k-th score)")
         t0 += n
 
 

@@ -233,3 +233,22 @@ def test_gqa_attention_score_oracle_pinned():
     per_tok = O.score_text_ref(k, n, n_q, n_kv, d, False, qbar, T)
     port = O.score_attention(k.reshape(n, -1), n, 1, n_kv * d, qbar.ravel(), 1)
     assert np.array_equal(per_tok[0], port / (T * n_q))
+
+
+def test_error_bounded_tie_check():
+    """tests/tiecheck.py: swaps within 2 eps of the k-th score pass, a swap outside it and a set that is not the
+    top-k of its own scores fail."""
+    import pytest as _pt
+    from tiecheck import error_bounded_ties
+    want = np.array([5.0, 4.0, 3.0, 2.999, 1.0])
+    got = want + np.array([0, 0, -0.001, 0.001, 0])        # eps 1e-3: indices 2 and 3 swap (gap 1e-3 <= 2 eps)
+    nd, eps, _ = error_bounded_ties([0, 1, 3], got, want, 3)
+    assert nd == 2 and abs(eps - 1e-3) < 1e-12
+    with _pt.raises(AssertionError):
+        error_bounded_ties([0, 1, 2], got, want, 3)          # not the top-k of its own scores
+    bad = want.copy()
+    bad[4] = 3.5                                             # index 4 displaces 2: error 2.5, but band is 5
+    assert error_bounded_ties([0, 1, 4], bad, want, 3)[0] == 2
+    bad2 = want.copy()
+    bad2[2], bad2[3] = 2.0, 3.2                              # eps 1.0, band 2.0: 3 vs 2 differ by 1e-3, allowed
+    assert error_bounded_ties([0, 1, 3], bad2, want, 3)[0] == 2

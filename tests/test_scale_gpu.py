@@ -25,6 +25,7 @@ import torch
 
 import paper_2505_16175_b200 as qp
 from oracle import oracle as O
+from tiecheck import error_bounded_ties
 
 pytestmark = pytest.mark.gpu
 N_Q, N_KV, D = 28, 4, 128
@@ -124,6 +125,7 @@ def test_c3b_launch_shape_snapkv(cuda):
     _device_structure(plan, k, v, buf, N_KV, D)
     scale = 1 / math.sqrt(D)
     total_diff = total_rows = 0
+    max_rel = 0.0
     for gi in (0, 31, 63):
         t0, n, r0, kk = int(plan.tok_off[gi]), sizes[gi], int(plan.row_off[gi]), int(plan.keep[gi])
         qf, kf = (x[t0:t0 + n].float().cpu().numpy() for x in (q, k))
@@ -134,9 +136,14 @@ def test_c3b_launch_shape_snapkv(cuda):
         for h in range(N_KV):
             diff, allowed = _near_tie_mismatches(idx[:, h], want[h], kk, 1e-4)
             assert diff == allowed, f"group {gi} head {h}: {diff - allowed} index differences outside the tie band"
+            # the device's set is the top-k of its own scores, and differs from the oracle's only within 2 x the
+            # measured score error of this head (tests/tiecheck.py)
+            _, eps, _ = error_bounded_ties(idx[:, h], got[h], want[h], kk)
+            max_rel = max(max_rel, eps / float(np.max(np.abs(want[h]))))
             total_diff += diff
             total_rows += kk
-    print(f"C3b SnapKV: {total_diff} near-tie index differences over {total_rows} retained rows")
+    print(f"C3b SnapKV: {total_diff} near-tie index differences over {total_rows} retained rows, "
+          f"max score error {max_rel:.3g} of the head's largest score")
     assert total_diff <= 0.01 * total_rows
 
 
@@ -154,6 +161,7 @@ def test_c3_launch_shape_snapkv_layer(cuda, window, pool):
     _device_structure(plan, k, v, buf, N_KV, D)
     scale = 1 / math.sqrt(D)
     total_diff = total_rows = 0
+    max_rel = 0.0
     for gi in (0, 31, 63):
         t0, n, r0, kk = int(plan.tok_off[gi]), sizes[gi], int(plan.row_off[gi]), int(plan.keep[gi])
         qf, kf = (x[t0:t0 + n].float().cpu().numpy() for x in (q, k))
@@ -164,9 +172,14 @@ def test_c3_launch_shape_snapkv_layer(cuda, window, pool):
         for h in range(N_KV):
             diff, allowed = _near_tie_mismatches(idx[:, h], want[h], kk, 1e-4)
             assert diff == allowed, f"group {gi} head {h}: {diff - allowed} index differences outside the tie band"
+            # the device's set is the top-k of its own scores, and differs from the oracle's only within 2 x the
+            # measured score error of this head (tests/tiecheck.py)
+            _, eps, _ = error_bounded_ties(idx[:, h], got[h], want[h], kk)
+            max_rel = max(max_rel, eps / float(np.max(np.abs(want[h]))))
             total_diff += diff
             total_rows += kk
-    print(f"C3 SnapKV W={window} pool={pool}: {total_diff} near-tie index differences over {total_rows} rows")
+    print(f"C3 SnapKV W={window} pool={pool}: {total_diff} near-tie index differences over {total_rows} rows, "
+          f"max score error {max_rel:.3g} of the head's largest score")
     assert total_diff <= 0.01 * total_rows
 
 
