@@ -757,15 +757,17 @@ int launch_attention(cudaStream_t stream, const qvk_groups* g, const void* q, co
     prm.total_units = static_cast<int>(units);
     const int sms = grid_sms();
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(units, sms));
-    // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 2 | 4 | 6;
+    // Of every 16 exponential pairs, kPoly run on the FMA pipe (tuning knob QVK_ATTN_POLY = 0 | 1 | 2 | 3 | 4 | 6;
     // DESIGN.md §3.1): 2 and 4 are equal at boost clocks, 2 is ~0.5 % ahead inside the power-capped C4 step.
     static const int poly = [] {
         const int v = env_knob("QVK_ATTN_POLY", 2);
-        return (v == 0 || v == 4 || v == 6) ? v : 2;
+        return (v == 0 || v == 1 || v == 3 || v == 4 || v == 6) ? v : 2;
     }();
     if (d_h == 128) {
         switch (poly) {
             case 0: return launch_attention_d<128, 0>(stream, mq, mk, mv, mo, prm, grid);
+            case 1: return launch_attention_d<128, 1>(stream, mq, mk, mv, mo, prm, grid);
+            case 3: return launch_attention_d<128, 3>(stream, mq, mk, mv, mo, prm, grid);
             case 4: return launch_attention_d<128, 4>(stream, mq, mk, mv, mo, prm, grid);
             case 6: return launch_attention_d<128, 6>(stream, mq, mk, mv, mo, prm, grid);
             default: return launch_attention_d<128, 2>(stream, mq, mk, mv, mo, prm, grid);
